@@ -1,0 +1,119 @@
+/*
+ * kernid_cuda.h -- C-ABI of libkernid_cuda.so, the B200 (sm_100a) implementation of the
+ * far-field hot path of arXiv 1409.2802's reference (`kernid`, /root/reference/proj).
+ *
+ * The reference has no FFI layer: its hot path is the header-only C++ API in
+ * proj/include/kernid/*.hpp. Each entry point below replaces the
+ * device-side work of one reference function; the cited reference function is what a
+ * maintainer would re-point at this ABI (bindings in INTEGRATION.md).
+ *
+ * Conventions (mirroring the reference):
+ *   - matrices are column-major FP64 (Eigen default, kernel.hpp:14); indices int64
+ *     (Eigen::Index, geometry.hpp:23-24);
+ *   - no exceptions cross the boundary: every call returns a kid status code that maps
+ *     1:1 onto the reference exception taxonomy (errors.hpp:11-77), message via
+ *     kid_last_error();
+ *   - buffers passed to the plain entry points are HOST memory (caller-allocated);
+ *     the *_dev variants take device pointers, run asynchronously on the context stream
+ *     and are what bench.py times and what the multi-GPU host layer all-reduces;
+ *   - one context per device per host thread; a context is not re-entrant.
+ *   - the Gaussian kernel K(y, x) = exp(-||x - y||^2 / (2 h^2)) (kernel.hpp:77-79) is the
+ *     only family on this path (BASELINE.json north_star).
+ */
+#ifndef KERNID_CUDA_H
+#define KERNID_CUDA_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> reference exceptions (errors.hpp) */
+#define KID_OK 0
+#define KID_E_RANGE 1        /* RangeError */
+#define KID_E_DIM 2          /* DimensionError */
+#define KID_E_NO_TARGETS 3   /* NoTargetsError (geometry.hpp:61-63) */
+#define KID_E_NUMERICAL 4    /* NumericalError (lowrank.hpp:301-302) */
+#define KID_E_ERROR 5        /* Error (base class) */
+#define KID_E_CUDA 6         /* Error: CUDA runtime failure */
+#define KID_E_OOM 7          /* Error: device allocation failed */
+#define KID_E_ILLCOND 8      /* IllConditionedSkeletonError (lowrank.hpp:243-246) */
+#define KID_E_CONFIG 9       /* ConfigError (kernel.hpp:29-36, h <= 0) */
+
+/* kid_recon_error flags */
+#define KID_RECON_DTD 1u     /* accumulate the residual Gram D^T D (spectral norm, compress.hpp:141-154) */
+#define KID_RECON_KTK 2u     /* also accumulate K^T K in the same pass (matrix_norm, compress.hpp:156-159) */
+
+typedef struct kid_ctx kid_ctx;
+
+int kid_abi_version(void);
+/* Create a context on CUDA device `device` (one per process/GPU). */
+int kid_create(kid_ctx** out, int32_t device);
+void kid_destroy(kid_ctx* ctx);
+const char* kid_last_error(const kid_ctx* ctx);
+/* Run subsequent work on an external cudaStream_t (NULL: the context's own stream). */
+int kid_set_stream(kid_ctx* ctx, void* cuda_stream);
+int kid_synchronize(kid_ctx* ctx);
+
+/* ---- point set (PointSet, kernel.hpp:14): N x d column-major ----
+ * index_offset: global index of local row 0 when the point set is sharded across ranks. */
+int kid_set_points(kid_ctx* ctx, const double* host_pts, int64_t N, int32_t d, int64_t index_offset);
+/* Borrow an existing device buffer (no copy; must outlive its use). */
+int kid_set_points_device(kid_ctx* ctx, const double* dev_pts, int64_t N, int32_t d, int64_t index_offset);
+
+/* ---- pass 1: split_sources_targets (geometry.hpp:29-65) ----
+ * Exact (dist, idx) selection of the n nearest points to `center`, rho, and the stable
+ * compaction of targets {i not source : dist_i >= xi * rho} (ascending index). Distances are
+ * computed bit-exactly as the reference (sequential sum of squared differences, no FMA,
+ * correctly-rounded sqrt). Targets stay on the device; fetch them with kid_get_targets. */
+int kid_split(kid_ctx* ctx, const double* center, int64_t n, double xi, int64_t* src_idx_out,
+              double* rho_out, int64_t* n_targets_out);
+/* Sharded split, step 1: the local n smallest (dist, global idx) keys, ascending. */
+int kid_split_candidates(kid_ctx* ctx, const double* center, int64_t n, double* cand_dist,
+                         int64_t* cand_idx);
+/* Sharded split, step 2: given the global source set (ascending global indices) and rho,
+ * compact the local targets. Also fixes the source coordinates used by the FP64 passes
+ * (src_points: n x d column-major, host). */
+int kid_split_finish(kid_ctx* ctx, const int64_t* src_idx, int64_t n, const double* src_points,
+                     double rho, double xi, int64_t* n_targets_out);
+int kid_get_targets(kid_ctx* ctx, int64_t* tgt_idx_out, int64_t count);
+/* Explicit block K(T, S) (kernel_matrix(spec, targets, sources), kernel.hpp:202): targets
+ * nt x d and sources m x d, both column-major host arrays. Replaces the split's block. */
+int kid_set_block(kid_ctx* ctx, const double* targets, int64_t nt, const double* sources, int64_t m,
+                  int32_t d);
+int kid_block_shape(const kid_ctx* ctx, int64_t* nt, int64_t* m, int32_t* d);
+
+/* ---- pass 2a: EuclideanNorm weights w_i = ||K_i||_2 (sampling.hpp:189-196) ---- */
+int kid_row_norms(kid_ctx* ctx, double h, double* w_out);
+int kid_row_norms_dev(kid_ctx* ctx, double h, double* d_w);
+
+/* ---- pass 2b: Gram K^T K (m x m col-major) for the right factor / spectrum of K
+ * (lowrank.hpp:56-90, replaced by the Gram route) and ||K||_F^2 ---- */
+int kid_gram(kid_ctx* ctx, double h, double* G_out, double* sumsq_K_out);
+int kid_gram_dev(kid_ctx* ctx, double h, double* d_G, double* d_sumsq);
+
+/* ---- pass 2b': leverage scores l_i = ||K_i W||^2, W = V_r Sigma_r^-1 (m x r col-major),
+ * lowrank.hpp:304-305 ---- */
+int kid_leverage(kid_ctx* ctx, double h, const double* W, int64_t r, double* scores_out);
+int kid_leverage_dev(kid_ctx* ctx, double h, const double* d_W, int64_t r, double* d_scores);
+
+/* ---- pass 3: fused reconstruction-error pass (compress.hpp:141-159, 199-206) ----
+ * D = K - K[:, skel] P (never materialised). Outputs ||D||_F^2, ||K||_F^2 and, per flags,
+ * D^T D and K^T K (m x m col-major; rows/cols of skeleton columns of D^T D are exactly 0). */
+int kid_recon_error(kid_ctx* ctx, double h, const int64_t* skel, int64_t r, const double* P,
+                    uint32_t flags, double* sumsq_D, double* sumsq_K, double* DtD, double* KtK);
+/* device variant: d_out receives [sumsq_D, sumsq_K, DtD (m*m), KtK (m*m if flag)] */
+int kid_recon_prepare(kid_ctx* ctx, const int64_t* skel, int64_t r, const double* P);
+int kid_recon_error_dev(kid_ctx* ctx, double h, uint32_t flags, double* d_out);
+
+/* ---- gather_rows of K on the device (compress.hpp:130-137): Ks (count x m col-major) ---- */
+int kid_eval_rows(kid_ctx* ctx, double h, const int64_t* rows, int64_t count, double* Ks_out);
+
+/* ---- instrumentation: number of kernels this context launched, last kernel's name ---- */
+int64_t kid_launch_count(const kid_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

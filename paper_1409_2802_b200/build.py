@@ -1,0 +1,64 @@
+"""Builds the native libraries in-tree (they travel to the GPU box with the repo snapshot).
+
+  libkernid_cuda.so  -- sm_100a kernels + the C-ABI of include/kernid_cuda.h (nvcc)
+  libkernid_host.so  -- the host-side C++ mirror of the reference `kernid::` API
+                        (include/kernid_b200.hpp) over the C-ABI (g++, -ffp-contract=off)
+"""
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+HOST = os.path.join(PKG, "host")
+CUDA_SO = os.path.join(PKG, "libkernid_cuda.so")
+HOST_SO = os.path.join(PKG, "libkernid_host.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CU_SRCS = ["kid_capi.cu", "kid_split.cu", "kid_passes.cu"]
+HOST_SRCS = ["kernid_host.cpp"]
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(p) > t for p in deps)
+
+
+def build_cuda(force=False, verbose=False):
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "kernid_cuda.h")]
+    if not force and not _stale(CUDA_SO, deps):
+        return CUDA_SO
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+           "-Xptxas", "-warn-spills", "-o", CUDA_SO] + [os.path.join(CSRC, f) for f in CU_SRCS]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    return CUDA_SO
+
+
+def build_host(force=False, verbose=False):
+    if not os.path.isdir(HOST):
+        return None
+    deps = [os.path.join(HOST, f) for f in os.listdir(HOST)] + [os.path.join(ROOT, "include", f)
+                                                                for f in os.listdir(os.path.join(ROOT, "include"))]
+    if not force and not _stale(HOST_SO, deps):
+        return HOST_SO
+    cmd = ["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-ffp-contract=off", "-Wall",
+           "-I", os.path.join(ROOT, "include"), "-o", HOST_SO] + [os.path.join(HOST, f) for f in HOST_SRCS] + \
+          ["-ldl", "-lpthread"]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    return HOST_SO
+
+
+def build_all(force=False, verbose=False):
+    build_cuda(force, verbose)
+    build_host(force, verbose)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, verbose=True)

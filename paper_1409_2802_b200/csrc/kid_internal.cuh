@@ -1,0 +1,144 @@
+// kid_internal.cuh -- shared device helpers and the context of libkernid_cuda.so.
+//
+// Layout in HBM:
+//   points   N x d column-major FP64 (Eigen PointSet, kernel.hpp:14): coordinate k of
+//            point i at pts[i + k*N]; every pass reads a coordinate column coalesced;
+//   dist     N FP64, the bit-exact ||p_i - c|| of pass 1 (geometry.hpp:36-37);
+//   tgt_idx  N_T int64 local indices of the targets, ascending (geometry.hpp:58-60);
+//   sources  m x d column-major (gathered once per split); the FP64 passes stage them
+//            in shared memory, permuted [skeleton | non-skeleton] for pass 3.
+// K itself is never stored: every FP64 pass re-evaluates its target tile in registers
+// / shared memory (SURVEY.md 8a A5 "never materialised on GPU").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/kernid_cuda.h"
+
+namespace kid {
+
+// ---------------------------------------------------------------- device math
+
+// Sequential squared distance with no FMA contraction (kernel.hpp:60-68): acc starts
+// at 0.0, acc += (a_k - b_k)^2 in k order; __d*_rn keep nvcc from fusing.
+__device__ __forceinline__ double sqdist_exact(const double* a, int64_t sa, const double* b,
+                                               int64_t sb, int d) {
+  double acc = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double diff = __dsub_rn(a[k * sa], b[k * sb]);
+    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+  }
+  return acc;
+}
+
+// Gaussian entry exp(-sq / (2 h^2)) with the reference's argument rounding
+// (kernel.hpp:77-79: -sq / (2.0*h*h), denom = (2.0*h)*h computed on the host).
+__device__ __forceinline__ double gauss_exact(double sq, double denom) {
+  return exp(__ddiv_rn(-sq, denom));
+}
+
+// FP64 tensor-core MMA (SASS DMMA.8x8x4): C[8x8] += A[8x4] * B[4x8].
+// Fragments: A[row = lane>>2][k = lane&3], B[k = lane&3][col = lane>>2],
+// C[row = lane>>2][col = 2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace kid
+
+// ---------------------------------------------------------------- context
+struct kid_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  // point set
+  const double* pts = nullptr;  // device, N x d col-major (owned or borrowed)
+  double* pts_own = nullptr;
+  size_t pts_own_cap = 0;
+  int64_t N = 0;
+  int32_t d = 0;
+  int64_t offset = 0;
+
+  // split state
+  double* dist = nullptr;
+  size_t dist_cap = 0;
+  int64_t* tgt_idx = nullptr;
+  size_t tgt_cap = 0;
+  int64_t n_split_targets = 0;
+
+  // current block K(T, S)
+  const double* tbase = nullptr;  // target coordinate base (points or explicit targets)
+  int64_t tld = 0;                // leading dimension of tbase
+  const int64_t* tidx = nullptr;  // nullptr: identity
+  int64_t nt = 0;
+  double* blk_tgt = nullptr;  // owned explicit targets
+  size_t blk_tgt_cap = 0;
+  double* src = nullptr;  // m x d col-major
+  size_t src_cap = 0;
+  int64_t m = 0;
+
+  // pass-3 operands (kid_recon_prepare)
+  int64_t r = 0;
+  double* src_perm = nullptr;  // m x d, columns [skel | non-skel]
+  size_t src_perm_cap = 0;
+  double* P2 = nullptr;        // r x meff row-major, stride = r-major padded
+  size_t P2_cap = 0;
+  std::vector<int64_t> nonskel;  // host: original column of each non-skeleton column
+  std::vector<int64_t> skel_h;
+
+  // scratch
+  void* scratch = nullptr;
+  size_t scratch_cap = 0;
+  double* partial = nullptr;
+  size_t partial_cap = 0;
+  double* hbuf = nullptr;  // pinned host staging
+  size_t hbuf_cap = 0;
+  int64_t* counter = nullptr;  // device counters [8]
+};
+
+namespace kid {
+
+int fail(kid_ctx* c, int code, const std::string& msg);
+int cuda_fail(kid_ctx* c, cudaError_t e, const char* where);
+int ensure(kid_ctx* c, void** p, size_t* cap, size_t bytes);
+int ensure_pinned(kid_ctx* c, size_t bytes);
+void* scratch(kid_ctx* c, size_t bytes);
+
+#define KID_CK(ctx, call)                                       \
+  do {                                                          \
+    cudaError_t e_ = (call);                                    \
+    if (e_ != cudaSuccess) return ::kid::cuda_fail(ctx, e_, #call); \
+  } while (0)
+#define KID_LAUNCHED(ctx)                                              \
+  do {                                                                 \
+    (ctx)->launches++;                                                 \
+    cudaError_t e_ = cudaGetLastError();                               \
+    if (e_ != cudaSuccess) return ::kid::cuda_fail(ctx, e_, "launch"); \
+  } while (0)
+
+// pass entry points (kid_split.cu / kid_passes.cu)
+int split_candidates(kid_ctx* c, const double* center_h, int64_t n, double* cand_dist_h,
+                     int64_t* cand_idx_h);
+int split_finish(kid_ctx* c, const int64_t* src_idx_h, int64_t n, const double* src_pts_h, double rho,
+                 double xi, int64_t* n_targets_out);
+int row_norms_dev(kid_ctx* c, double h, double* d_w);
+int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out);
+int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores);
+int eval_rows_dev(kid_ctx* c, double h, const int64_t* d_rows, int64_t count, double* d_Ks);
+
+}  // namespace kid

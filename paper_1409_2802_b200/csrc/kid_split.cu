@@ -1,0 +1,390 @@
+// kid_split.cu -- pass 1: the well-separatedness filter (split_sources_targets,
+// /root/reference/proj/include/kernid/geometry.hpp:29-65) as HBM-streaming kernels.
+//
+//   (a) sample bound: exact distances of a strided sample of S points; the n-th smallest
+//       sample key T bounds the global n-th smallest key from above (any n points at
+//       distance <= T prove it), so only keys <= T can be sources;
+//   (b) k_dist_cand: one coalesced pass over the N x d coordinates computing the bit-exact
+//       distance (sequential sum of squared differences, no FMA, correctly-rounded sqrt;
+//       geometry.hpp:36-37), storing it, and appending (key, idx) when key <= T;
+//   (c) candidates sorted by (dist, idx) (two stable radix sorts) -> the exact source set of
+//       nth_element with the (dist, idx) comparator (geometry.hpp:39-45);
+//   (d) k_compact: single-pass decoupled look-back stable compaction of
+//       {i not source : dist_i >= xi * rho} in ascending index (geometry.hpp:55-60).
+// Non-negative doubles order like their bit patterns, so keys are the raw dist bits.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "kid_internal.cuh"
+
+namespace kid {
+namespace {
+
+constexpr int kSampleMax = 65536;
+
+__device__ __forceinline__ double point_dist(const double* __restrict__ pts, int64_t N, int d,
+                                             int64_t i, const double* __restrict__ c) {
+  double diff = __dsub_rn(pts[i], c[0]);
+  double acc = __dmul_rn(diff, diff);
+  for (int k = 1; k < d; ++k) {
+    diff = __dsub_rn(pts[i + k * N], c[k]);
+    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+  }
+  return __dsqrt_rn(acc);
+}
+
+__global__ void k_sample_keys(const double* __restrict__ pts, int64_t N, int d,
+                              const double* __restrict__ center, int64_t S,
+                              unsigned long long* __restrict__ keys) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const int64_t i = (S == N) ? j : (int64_t)(((__int128)j * N) / S);
+  keys[j] = (unsigned long long)__double_as_longlong(point_dist(pts, N, d, i, center));
+}
+
+// (b): one thread per point, grid-stride; warp-aggregated append of candidates.
+__global__ void __launch_bounds__(256) k_dist_cand(const double* __restrict__ pts, int64_t N, int d,
+                                                   const double* __restrict__ center,
+                                                   const unsigned long long* __restrict__ T_key,
+                                                   double* __restrict__ dist,
+                                                   unsigned long long* __restrict__ cand_key,
+                                                   unsigned long long* __restrict__ cand_idx,
+                                                   unsigned long long* __restrict__ cand_count,
+                                                   int64_t cap) {
+  __shared__ double c_s[64];
+  if (threadIdx.x < d) c_s[threadIdx.x] = center[threadIdx.x];
+  __syncthreads();
+  const unsigned long long T = *T_key;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < N; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool cand = false;
+    unsigned long long key = 0;
+    if (i < N) {
+      double diff = __dsub_rn(pts[i], c_s[0]);
+      double acc = __dmul_rn(diff, diff);
+      for (int k = 1; k < d; ++k) {
+        diff = __dsub_rn(pts[i + k * N], c_s[k]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+      }
+      const double v = __dsqrt_rn(acc);
+      dist[i] = v;
+      key = (unsigned long long)__double_as_longlong(v);
+      cand = key <= T;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, cand);
+    if (mask) {
+      unsigned long long pos0 = 0;
+      if (lane == 0) pos0 = atomicAdd(cand_count, (unsigned long long)__popc(mask));
+      pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+      if (cand) {
+        const unsigned long long pos = pos0 + __popc(mask & ((1u << lane) - 1u));
+        if ((int64_t)pos < cap) {
+          cand_key[pos] = key;
+          cand_idx[pos] = (unsigned long long)i;
+        }
+      }
+    }
+  }
+}
+
+// overflow path: re-collect candidates from the stored distances (no recompute)
+__global__ void k_cand_from_dist(const double* __restrict__ dist, int64_t N,
+                                 const unsigned long long* __restrict__ T_key,
+                                 unsigned long long* __restrict__ cand_key,
+                                 unsigned long long* __restrict__ cand_idx,
+                                 unsigned long long* __restrict__ cand_count) {
+  const unsigned long long T = *T_key;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < N; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    unsigned long long key = 0;
+    bool cand = false;
+    if (i < N) {
+      key = (unsigned long long)__double_as_longlong(dist[i]);
+      cand = key <= T;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, cand);
+    if (mask) {
+      unsigned long long pos0 = 0;
+      if (lane == 0) pos0 = atomicAdd(cand_count, (unsigned long long)__popc(mask));
+      pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+      if (cand) {
+        const unsigned long long pos = pos0 + __popc(mask & ((1u << lane) - 1u));
+        cand_key[pos] = key;
+        cand_idx[pos] = (unsigned long long)i;
+      }
+    }
+  }
+}
+
+__global__ void k_gather_sources(const double* __restrict__ pts, int64_t N, int d,
+                                 const int64_t* __restrict__ src_local, int64_t n,
+                                 double* __restrict__ src) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  for (int k = 0; k < d; ++k) src[j + k * n] = pts[src_local[j] + k * N];
+}
+
+// (d) decoupled look-back stable compaction ------------------------------------
+constexpr int kCT = 256, kIPT = 8, kTile = kCT * kIPT;
+constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ bool is_source(const int64_t* __restrict__ s, int64_t n, int64_t i) {
+  int64_t lo = 0, hi = n;  // lower_bound over the ascending local source list
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (s[mid] < i) lo = mid + 1; else hi = mid;
+  }
+  return lo < n && s[lo] == i;
+}
+
+__global__ void __launch_bounds__(kCT) k_compact(const double* __restrict__ dist, int64_t N, double cutoff,
+                                                 double rho, const int64_t* __restrict__ src_local,
+                                                 int64_t n_src, int64_t* __restrict__ out,
+                                                 unsigned long long* __restrict__ tile_status,
+                                                 unsigned int* __restrict__ tile_counter,
+                                                 int64_t* __restrict__ total_out, int64_t ntiles) {
+  __shared__ unsigned int tile_s;
+  __shared__ long long warp_tot[kCT / 32];
+  __shared__ long long excl_s;
+  if (threadIdx.x == 0) tile_s = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const int64_t tile = tile_s;
+  const int64_t base = tile * kTile + (int64_t)threadIdx.x * kIPT;
+  unsigned flags = 0;
+  int cnt = 0;
+  if (base + kIPT <= N) {
+    const double2* p2 = reinterpret_cast<const double2*>(dist + base);
+#pragma unroll
+    for (int j = 0; j < kIPT / 2; ++j) {
+      const double2 v = __ldcs(p2 + j);
+      bool f0 = v.x >= cutoff, f1 = v.y >= cutoff;
+      if (f0 && v.x <= rho) f0 = !is_source(src_local, n_src, base + 2 * j);
+      if (f1 && v.y <= rho) f1 = !is_source(src_local, n_src, base + 2 * j + 1);
+      flags |= (unsigned)f0 << (2 * j);
+      flags |= (unsigned)f1 << (2 * j + 1);
+    }
+  } else {
+    for (int j = 0; j < kIPT; ++j) {
+      const int64_t i = base + j;
+      if (i < N) {
+        const double v = dist[i];
+        bool f = v >= cutoff;
+        if (f && v <= rho) f = !is_source(src_local, n_src, i);
+        flags |= (unsigned)f << j;
+      }
+    }
+  }
+  cnt = __popc(flags);
+  // block-wide exclusive scan of cnt
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long run = 0;
+    for (int w = 0; w < kCT / 32; ++w) {
+      const long long t = warp_tot[w];
+      warp_tot[w] = run;
+      run += t;
+    }
+    const long long total = run;
+    long long excl = 0;
+    if (tile == 0) {
+      __threadfence();
+      atomicExch(&tile_status[0], kStInc | (unsigned long long)total);
+    } else {
+      __threadfence();
+      atomicExch(&tile_status[tile], kStAgg | (unsigned long long)total);
+      int64_t p = tile - 1;
+      for (;;) {
+        const unsigned long long s = *((volatile unsigned long long*)&tile_status[p]);
+        const unsigned long long st = s & ~kValMask;
+        if (st == 0) continue;
+        excl += (long long)(s & kValMask);
+        if (st == kStInc) break;
+        --p;
+      }
+      __threadfence();
+      atomicExch(&tile_status[tile], kStInc | (unsigned long long)(excl + total));
+    }
+    excl_s = excl;
+    if (tile == ntiles - 1) *total_out = excl + total;
+  }
+  __syncthreads();
+  int64_t pos = excl_s + warp_tot[warp] + (incl - cnt);
+  while (flags) {
+    const int j = __ffs(flags) - 1;
+    flags &= flags - 1;
+    out[pos++] = base + j;
+  }
+}
+
+int sort_candidates(kid_ctx* c, unsigned long long* key, unsigned long long* idx, int64_t count,
+                    unsigned long long* key_alt, unsigned long long* idx_alt, int end_bit_idx) {
+  // stable LSD order: by idx first, then stably by key -> (dist, idx) lexicographic
+  size_t tmp1 = 0, tmp2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp1, idx, idx_alt, key, key_alt, (int)count, 0, end_bit_idx, c->stream);
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp2, key_alt, key, idx_alt, idx, (int)count, 0, 64, c->stream);
+  void* tmp = nullptr;
+  size_t cap = 0;
+  const size_t need = std::max(tmp1, tmp2);
+  if (ensure(c, &tmp, &cap, need)) return KID_E_OOM;
+  KID_CK(c, cub::DeviceRadixSort::SortPairs(tmp, tmp1, idx, idx_alt, key, key_alt, (int)count, 0, end_bit_idx, c->stream));
+  c->launches += 2;
+  KID_CK(c, cub::DeviceRadixSort::SortPairs(tmp, tmp2, key_alt, key, idx_alt, idx, (int)count, 0, 64, c->stream));
+  c->launches += 2;
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  cudaFree(tmp);
+  return KID_OK;
+}
+
+}  // namespace
+
+// Local n smallest (dist, idx) keys, ascending; indices are GLOBAL (offset added).
+int split_candidates(kid_ctx* c, const double* center_h, int64_t n, double* cand_dist_h,
+                     int64_t* cand_idx_h) {
+  const int64_t N = c->N;
+  const int d = c->d;
+  if (!c->pts || N < 1) return fail(c, KID_E_ERROR, "kid_split: no point set");
+  if (d > 64) return fail(c, KID_E_DIM, "kid_split: d > 64 unsupported");
+  const int64_t nl = std::min<int64_t>(n, N);  // a shard may hold fewer than n points
+  if (ensure(c, (void**)&c->dist, &c->dist_cap, sizeof(double) * N)) return KID_E_OOM;
+
+  // scratch layout: center | T_key | count | sample keys (2x) | candidates
+  const int64_t S = N <= std::max<int64_t>(kSampleMax, 4 * nl) ? N : std::max<int64_t>(kSampleMax, 4 * nl);
+  int64_t cap = std::max<int64_t>(4 * nl + 1024, (int64_t)((double)N * (double)nl / (double)S * 2.0) + 4096);
+  cap = std::min<int64_t>(cap, N);
+  const size_t bytes = 64 * 8 + 16 + 16 + 2 * sizeof(unsigned long long) * S + 4 * sizeof(unsigned long long) * cap;
+  char* base = (char*)scratch(c, bytes);
+  if (!base) return KID_E_OOM;
+  double* center = (double*)base;
+  unsigned long long* T_key = (unsigned long long*)(base + 512);
+  unsigned long long* count = (unsigned long long*)(base + 512 + 16);
+  unsigned long long* skeys = (unsigned long long*)(base + 512 + 32);
+  unsigned long long* skeys2 = skeys + S;
+  unsigned long long* ck = skeys2 + S;
+  unsigned long long* ci = ck + cap;
+  unsigned long long* ck2 = ci + cap;
+  unsigned long long* ci2 = ck2 + cap;
+
+  KID_CK(c, cudaMemcpyAsync(center, center_h, sizeof(double) * d, cudaMemcpyHostToDevice, c->stream));
+  KID_CK(c, cudaMemsetAsync(count, 0, sizeof(unsigned long long), c->stream));
+  k_sample_keys<<<(unsigned)((S + 255) / 256), 256, 0, c->stream>>>(c->pts, N, d, center, S, skeys);
+  KID_LAUNCHED(c);
+  {
+    size_t tmpb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tmpb, skeys, skeys2, (int)S, 0, 64, c->stream);
+    void* tmp = nullptr;
+    size_t tcap = 0;
+    if (ensure(c, &tmp, &tcap, tmpb)) return KID_E_OOM;
+    KID_CK(c, cub::DeviceRadixSort::SortKeys(tmp, tmpb, skeys, skeys2, (int)S, 0, 64, c->stream));
+    c->launches += 4;
+    KID_CK(c, cudaMemcpyAsync(T_key, skeys2 + (nl - 1), sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                              c->stream));
+    KID_CK(c, cudaStreamSynchronize(c->stream));
+    cudaFree(tmp);
+  }
+  const int blocks = c->sms * 8;
+  k_dist_cand<<<blocks, 256, 0, c->stream>>>(c->pts, N, d, center, T_key, c->dist, ck, ci, count, cap);
+  KID_LAUNCHED(c);
+  unsigned long long cnt = 0;
+  KID_CK(c, cudaMemcpyAsync(&cnt, count, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  if ((int64_t)cnt > cap) {  // loose bound (adversarial ordering): recollect into a larger buffer
+    const int64_t big = (int64_t)cnt;
+    unsigned long long* buf = nullptr;
+    KID_CK(c, cudaMalloc(&buf, 4 * sizeof(unsigned long long) * big));
+    ck = buf; ci = ck + big; ck2 = ci + big; ci2 = ck2 + big;
+    KID_CK(c, cudaMemsetAsync(count, 0, sizeof(unsigned long long), c->stream));
+    k_cand_from_dist<<<blocks, 256, 0, c->stream>>>(c->dist, N, T_key, ck, ci, count);
+    KID_LAUNCHED(c);
+    int end_bit = 1;
+    while (end_bit < 63 && (1ll << end_bit) < N) ++end_bit;
+    int rc = sort_candidates(c, ck, ci, big, ck2, ci2, end_bit);
+    if (!rc) {
+      std::vector<unsigned long long> hk(nl), hi(nl);
+      KID_CK(c, cudaMemcpy(hk.data(), ck, sizeof(unsigned long long) * nl, cudaMemcpyDeviceToHost));
+      KID_CK(c, cudaMemcpy(hi.data(), ci, sizeof(unsigned long long) * nl, cudaMemcpyDeviceToHost));
+      for (int64_t k = 0; k < nl; ++k) {
+        std::memcpy(&cand_dist_h[k], &hk[k], 8);
+        cand_idx_h[k] = (int64_t)hi[k] + c->offset;
+      }
+    }
+    cudaFree(buf);
+    return rc;
+  }
+  int end_bit = 1;
+  while (end_bit < 63 && (1ll << end_bit) < N) ++end_bit;
+  int rc = sort_candidates(c, ck, ci, (int64_t)cnt, ck2, ci2, end_bit);
+  if (rc) return rc;
+  std::vector<unsigned long long> hk(nl), hi(nl);
+  KID_CK(c, cudaMemcpyAsync(hk.data(), ck, sizeof(unsigned long long) * nl, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaMemcpyAsync(hi.data(), ci, sizeof(unsigned long long) * nl, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  for (int64_t k = 0; k < nl; ++k) {
+    std::memcpy(&cand_dist_h[k], &hk[k], 8);
+    cand_idx_h[k] = (int64_t)hi[k] + c->offset;
+  }
+  return KID_OK;
+}
+
+// Given the global source set (ascending GLOBAL indices) and rho, compact the local targets.
+// src_pts_h (n x d col-major host) may be null when every source is local.
+int split_finish(kid_ctx* c, const int64_t* src_idx_h, int64_t n, const double* src_pts_h, double rho,
+                 double xi, int64_t* n_targets_out) {
+  const int64_t N = c->N;
+  const int d = c->d;
+  std::vector<int64_t> local;
+  local.reserve(n);
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t li = src_idx_h[k] - c->offset;
+    if (li >= 0 && li < N) local.push_back(li);
+  }
+  const int64_t nloc = (int64_t)local.size();
+  const int64_t ntiles = (N + kTile - 1) / kTile;
+  const size_t bytes = sizeof(int64_t) * (nloc + n + 8) + sizeof(unsigned long long) * (ntiles + 8);
+  char* base = (char*)scratch(c, bytes);
+  if (!base) return KID_E_OOM;
+  int64_t* src_local = (int64_t*)base;
+  int64_t* src_all_local = src_local + nloc;  // gather list when all sources are local
+  unsigned long long* status = (unsigned long long*)(src_all_local + n + 8);
+  if (ensure(c, (void**)&c->tgt_idx, &c->tgt_cap, sizeof(int64_t) * N)) return KID_E_OOM;
+  if (ensure(c, (void**)&c->src, &c->src_cap, sizeof(double) * n * d)) return KID_E_OOM;
+  if (nloc) KID_CK(c, cudaMemcpyAsync(src_local, local.data(), sizeof(int64_t) * nloc, cudaMemcpyHostToDevice, c->stream));
+  if (src_pts_h) {
+    KID_CK(c, cudaMemcpyAsync(c->src, src_pts_h, sizeof(double) * n * d, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    if (nloc != n) return fail(c, KID_E_ERROR, "kid_split_finish: non-local sources need src_points");
+    k_gather_sources<<<(unsigned)((n + 127) / 128), 128, 0, c->stream>>>(c->pts, N, d, src_local, n, c->src);
+    KID_LAUNCHED(c);
+  }
+  KID_CK(c, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ntiles, c->stream));
+  KID_CK(c, cudaMemsetAsync(c->counter, 0, sizeof(int64_t) * 2, c->stream));
+  const double cutoff = xi * rho;  // geometry.hpp:57
+  k_compact<<<(unsigned)ntiles, kCT, 0, c->stream>>>(c->dist, N, cutoff, rho, src_local, nloc, c->tgt_idx, status,
+                                                     (unsigned int*)c->counter, c->counter + 1, ntiles);
+  KID_LAUNCHED(c);
+  int64_t nt = 0;
+  KID_CK(c, cudaMemcpyAsync(&nt, c->counter + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  c->n_split_targets = nt;
+  c->tbase = c->pts;
+  c->tld = N;
+  c->tidx = c->tgt_idx;
+  c->nt = nt;
+  c->m = n;
+  c->r = 0;
+  *n_targets_out = nt;
+  return KID_OK;
+}
+
+}  // namespace kid

@@ -1,0 +1,141 @@
+"""GPU parity of the C-ABI (libkernid_cuda.so) against the CPU oracle.
+
+Bars: split (sources, rho bits, targets) bit-exact; per-entry
+passes (row norms, gathered rows) within 1e-12 relative (CUDA exp vs glibc exp differ
+by <= 2 ulp); Grams |dG_jk| <= 1e-10 sqrt(G_jj G_kk) (hard part 2);
+leverage within 1e-10 of the oracle; rel_error within 1e-10 relative (the
+tolerance-ladder floor applies where D is rounding noise).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_1409_2802_b200._lib import Device
+    d = Device(0)
+    yield d
+    d.close()
+
+
+def _trial(O, d, N, n, xi, seed=1, trial=0, scheme=0, h_value=1.0):
+    data_seed = O.derive_seed(seed, trial, scheme)
+    return O.prepare_trial(d, N, n, xi, data_seed, h_value)
+
+
+@pytest.mark.parametrize("d,N,n,xi", [(2, 100_000, 100, 2.0), (1, 20_000, 100, 2.0), (3, 200_000, 100, 2.0),
+                                      (5, 50_000, 100, 3.0), (8, 300_000, 512, 2.0), (16, 30_000, 256, 2.0),
+                                      (3, 2_000, 40, 0.0), (4, 70_000, 1000, 1.0)])
+def test_split_bit_exact(oracle, dev, d, N, n, xi):
+    t = _trial(oracle, d, N, n, xi)
+    dev.set_points(t.points)
+    src, rho, nt = dev.split(t.center, n, xi)
+    assert np.array_equal(src, t.split.source_indices)
+    assert rho == t.split.rho  # bitwise (same double)
+    assert nt == t.split.target_indices.size
+    assert np.array_equal(dev.targets(), t.split.target_indices)
+
+
+def test_split_ties_and_errors(oracle, dev):
+    from paper_1409_2802_b200._lib import KidError, KID_E_NO_TARGETS, KID_E_RANGE, KID_E_DIM
+    ps = np.array([[1.0], [-1.0], [1.0], [-1.0], [1.0], [5.0]])
+    dev.set_points(ps)
+    src, rho, nt = dev.split([0.0], 3, 1.0)
+    ref = oracle.split_sources_targets(ps, [0.0], 3, 1.0)
+    assert np.array_equal(src, ref.source_indices) and rho == ref.rho
+    assert np.array_equal(dev.targets(), ref.target_indices)
+    line = np.array([[0.0], [0.1], [-0.1], [0.5], [-0.5], [2.0], [-2.0], [3.0]])
+    dev.set_points(line)
+    src, rho, nt = dev.split([0.0], 3, 2.0)
+    assert list(src) == [0, 1, 2] and list(dev.targets()) == [3, 4, 5, 6, 7]
+    for args, code in ((([0.0], 3, 100.0), KID_E_NO_TARGETS), (([0.0], 0, 1.0), KID_E_RANGE),
+                       (([0.0], 8, 1.0), KID_E_RANGE), (([0.0, 0.0], 3, 1.0), KID_E_DIM)):
+        with pytest.raises(KidError) as e:
+            dev.split(*args)
+        assert e.value.code == code
+
+
+def _block(oracle, d=3, N=20_000, n=100, xi=2.0, h_value=1.0):
+    t = _trial(oracle, d, N, n, xi, h_value=h_value)
+    K = oracle.kernel_matrix(t.targets, t.sources, t.h)
+    return t, K
+
+
+@pytest.mark.parametrize("d", [2, 3, 5])
+def test_row_norms_and_rows(oracle, dev, d):
+    t, K = _block(oracle, d=d)
+    dev.set_points(t.points)
+    dev.split(t.center, 100, 2.0)
+    w = dev.row_norms(t.h)
+    ref = oracle.row_norms(K)
+    nz = ref > 0
+    assert np.all(np.abs(w[nz] - ref[nz]) <= 1e-12 * ref[nz])
+    assert np.all(w[~nz] == 0.0)
+    rows = np.array([0, 5, 17, K.shape[0] - 1])
+    Ks = dev.eval_rows(t.h, rows)
+    assert np.allclose(Ks, K[rows], rtol=1e-12, atol=0)
+
+
+def _gram_ok(G, ref, tol=1e-10):
+    dg = np.sqrt(np.abs(np.diag(ref)))
+    bound = tol * np.outer(dg, dg) + 1e-300
+    return np.all(np.abs(G - ref) <= bound)
+
+
+@pytest.mark.parametrize("d,n", [(2, 100), (3, 100), (4, 37), (8, 64)])
+def test_gram(oracle, dev, d, n):
+    t, K = _block(oracle, d=d, n=n)
+    dev.set_points(t.points)
+    dev.split(t.center, n, 2.0)
+    G, sk = dev.gram(t.h)
+    ref = K.T @ K
+    assert _gram_ok(G, ref)
+    assert sk == pytest.approx(np.sum(K * K), rel=1e-12)
+    assert np.array_equal(G, G.T)
+
+
+@pytest.mark.parametrize("d,eps", [(2, 1e-2), (2, 1e-8), (3, 1e-8), (4, 1e-4)])
+def test_recon_error_vs_oracle(oracle, dev, d, eps):
+    t, K = _block(oracle, d=d)
+    nt = K.shape[0]
+    rows = oracle.sample_rows(oracle.SCHEME_UNIFORM, nt, 0.02, oracle.derive_seed(7, 0, 1))
+    res = oracle.compress_id(K, rows, eps=eps)
+    dev.set_points(t.points)
+    dev.split(t.center, 100, 2.0)
+    sd, sk, DtD, _ = dev.recon_error(t.h, res.skeleton, res.P)
+    r_sd, r_sk, r_DtD, r_KtK = oracle.residual_stats(K, res.skeleton, res.P)
+    assert sk == pytest.approx(r_sk, rel=1e-12)
+    assert sd == pytest.approx(r_sd, rel=1e-9)
+    assert _gram_ok(DtD, r_DtD, 1e-9)
+    # spectral relative error: sqrt(lmax(D^T D) / lmax(K^T K)) vs the oracle's exact SVD path
+    G, _ = dev.gram(t.h)
+    rel = math.sqrt(np.linalg.eigvalsh(DtD)[-1] / np.linalg.eigvalsh(G)[-1])
+    floor = 10 * math.sqrt(res.rank) * 2.2e-16 * np.abs(res.P).max() * math.sqrt(r_sk) / math.sqrt(np.linalg.eigvalsh(r_KtK)[-1])
+    assert abs(rel - res.rel_error) <= max(1e-10 * res.rel_error, floor)
+
+
+def test_leverage(oracle, dev):
+    t, K = _block(oracle, d=3)
+    dev.set_points(t.points)
+    dev.split(t.center, 100, 2.0)
+    for r in (5, 20):
+        sv, V = oracle.right_factor(K)
+        W = V[:, :r] / sv[:r]
+        ref, _ = oracle.row_leverage_scores(K, r)
+        got = dev.leverage(t.h, W)
+        assert np.max(np.abs(got - ref)) <= 1e-10 * max(1.0, ref.max())
+        assert got.sum() == pytest.approx(r, rel=1e-8)
+
+
+def test_explicit_block(oracle, dev):
+    tg = oracle.gen_normal(5, 333, 11) + 4.0
+    sr = oracle.gen_normal(5, 21, 12)
+    dev.set_block(tg, sr)
+    K = oracle.kernel_matrix(tg, sr, 0.9)
+    assert np.allclose(dev.row_norms(0.9), oracle.row_norms(K), rtol=1e-12, atol=0)
+    G, _ = dev.gram(0.9)
+    assert _gram_ok(G, K.T @ K)
