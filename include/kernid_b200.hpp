@@ -1,0 +1,236 @@
+// kernid_b200.hpp -- host C++ mirror of the reference `kernid::` API for the far-field hot
+// path, running the O(N_T * m) work on the B200 through the C-ABI of kernid_cuda.h.
+//
+// Same names, argument meaning and error behaviour as /root/reference/proj/include/kernid/
+// (namespace kernid_b200 instead of kernid). What changes:
+//   * the dense Eigen::MatrixXd K of kernel_matrix() (kernel.hpp:202-208) is replaced by a
+//     KernelBlock: the device-resident K(T, S) of the last split, never materialised;
+//   * sample_rows / row_leverage_scores / compress_id take that block (SampleContext::K);
+//   * spectral norms come from the residual Gram D^T D accumulated on the device (one pass,
+//     exact up to rounding) instead of QR+SVD of a materialised difference or power
+//     iteration (compress.hpp:141-159) -- NormPolicy is accepted for API parity;
+//   * the tiny host steps stay on the host as in the reference: K_s rows evaluated with the
+//     reference arithmetic (glibc exp, no FMA) so the ID skeleton is bit-identical, CPQR/ID,
+//     epsilon-rank, weighted draws.
+#pragma once
+#include <cstdint>
+#include <optional>
+#include <ostream>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kernid_cuda.h"
+
+namespace kernid_b200 {
+
+// ------------------------------------------------------------- errors.hpp:11-77
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DimensionError : public Error { public: using Error::Error; };
+class NoTargetsError : public Error { public: using Error::Error; };
+class RangeError : public Error { public: using Error::Error; };
+class IllConditionedSkeletonError : public Error { public: using Error::Error; };
+class ConfigError : public Error { public: using Error::Error; };
+class NumericalError : public Error { public: using Error::Error; };
+[[noreturn]] void throw_status(int code, const std::string& msg);
+
+// ------------------------------------------------------------- rng.hpp:19-78
+std::uint64_t splitmix64(std::uint64_t& state);
+std::uint64_t derive_seed(std::uint64_t master, std::uint64_t key_a, std::uint64_t key_b = 0);
+class Rng {
+ public:
+  explicit Rng(std::uint64_t seed) : engine_(seed) {}
+  std::uint64_t next_u64() { return engine_(); }
+  double uniform01() { return static_cast<double>(engine_() >> 11) * 0x1.0p-53; }
+  std::uint64_t below(std::uint64_t n);
+  double normal();
+
+ private:
+  std::mt19937_64 engine_;
+  bool has_spare_ = false;
+  double spare_ = 0.0;
+};
+
+// ------------------------------------------------------------- dense host matrix
+// Column-major like Eigen::MatrixXd (only what the host steps need).
+struct Matrix {
+  int64_t rows = 0, cols = 0;
+  std::vector<double> a;
+  Matrix() = default;
+  Matrix(int64_t r, int64_t c, double v = 0.0) : rows(r), cols(c), a(static_cast<size_t>(r * c), v) {}
+  double& operator()(int64_t i, int64_t j) { return a[static_cast<size_t>(i + j * rows)]; }
+  double operator()(int64_t i, int64_t j) const { return a[static_cast<size_t>(i + j * rows)]; }
+  double* data() { return a.data(); }
+  const double* data() const { return a.data(); }
+};
+
+// ------------------------------------------------------------- kernel.hpp / datagen.hpp
+using PointSet = Matrix;  // N x d, one point per row (kernel.hpp:14)
+struct KernelSpec {       // Gaussian family only on this path (kernel.hpp:23-52)
+  double h = 1.0;
+  static KernelSpec gaussian(double h) { return {h}; }
+  void validate() const;
+};
+PointSet gen_normal(int d, int64_t N, std::uint64_t seed);  // datagen.hpp:35-43
+double silverman_bandwidth(int d, long long N);             // kernel.hpp:119-123
+double eval_kernel(const KernelSpec& spec, const double* x, int64_t sx, const double* y, int64_t sy, int d);
+
+// ------------------------------------------------------------- device
+class Device {
+ public:
+  explicit Device(int device = 0);
+  ~Device();
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+  kid_ctx* ctx() const { return ctx_; }
+  void check(int status) const;  // throws the mirrored exception
+
+ private:
+  kid_ctx* ctx_ = nullptr;
+};
+
+// ------------------------------------------------------------- geometry.hpp:21-65
+struct SourceTargetSplit {
+  std::vector<double> center;
+  std::vector<int64_t> source_indices;
+  std::vector<int64_t> target_indices;
+  double rho = 0.0;
+  double xi = 0.0;
+};
+// Uploads `ps` and runs pass 1 on the device; the block K(T, S) stays resident on `dev`.
+SourceTargetSplit split_sources_targets(Device& dev, const PointSet& ps, const std::vector<double>& x_c,
+                                        int64_t n, double xi);
+
+// The device-resident K(T, S) of the last split (replaces the dense MatrixXd K).
+class KernelBlock {
+ public:
+  KernelBlock(Device& dev, KernelSpec spec, const PointSet& points, const SourceTargetSplit& split);
+  int64_t rows() const { return static_cast<int64_t>(split_->target_indices.size()); }
+  int64_t cols() const { return static_cast<int64_t>(split_->source_indices.size()); }
+  const KernelSpec& spec() const { return spec_; }
+  Device& device() const { return *dev_; }
+  // rows of K with the reference arithmetic (gather_rows, compress.hpp:130-137)
+  Matrix rows_exact(const std::vector<int64_t>& idx) const;
+  std::vector<double> row_norms() const;        // sampling.hpp:193 (device)
+  Matrix gram(double* sumsq = nullptr) const;   // K^T K (device)
+  double spectral_norm() const;                 // ||K||_2 = sqrt(lambda_max(K^T K))
+
+ private:
+  Device* dev_;
+  KernelSpec spec_;
+  const PointSet* points_;
+  const SourceTargetSplit* split_;
+};
+
+// ------------------------------------------------------------- lowrank.hpp (host, small)
+struct IDFactorization {
+  std::vector<int64_t> skeleton;
+  Matrix projection;  // r x n, original column order
+  int64_t rank = 0;
+};
+struct LeverageScores {
+  std::vector<double> scores;
+  bool degenerate_gap = false;
+};
+std::vector<double> singular_values(const Matrix& A);                       // lowrank.hpp:70-77
+int64_t epsilon_rank(const std::vector<double>& sv, double eps,
+                     std::optional<double> reference_sigma1 = std::nullopt);  // :117-126
+IDFactorization interpolative_decomposition(const Matrix& A, int64_t r);     // :235-262
+void sym_eig(const Matrix& A, std::vector<double>& evals, Matrix* evecs);   // Gram route
+LeverageScores row_leverage_scores(const KernelBlock& K, int64_t r);        // :296-308 (device)
+
+// ------------------------------------------------------------- sampling.hpp
+enum class SchemeKind { Uniform, Bernoulli, EuclideanNorm, Distance, Leverage, NearestNeighbor };
+struct SamplingScheme {
+  SchemeKind kind = SchemeKind::Uniform;
+  bool replacement = false;
+  int64_t rank_for_leverage = 1;
+  bool distance_direct = false;
+  std::string name() const;
+};
+struct RowSample {
+  std::vector<int64_t> indices;
+  double fraction = 0.0;
+  std::uint64_t seed = 0;
+};
+struct SampleContext {
+  int64_t m = 0;
+  const KernelBlock* K = nullptr;
+  const SourceTargetSplit* split = nullptr;
+  const PointSet* points = nullptr;
+};
+int64_t sample_count(double s, int64_t m);
+std::vector<int64_t> weighted_draw(const std::vector<double>& weights, int64_t count, bool replacement, Rng& rng);
+RowSample sample_rows(const SamplingScheme& scheme, const SampleContext& ctx, double s, std::uint64_t seed);
+
+// ------------------------------------------------------------- compress.hpp
+struct RankRule {
+  std::optional<double> eps;
+  std::optional<int64_t> fixed_r;
+  std::optional<double> reference_sigma1;
+  static RankRule from_eps(double e) { return {e, std::nullopt, std::nullopt}; }
+  static RankRule from_fixed(int64_t r) { return {std::nullopt, r, std::nullopt}; }
+  int64_t resolve(const std::vector<double>& sv) const;
+};
+struct NormPolicy {
+  double memory_budget_values = 2e8;
+  double power_tol = 1e-6;
+  int power_cap = 1000;
+};
+struct StageTimings {
+  double sample_ms = 0.0, factor_ms = 0.0, error_ms = 0.0;
+};
+struct CompressionReport {
+  SamplingScheme scheme;
+  double fraction = 0.0;
+  int64_t rank = 0;
+  double rel_error = 0.0;       // ||C P - K||_2 / ||K||_2 (the reference metric)
+  double rel_error_fro = 0.0;   // ||C P - K||_F / ||K||_F (north-star literal)
+  std::optional<double> bound_id;
+  std::optional<double> bound_sampling;
+  std::uint64_t seed = 0;
+  StageTimings timings;
+  bool rank_zero = false;
+  double sigma_r1_sample = 0.0;
+  double sigma1_sample = 0.0;
+};
+struct CompressOptions {
+  NormPolicy norms;
+  std::optional<std::vector<double>> full_spectrum;
+  std::optional<double> k_norm;
+  double theorem_eps = 0.5;
+};
+double bound_id_value(int64_t n, int64_t r, double sigma_r1);
+double reconstruction_bound(int64_t m, int64_t s_count, double eps, double sigma_r1);
+std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, const RowSample& sample,
+                                                          const RankRule& rule, const CompressOptions& opts = {});
+
+// ------------------------------------------------------------- harness.hpp (compress sweep)
+struct ExperimentConfig {
+  int d = 2;
+  int64_t N = 100000;
+  int64_t n_sources = 100;
+  double xi = 2.0;
+  double h_value = 1.0;
+  bool h_in_silverman_units = true;
+  std::vector<SamplingScheme> schemes{SamplingScheme{}};
+  std::vector<bool> scheme_rank_auto{false};
+  std::vector<double> s_grid{1e-4, 1e-3, 1e-2, 1e-1, 1.0};
+  RankRule rank_rule = RankRule::from_eps(1e-2);
+  bool rank_reference_full = false;
+  bool emit_bound_sampling = false;
+  bool emit_timings = false;
+  double theorem_eps = 0.5;
+  int trials = 1;
+  std::uint64_t seed = 1;
+};
+// harness.hpp:143-328 for the Normal dataset / RandomPoint center / ID method.
+void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out, std::ostream* log = nullptr);
+std::string format_double(double v);
+
+}  // namespace kernid_b200

@@ -3,7 +3,7 @@
  * far-field hot path of arXiv 1409.2802's reference (`kernid`, /root/reference/proj).
  *
  * The reference has no FFI layer: its hot path is the header-only C++ API in
- * proj/include/kernid/*.hpp. Each entry point below replaces the
+ * proj/include/kernid/ headers. Each entry point below replaces the
  * device-side work of one reference function; the cited reference function is what a
  * maintainer would re-point at this ABI (bindings in INTEGRATION.md).
  *
@@ -103,15 +103,24 @@ int kid_leverage_dev(kid_ctx* ctx, double h, const double* d_W, int64_t r, doubl
  * D^T D and K^T K (m x m col-major; rows/cols of skeleton columns of D^T D are exactly 0). */
 int kid_recon_error(kid_ctx* ctx, double h, const int64_t* skel, int64_t r, const double* P,
                     uint32_t flags, double* sumsq_D, double* sumsq_K, double* DtD, double* KtK);
-/* device variant: d_out receives [sumsq_D, sumsq_K, DtD (m*m), KtK (m*m if flag)] */
+/* device variant (after kid_recon_prepare): d_out receives [sumsq_D, sumsq_K, D^T D restricted
+ * to the m - r non-skeleton columns ((m-r) x (m-r) col-major, ascending original column)] */
 int kid_recon_prepare(kid_ctx* ctx, const int64_t* skel, int64_t r, const double* P);
 int kid_recon_error_dev(kid_ctx* ctx, double h, uint32_t flags, double* d_out);
 
 /* ---- gather_rows of K on the device (compress.hpp:130-137): Ks (count x m col-major) ---- */
 int kid_eval_rows(kid_ctx* ctx, double h, const int64_t* rows, int64_t count, double* Ks_out);
 
-/* ---- instrumentation: number of kernels this context launched, last kernel's name ---- */
+/* ---- diagnostics: the FP64 passes' exp(x), x <= 0 (for accuracy checks against libm) ---- */
+int kid_exp_check(kid_ctx* ctx, const double* x, int64_t n, double* y);
+
+/* ---- instrumentation: number of kernels this context has launched ---- */
 int64_t kid_launch_count(const kid_ctx* ctx);
+/* Kernel timing: when enabled, each pass records a CUDA event pair on its stream around its
+ * dominant kernel (k_dist_cand / k_compact, k_row_norms, k_gram, k_leverage); kid_profile_read
+ * returns the per-launch durations in ms (oldest first) and resets the list. */
+int kid_profile(kid_ctx* ctx, int32_t enable);
+int kid_profile_read(kid_ctx* ctx, double* ms_each, int64_t cap, int64_t* count);
 
 #ifdef __cplusplus
 }

@@ -37,7 +37,7 @@ SYMBOLS = ["kid_abi_version", "kid_create", "kid_destroy", "kid_last_error", "ki
            "kid_set_points", "kid_set_points_device", "kid_split", "kid_split_candidates", "kid_split_finish",
            "kid_get_targets", "kid_set_block", "kid_block_shape", "kid_row_norms", "kid_row_norms_dev", "kid_gram",
            "kid_gram_dev", "kid_leverage", "kid_leverage_dev", "kid_recon_error", "kid_recon_prepare",
-           "kid_recon_error_dev", "kid_eval_rows", "kid_launch_count"]
+           "kid_recon_error_dev", "kid_eval_rows", "kid_launch_count", "kid_profile", "kid_profile_read", "kid_exp_check"]
 
 
 def cuda_lib():
@@ -77,6 +77,9 @@ def cuda_lib():
         L.kid_eval_rows.argtypes = [vp, dbl, _ip, i64, _dp]
         L.kid_launch_count.argtypes = [vp]
         L.kid_launch_count.restype = i64
+        L.kid_profile.argtypes = [vp, i32]
+        L.kid_exp_check.argtypes = [vp, _dp, i64, _dp]
+        L.kid_profile_read.argtypes = [vp, vp, i64, P(i64)]
         _cuda = L
     return _cuda
 
@@ -121,6 +124,29 @@ class Device:
     @property
     def launches(self) -> int:
         return int(self.L.kid_launch_count(self.h))
+
+    def profile(self, enable: bool):
+        self._ck(self.L.kid_profile(self.h, int(enable)), "kid_profile")
+
+    def profile_read(self) -> np.ndarray:
+        cap = 1 << 16
+        buf = np.zeros(cap)
+        n = C.c_int64()
+        self._ck(self.L.kid_profile_read(self.h, buf.ctypes.data, cap, C.byref(n)), "kid_profile_read")
+        return buf[: min(n.value, cap)].copy()
+
+    def exp_check(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(max(x.size, 1))
+        self._ck(self.L.kid_exp_check(self.h, x, x.size, y), "kid_exp_check")
+        return y[: x.size].copy()
+
+    def recon_prepare(self, skel, P):
+        skel = np.ascontiguousarray(skel, dtype=np.int64)
+        self._ck(self.L.kid_recon_prepare(self.h, skel, skel.size, _colmajor(P)), "kid_recon_prepare")
+
+    def recon_error_dev(self, h: float, out_ptr: int, flags: int = KID_RECON_DTD):
+        self._ck(self.L.kid_recon_error_dev(self.h, h, flags, out_ptr), "kid_recon_error_dev")
 
     def set_stream(self, stream_ptr: int | None):
         self._ck(self.L.kid_set_stream(self.h, stream_ptr or None), "kid_set_stream")

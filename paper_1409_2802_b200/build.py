@@ -48,7 +48,7 @@ def build_host(force=False, verbose=False):
         return HOST_SO
     cmd = ["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-ffp-contract=off", "-Wall",
            "-I", os.path.join(ROOT, "include"), "-o", HOST_SO] + [os.path.join(HOST, f) for f in HOST_SRCS] + \
-          ["-ldl", "-lpthread"]
+          ["-L", PKG, "-lkernid_cuda", "-Wl,-rpath,$ORIGIN", "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
@@ -56,8 +56,9 @@ def build_host(force=False, verbose=False):
 
 
 def build_all(force=False, verbose=False):
+    cuda_rebuilt = _stale(CUDA_SO, [os.path.join(CSRC, f) for f in os.listdir(CSRC)])
     build_cuda(force, verbose)
-    build_host(force, verbose)
+    build_host(force or cuda_rebuilt, verbose)
 
 
 if __name__ == "__main__":

@@ -55,6 +55,24 @@ void* scratch(kid_ctx* c, size_t bytes) {
   return c->scratch;
 }
 
+void prof_begin(kid_ctx* c) {
+  if (!c->prof) return;
+  if (c->prof_used + 2 > c->prof_ev.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      c->prof_ev.push_back(e);
+    }
+  }
+  cudaEventRecord(c->prof_ev[c->prof_used], c->stream);
+}
+
+void prof_end(kid_ctx* c) {
+  if (!c->prof || c->prof_used + 2 > c->prof_ev.size()) return;
+  cudaEventRecord(c->prof_ev[c->prof_used + 1], c->stream);
+  c->prof_used += 2;
+}
+
 }  // namespace kid
 
 using namespace kid;
@@ -106,6 +124,7 @@ void kid_destroy(kid_ctx* c) {
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->hbuf) cudaFreeHost(c->hbuf);
+  for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -125,6 +144,27 @@ int kid_synchronize(kid_ctx* c) {
 }
 
 int64_t kid_launch_count(const kid_ctx* c) { return c ? c->launches : 0; }
+
+int kid_profile(kid_ctx* c, int32_t enable) {
+  if (!c) return KID_E_ERROR;
+  c->prof = enable != 0;
+  c->prof_used = 0;
+  return KID_OK;
+}
+
+int kid_profile_read(kid_ctx* c, double* ms_each, int64_t cap, int64_t* count) {
+  if (!c || !count) return KID_E_ERROR;
+  const int64_t n = (int64_t)(c->prof_used / 2);
+  for (int64_t k = 0; k < n && k < cap; ++k) {
+    float ms = 0.f;
+    KID_CK(c, cudaEventSynchronize(c->prof_ev[2 * k + 1]));
+    KID_CK(c, cudaEventElapsedTime(&ms, c->prof_ev[2 * k], c->prof_ev[2 * k + 1]));
+    if (ms_each) ms_each[k] = ms;
+  }
+  *count = n;
+  c->prof_used = 0;
+  return KID_OK;
+}
 
 int kid_set_points(kid_ctx* c, const double* host_pts, int64_t N, int32_t d, int64_t index_offset) {
   if (!c || !host_pts) return KID_E_ERROR;
@@ -387,6 +427,18 @@ int kid_eval_rows(kid_ctx* c, double h, const int64_t* rows, int64_t count, doub
   if (count) KID_CK(c, cudaMemcpyAsync(d_rows, rows, sizeof(int64_t) * count, cudaMemcpyHostToDevice, c->stream));
   if (int rc = eval_rows_dev(c, h, d_rows, count, buf)) return rc;
   if (count) KID_CK(c, cudaMemcpyAsync(Ks_out, buf, sizeof(double) * count * m, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  return KID_OK;
+}
+
+int kid_exp_check(kid_ctx* c, const double* x, int64_t n, double* y) {
+  if (!c || (n && (!x || !y))) return KID_E_ERROR;
+  if (int rc = set_device(c)) return rc;
+  double* buf = out_buffer(c, 2 * std::max<int64_t>(n, 1));
+  if (!buf) return KID_E_OOM;
+  if (n) KID_CK(c, cudaMemcpyAsync(buf, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  if (int rc = exp_check_dev(c, buf, n, buf + n)) return rc;
+  if (n) KID_CK(c, cudaMemcpyAsync(y, buf + n, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
   KID_CK(c, cudaStreamSynchronize(c->stream));
   return KID_OK;
 }

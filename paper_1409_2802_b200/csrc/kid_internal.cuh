@@ -40,6 +40,37 @@ __device__ __forceinline__ double gauss_exact(double sq, double denom) {
   return exp(__ddiv_rn(-sq, denom));
 }
 
+// exp(-q), q >= 0, for the Gaussian entries of the FP64 passes: table-driven and branch-free
+// (tab[j] = 2^(j/1024), correctly rounded, staged in shared memory from c_exp2_tab):
+//   -q = (1024k + j) ln2/1024 + r,  |r| <= ln2/2048,  e^r - 1 by a degree-4 Taylor polynomial
+//   (truncation r^5/120 < 4e-20), exp(-q) = 2^k (T[j] + T[j] (e^r - 1)); the 2^k is applied as
+//   2^(k+600) on the exponent field and one multiply by 2^-600 (exact for normal results,
+//   correctly rounded into the subnormal range; k is clamped where the result rounds to 0).
+// 11 FP64-pipe ops against ~20 for libdevice exp() plus the caller's divide; max error 1 ulp
+// against glibc (tests/test_gpu_parity.py::test_fast_exp_accuracy). Valid for q < 1.4e6.
+constexpr int kExpTab = 1024;
+__device__ __forceinline__ double exp_neg_fast(double q, const double* __restrict__ tab) {
+  const double shifter = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest-integer
+  double kd = fma(q, -1477.3197218702985, shifter);  // round(-q * 1024 / ln2)
+  const int n = __double2loint(kd);
+  kd -= shifter;
+  double r = fma(kd, -0.0006769015433292225, -q);
+  r = fma(kd, -1.8634911418658083e-13, r);
+  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p *= r;  // e^r - 1
+  const double t = tab[n & (kExpTab - 1)];
+  const double y = fma(t, p, t);
+  const int k = max(n >> 10, -1100);  // floor(n / 1024), clamped: 2^(k+600) stays normal
+  return __hiloint2double(__double2hiint(y) + ((k + 600) << 20), __double2loint(y)) * 0x1p-600;
+}
+
+// exp(x), x <= 0 (diagnostics and callers holding the argument)
+__device__ __forceinline__ double exp_fast(double x, const double* __restrict__ tab) {
+  return exp_neg_fast(-x, tab);
+}
+
 // FP64 tensor-core MMA (SASS DMMA.8x8x4): C[8x8] += A[8x4] * B[4x8].
 // Fragments: A[row = lane>>2][k = lane&3], B[k = lane&3][col = lane>>2],
 // C[row = lane>>2][col = 2*(lane&3) + {0,1}].
@@ -109,6 +140,12 @@ struct kid_ctx {
   double* hbuf = nullptr;  // pinned host staging
   size_t hbuf_cap = 0;
   int64_t* counter = nullptr;  // device counters [8]
+
+  // kernel timing (kid_profile): CUDA events on the launching stream around each pass'
+  // dominant kernel, read back by kid_profile_read
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;  // pairs
+  size_t prof_used = 0;
 };
 
 namespace kid {
@@ -140,5 +177,10 @@ int row_norms_dev(kid_ctx* c, double h, double* d_w);
 int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out);
 int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores);
 int eval_rows_dev(kid_ctx* c, double h, const int64_t* d_rows, int64_t count, double* d_Ks);
+int init_device_tables();
+int exp_check_dev(kid_ctx* c, const double* d_x, int64_t n, double* d_y);
+// event pair bracketing the dominant kernel of a pass (no-op unless profiling)
+void prof_begin(kid_ctx* c);
+void prof_end(kid_ctx* c);
 
 }  // namespace kid

@@ -14,12 +14,30 @@
 // CTA's contiguous target chunk; partials are reduced in a fixed chunk order so results
 // are bitwise reproducible run to run.
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "kid_internal.cuh"
 
 namespace kid {
+
+__device__ double c_exp2_tab[kExpTab];  // global (L2-resident); each CTA stages it in shared memory
+
+int init_device_tables() {
+  static thread_local int done_dev = -1;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return KID_E_CUDA;
+  if (done_dev == dev) return KID_OK;
+  double tab[kExpTab];
+  for (int j = 0; j < kExpTab; ++j) tab[j] = (double)exp2l((long double)j / (long double)kExpTab);
+  if (cudaMemcpyToSymbol(c_exp2_tab, tab, sizeof(tab)) != cudaSuccess) return KID_E_CUDA;
+  done_dev = dev;
+  return KID_OK;
+}
+
 namespace {
 
 constexpr int kTM = 32;        // targets per tile (SYRK k-depth: 8 DMMA k-steps)
@@ -46,9 +64,11 @@ __host__ __device__ constexpr int frag_stride(int cols) { return ceil_to(cols, 8
 // ------------------------------------------------------------------ row norms
 template <int D>
 __global__ void __launch_bounds__(256) k_row_norms(TargetView tv, int d_rt, const double* __restrict__ src,
-                                                   int64_t m, double denom, double* __restrict__ w) {
+                                                   int64_t m, double negc, double* __restrict__ w) {
   const int d = D ? D : d_rt;
   extern __shared__ double s_src[];  // d x m, s_src[j + k*m]
+  __shared__ double s_tab[kExpTab];
+  for (int e = threadIdx.x; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
   for (int64_t e = threadIdx.x; e < m * d; e += blockDim.x) s_src[e] = src[e];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tv.nt; i += (int64_t)gridDim.x * blockDim.x) {
@@ -72,7 +92,7 @@ __global__ void __launch_bounds__(256) k_row_norms(TargetView tv, int d_rt, cons
           sq = __dadd_rn(sq, __dmul_rn(diff, diff));
         }
       }
-      const double kv = gauss_exact(sq, denom);
+      const double kv = exp_fast(sq * negc, s_tab);
       acc = __dadd_rn(acc, __dmul_rn(kv, kv));  // sequential over j (sampling.hpp:193)
     }
     w[i] = __dsqrt_rn(acc);
@@ -85,164 +105,295 @@ struct GramArgs {
   int d;
   const double* src;   // m x d col-major, columns already in [skel | non-skel] order
   int m, r, meff;      // meff = m - r
-  double denom;        // (2h)h
+  double negc;         // -1 / (2 h^2)
+  double cscale;       // 1 / (sqrt(2) h): coordinates pre-scaled so that exp(-||x' - y'||^2)
   const double* P2;    // r x meff row-major, stride SP (device); nullptr when r == 0
-  const int2* blist;   // [nparts][kNW][BPW] (a, b) block pairs, a = -1: empty slot
+  const int2* blist;   // [nparts][kMW][TPW] (ti, tj) 16x16 warp tiles, x = -1: empty slot
   int nparts;
   int64_t ntiles;
   int nchunks;
   double* partial;     // [nchunks][LG][LG]
   int LG;              // padded Gram leading dimension = ceil8(meff)
   double* partial_sk;  // [nchunks] (written by part 0)
+  int dbg;             // profiling aid (KID_GRAM_DEBUG): 1 skip eval math, 2 skip D = K_N - K_S P2, 4 skip SYRK
+  long long* trace;    // profiling aid (KID_GRAM_TRACE): [warp][tile][4] clock64 stamps of CTA 0
 };
+constexpr int kTraceTiles = 64;
 
-template <int D, int BPW>
-__global__ void __launch_bounds__(kNT) k_gram(GramArgs A) {
+// Warp-specialized pipeline (one CTA per SM):
+//   warps 0..7  (kMW "MMA" warps): per tile, D = K_N - K_S P2 (DMMA, balanced block list) then
+//               G += D^T D (DMMA) on static 16x16 warp tiles (2x2 blocks of 8x8) of the upper
+//               triangle, accumulators register-resident across all tiles of the CTA's chunk;
+//   warps 8..15 (kEW "eval" warps): evaluate the next 32 x m K tiles into a kStages-deep
+//               shared-memory ring. Tiles are COLUMN-major (K[col][t], stride kST = 36): lane =
+//               target row, so each thread keeps its target's coordinates in registers, source
+//               coordinates are warp-broadcast, stores are conflict-free, and the DMMA fragment
+//               gathers [(x*8 + (lane>>2)) * kST + (lane&3)] stay conflict-free (36 = 4 mod 16).
+// Hand-off by named barriers: FULL[s] (eval arrive, MMA sync), EMPTY[s] (MMA arrive, eval sync),
+// one MMA-group barrier between the two DMMA phases. Both groups share the FP64 datapath
+// (DMMA and DFMA do not overlap on sm_100: tools/fp64_overlap.cu); the split hides latency.
+constexpr int kMW = 8, kEW = 8, kGT = (kMW + kEW) * 32;  // 512 threads
+constexpr int kStages = 3;
+constexpr int kST = kTM + 4;  // column-major tile stride
+constexpr int kGPW = 4;       // GEMM1 blocks per warp per batch
+constexpr int kBarFull = 1, kBarEmpty = 1 + kStages, kBarMma = 1 + 2 * kStages;
+
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+#define KID_TRACE(ev)                                                                              \
+  do {                                                                                             \
+    if (A.trace && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && it < kTraceTiles)            \
+      A.trace[((size_t)warp * kTraceTiles + it) * 4 + (ev)] = clock64();                           \
+  } while (0)
+
+template <int D, int TPW>
+__global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
   const int d = D ? D : A.d;
   const int m = A.m, r = A.r, meff = A.meff;
   const int r4 = ceil_to(r, 4);
-  const int SS = frag_stride(r4 > 0 ? r4 : 4);
-  const int SN = frag_stride(meff);
-  const int SP = SN;
   const int NBN = ceil_to(meff, 8) / 8;
+  const int SP = frag_stride(meff);
+  const int TS = ceil_to(r4 > 0 ? r4 : 4, 2) * kST, TN = ceil_to(NBN, 2) * 8 * kST;  // one stage of K_S / K_N
   extern __shared__ __align__(16) double smem[];
-  double* s_src = smem;                       // d x m
-  double* s_t = s_src + (size_t)d * m;        // d x kTM
-  double* KS = s_t + (size_t)d * kTM;         // kTM x SS
-  double* KN = KS + (size_t)kTM * SS;         // kTM x SN
-  double* sP = KN + (size_t)kTM * SN;         // r4 x SP
-  __shared__ double red[kNW];
+  double* s_src = smem;                        // d x m (scaled)
+  double* KSb = s_src + ceil_to(d * m, 2);     // kStages x (r4 x kST), column-major
+  double* KNb = KSb + (size_t)kStages * TS;    // kStages x (NBN*8 x kST), column-major
+  double* sP = KNb + (size_t)kStages * TN;     // r4 x SP (row-major P2)
+  __shared__ double red[kMW + kEW];
+  __shared__ double s_tab[kExpTab];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = blockIdx.x, part = blockIdx.y;
-  for (int e = tid; e < m * d; e += kNT) s_src[e] = A.src[e];
-  for (int e = tid; e < kTM * SS; e += kNT) KS[e] = 0.0;
-  for (int e = tid; e < kTM * SN; e += kNT) KN[e] = 0.0;
-  for (int e = tid; e < r4 * SP; e += kNT) {
+  for (int e = tid; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
+  for (int e = tid; e < m * d; e += kGT) s_src[e] = A.src[e] * A.cscale;
+  for (int e = tid; e < kStages * TS; e += kGT) KSb[e] = 0.0;
+  for (int e = tid; e < kStages * TN; e += kGT) KNb[e] = 0.0;
+  for (int e = tid; e < r4 * SP; e += kGT) {
     const int k = e / SP, n = e % SP;
     sP[e] = (k < r && n < meff) ? A.P2[(size_t)k * SP + n] : 0.0;
   }
-  int2 bl[BPW];
-#pragma unroll
-  for (int s = 0; s < BPW; ++s) bl[s] = A.blist[((size_t)part * kNW + warp) * BPW + s];
-  double acc[BPW][2];
-#pragma unroll
-  for (int s = 0; s < BPW; ++s) acc[s][0] = acc[s][1] = 0.0;
-  double sk = 0.0;
+  const int64_t tile_lo = A.ntiles * chunk / A.nchunks, tile_hi = A.ntiles * (chunk + 1) / A.nchunks;
+  const int ntile = (int)(tile_hi - tile_lo);
   __syncthreads();
 
-  const int64_t tile_lo = A.ntiles * chunk / A.nchunks, tile_hi = A.ntiles * (chunk + 1) / A.nchunks;
-  for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
-    const int64_t t0 = tile * kTM;
-    for (int e = tid; e < kTM * d; e += kNT) {
-      const int t = e % kTM, k = e / kTM;
-      s_t[t + k * kTM] = (t0 + t < A.tv.nt) ? tcoord(A.tv, t0 + t, k) : 0.0;
-    }
-    __syncthreads();
-    // (1) evaluate the 32 x m tile: columns [0, r) -> KS, [r, m) -> KN
-    for (int e = tid; e < kTM * m; e += kNT) {
-      const int t = e / m, j = e - t * m;
-      double kv = 0.0;
-      if (t0 + t < A.tv.nt) {
-        double sq = 0.0;
-        if (D) {
+  if (warp >= kMW) {
+    // ================================================================ eval warps
+    const int ew = warp - kMW;  // this warp evaluates columns j = ew, ew + kEW, ...
+    // target coordinates live in registers for the compiled dimensions; the generic-d path
+    // (D == 0) re-reads them through L1 (tc holds a single slot there)
+    constexpr int DR = D ? D : 1;
+    double tc[DR], tn[DR];
+    double sk = 0.0;
+    {
+      const int64_t i = tile_lo * kTM + lane;
 #pragma unroll
-          for (int k = 0; k < (D ? D : 1); ++k) {
-            const double diff = __dsub_rn(s_t[t + k * kTM], s_src[j + k * m]);
-            sq = __dadd_rn(sq, __dmul_rn(diff, diff));
-          }
-        } else {
-          for (int k = 0; k < d; ++k) {
-            const double diff = __dsub_rn(s_t[t + k * kTM], s_src[j + k * m]);
-            sq = __dadd_rn(sq, __dmul_rn(diff, diff));
-          }
-        }
-        kv = gauss_exact(sq, A.denom);
+      for (int k = 0; k < DR; ++k) tc[k] = (k < d && ntile > 0 && i < A.tv.nt) ? tcoord(A.tv, i, k) * A.cscale : 0.0;
+    }
+    for (int it = 0; it < ntile; ++it) {
+      const int s = it % kStages;
+      const int64_t t0 = (tile_lo + it) * kTM;
+      const bool valid = t0 + lane < A.tv.nt;
+      {  // prefetch the next tile's coordinates (latency overlaps the evaluation)
+        const int64_t i = t0 + kTM + lane;
+        const bool ok = it + 1 < ntile && i < A.tv.nt;
+#pragma unroll
+        for (int k = 0; k < DR; ++k) tn[k] = (k < d && ok) ? tcoord(A.tv, i, k) : 0.0;
       }
-      sk = fma(kv, kv, sk);
-      if (j < r) KS[t * SS + j] = kv;
-      else KN[t * SN + (j - r)] = kv;
-    }
-    __syncthreads();
-    // (2) D = K_N - K_S P2 on DMMA (skipped in mode K, r == 0)
-    if (r > 0) {
-      for (int nb = warp; nb < NBN; nb += kNW) {
-        double c[kTM / 8][2];
+      KID_TRACE(0);
+      if (it >= kStages) nbar_sync(kBarEmpty + s, kGT);  // the MMA warps released stage s
+      KID_TRACE(1);
+      double* KS = KSb + (size_t)s * TS;
+      double* KN = KNb + (size_t)s * TN;
+      if (!(A.dbg & 1)) {
+        // two independent exp chains per iteration (columns j, j + kEW)
+        for (int j = ew; j < m; j += 2 * kEW) {
+          const int j1 = j + kEW < m ? j + kEW : j;
+          double q0 = 0.0, q1 = 0.0;
 #pragma unroll
-        for (int rb = 0; rb < kTM / 8; ++rb) c[rb][0] = c[rb][1] = 0.0;
-        for (int k0 = 0; k0 < r4; k0 += 4) {
-          const double b = sP[(k0 + (lane & 3)) * SP + nb * 8 + (lane >> 2)];
-#pragma unroll
-          for (int rb = 0; rb < kTM / 8; ++rb) {
-            const double a = KS[(rb * 8 + (lane >> 2)) * SS + k0 + (lane & 3)];
-            dmma884(c[rb][0], c[rb][1], a, b);
+          for (int k = 0; k < (D ? D : d); ++k) {
+            const double tk = D ? tc[D ? k : 0] : (valid ? tcoord(A.tv, t0 + lane, k) * A.cscale : 0.0);
+            const double d0 = tk - s_src[j + k * m];
+            const double d1 = tk - s_src[j1 + k * m];
+            q0 = fma(d0, d0, q0);
+            q1 = fma(d1, d1, q1);
           }
-        }
-#pragma unroll
-        for (int rb = 0; rb < kTM / 8; ++rb) {
-          double* p = &KN[(rb * 8 + (lane >> 2)) * SN + nb * 8 + 2 * (lane & 3)];
-          p[0] = p[0] - c[rb][0];
-          p[1] = p[1] - c[rb][1];
+          double k0v = exp_neg_fast(q0, s_tab), k1v = exp_neg_fast(q1, s_tab);
+          if (!valid) k0v = k1v = 0.0;
+          sk = fma(k0v, k0v, sk);
+          *((j < r) ? &KS[j * kST + lane] : &KN[(j - r) * kST + lane]) = k0v;
+          if (j + kEW < m) {
+            sk = fma(k1v, k1v, sk);
+            *((j1 < r) ? &KS[j1 * kST + lane] : &KN[(j1 - r) * kST + lane]) = k1v;
+          }
         }
       }
-      __syncthreads();
+      KID_TRACE(2);
+      nbar_arrive(kBarFull + s, kGT);  // stage s holds tile it
+#pragma unroll
+      for (int k = 0; k < DR; ++k) tc[k] = tn[k] * A.cscale;
     }
-    // (3) G += T^T T, k = 32 targets, register-resident 8x8 blocks
+    if (part == 0) {
+      sk = warp_sum(sk);
+      if (lane == 0) red[warp] = sk;
+    }
+  } else {
+    // ================================================================ MMA warps
+    int2 tl[TPW];  // (ti, tj) 16x16 warp tiles of the upper triangle, x = -1: empty
 #pragma unroll
-    for (int k0 = 0; k0 < kTM; k0 += 4) {
-      const double* row = KN + (k0 + (lane & 3)) * SN + (lane >> 2);
-      int cur = -1;
-      double af = 0.0;
+    for (int q = 0; q < TPW; ++q) tl[q] = A.blist[((size_t)part * kMW + warp) * TPW + q];
+    double acc[TPW][2][2][2];
 #pragma unroll
-      for (int s = 0; s < BPW; ++s) {
-        if (bl[s].x >= 0) {
-          if (bl[s].x != cur) {
-            af = row[bl[s].x * 8];
-            cur = bl[s].x;
+    for (int q = 0; q < TPW; ++q)
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) acc[q][u][v][0] = acc[q][u][v][1] = 0.0;
+    const int NB = NBN;
+    int vmask[TPW];  // which of the 4 blocks of each warp tile lie in the upper triangle
+#pragma unroll
+    for (int q = 0; q < TPW; ++q) {
+      vmask[q] = 0;
+      if (tl[q].x >= 0)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int a = 2 * tl[q].x + u, b = 2 * tl[q].y + v;
+            if (a < NB && b < NB && a <= b) vmask[q] |= 1 << (2 * u + v);
           }
-          const double bf = row[bl[s].y * 8];
-          dmma884(acc[s][0], acc[s][1], af, bf);
+    }
+    const int nblk1 = 4 * NBN;  // GEMM1 blocks (nb-major, rb minor)
+    const int g_lo = nblk1 * warp / kMW, g_hi = nblk1 * (warp + 1) / kMW;
+    const int fr = (lane >> 2), fk = (lane & 3);  // fragment coordinates
+    for (int it = 0; it < ntile; ++it) {
+      const int s = it % kStages;
+      KID_TRACE(0);
+      nbar_sync(kBarFull + s, kGT);
+      KID_TRACE(1);
+      const double* KS = KSb + (size_t)s * TS;
+      double* KN = KNb + (size_t)s * TN;
+      if (r > 0) {  // D = K_N - K_S P2, column-major in place
+        for (int g0 = (A.dbg & 2) ? g_hi : g_lo; g0 < g_hi; g0 += kGPW) {
+          double c[kGPW][2];
+#pragma unroll
+          for (int q = 0; q < kGPW; ++q) c[q][0] = c[q][1] = 0.0;
+          for (int k0 = 0; k0 < r4; k0 += 4) {
+            double a[kGPW], b[kGPW];
+#pragma unroll
+            for (int q = 0; q < kGPW; ++q) {
+              const int g = g0 + q < g_hi ? g0 + q : g_lo;
+              const int nb = g >> 2, rb = g & 3;
+              a[q] = KS[(k0 + fk) * kST + rb * 8 + fr];
+              b[q] = sP[(k0 + fk) * SP + nb * 8 + fr];
+            }
+#pragma unroll
+            for (int q = 0; q < kGPW; ++q)
+              if (g0 + q < g_hi) dmma884(c[q][0], c[q][1], a[q], b[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < kGPW; ++q) {
+            if (g0 + q < g_hi) {
+              const int g = g0 + q, nb = g >> 2, rb = g & 3;
+              double* p = &KN[(nb * 8 + 2 * fk) * kST + rb * 8 + fr];
+              p[0] -= c[q][0];
+              p[kST] -= c[q][1];
+            }
+          }
+        }
+        nbar_sync(kBarMma, kMW * 32);
+      }
+      KID_TRACE(2);
+      // G += D^T D over the 32 rows of the stage; fragments F(x) = D[k0 + fk][x*8 + fr],
+      // double-buffered so the loads of k-step k+1 overlap the DMMAs of k-step k
+      if (!(A.dbg & 4)) {
+        const double* col = KN + fr * kST + fk;
+        double fa[2][TPW][2], fb[2][TPW][2];
+        auto load = [&](int buf, int k0) {
+#pragma unroll
+          for (int q = 0; q < TPW; ++q) {
+            const int ti = tl[q].x >= 0 ? tl[q].x : 0, tj = tl[q].x >= 0 ? tl[q].y : 0;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              fa[buf][q][u] = col[(2 * ti + u) * 8 * kST + k0];
+              fb[buf][q][u] = col[(2 * tj + u) * 8 * kST + k0];
+            }
+          }
+        };
+        load(0, 0);
+#pragma unroll
+        for (int kk = 0; kk < kTM / 4; ++kk) {
+          if (kk + 1 < kTM / 4) load((kk + 1) & 1, (kk + 1) * 4);
+#pragma unroll
+          for (int q = 0; q < TPW; ++q) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+              for (int v = 0; v < 2; ++v)
+                if (vmask[q] & (1 << (2 * u + v)))
+                  dmma884(acc[q][u][v][0], acc[q][u][v][1], fa[kk & 1][q][u], fb[kk & 1][q][v]);
+          }
         }
       }
+      KID_TRACE(3);
+      if (it + kStages < ntile) nbar_arrive(kBarEmpty + s, kGT);  // release stage s
     }
-    __syncthreads();
+    double* G = A.partial + (size_t)chunk * A.LG * A.LG;
+#pragma unroll
+    for (int q = 0; q < TPW; ++q) {
+      if (tl[q].x < 0) continue;
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int a = 2 * tl[q].x + u, b = 2 * tl[q].y + v;
+          if (a < NB && b < NB && a <= b) {
+            const int row = a * 8 + fr, colx = b * 8 + 2 * fk;
+            G[row + (size_t)colx * A.LG] = acc[q][u][v][0];
+            G[row + (size_t)(colx + 1) * A.LG] = acc[q][u][v][1];
+          }
+        }
+    }
   }
-  // partial Gram blocks of this (chunk, part)
-  double* G = A.partial + (size_t)chunk * A.LG * A.LG;
-#pragma unroll
-  for (int s = 0; s < BPW; ++s) {
-    if (bl[s].x >= 0) {
-      const int row = bl[s].x * 8 + (lane >> 2);
-      const int col = bl[s].y * 8 + 2 * (lane & 3);
-      G[row + (size_t)col * A.LG] = acc[s][0];
-      G[row + (size_t)(col + 1) * A.LG] = acc[s][1];
-    }
-  }
-  (void)NBN;
   if (part == 0) {
-    sk = warp_sum(sk);
-    if (lane == 0) red[warp] = sk;
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
-      for (int w = 0; w < kNW; ++w) t += red[w];
+      for (int w = kMW; w < kMW + kEW; ++w) t += red[w];
       A.partial_sk[chunk] = t;
     }
   }
 }
 
-// out = [sumsq_T, sumsq_K, G (meff x meff col-major, symmetric from the upper triangle)]
-__global__ void k_gram_reduce(const double* __restrict__ partial, int nchunks, int LG, int meff,
-                              const double* __restrict__ partial_sk, double* __restrict__ out) {
+// out = [sumsq_T, sumsq_K, G (meff x meff col-major, symmetric from the upper triangle)].
+// Block = 32 consecutive output elements x 32 chunk groups; group g sums chunks g, g+32, ...
+// in order, then the 32 group sums are combined in a fixed order: deterministic.
+__global__ void __launch_bounds__(1024) k_gram_reduce(const double* __restrict__ partial, int nchunks, int LG,
+                                                      int meff, const double* __restrict__ partial_sk,
+                                                      double* __restrict__ out) {
+  __shared__ double part_s[32][33];
   const int64_t total = (int64_t)meff * meff;
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   double* G = out + 2;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int x = (int)(e % meff), y = (int)(e / meff);
-    int ux = x, uy = y;
-    if ((x >> 3) > (y >> 3) || (((x >> 3) == (y >> 3)) && x > y)) { ux = y; uy = x; }
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < total; base += (int64_t)gridDim.x * 32) {
+    const int64_t e = base + lane;
     double s = 0.0;
-    for (int c = 0; c < nchunks; ++c) s += partial[(size_t)c * LG * LG + ux + (size_t)uy * LG];
-    G[x + (size_t)y * meff] = s;
+    int64_t off = 0;
+    if (e < total) {
+      const int x = (int)(e % meff), y = (int)(e / meff);
+      int ux = x, uy = y;
+      if ((x >> 3) > (y >> 3) || (((x >> 3) == (y >> 3)) && x > y)) { ux = y; uy = x; }
+      off = ux + (int64_t)uy * LG;
+      for (int c = g; c < nchunks; c += 32) s += partial[(size_t)c * LG * LG + off];
+    }
+    part_s[g][lane] = s;
+    __syncthreads();
+    if (g == 0 && e < total) {
+      double t = 0.0;
+      for (int q = 0; q < 32; ++q) t += part_s[q][lane];
+      G[e] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -263,7 +414,7 @@ struct LevArgs {
   int d;
   const double* src;
   int m, r;
-  double denom;
+  double negc;
   const double* W;  // m x r col-major (device)
   bool w_in_smem;
   double* scores;
@@ -284,6 +435,10 @@ __global__ void __launch_bounds__(kNT) k_leverage(LevArgs A) {
   double* rowpart = KN + (size_t)kTM * SN;  // kTM x NBR
   double* sW = rowpart + (size_t)kTM * NBR; // m4 x SW (row-major) when w_in_smem
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double s_tab[kExpTab];
+  for (int e = tid; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
+  const int t_init = tid / m, j_init = tid - (tid / m) * m;
+  const int step_t = kNT / m, step_j = kNT - (kNT / m) * m;
   for (int e = tid; e < m * d; e += kNT) s_src[e] = A.src[e];
   for (int e = tid; e < kTM * SN; e += kNT) KN[e] = 0.0;
   if (A.w_in_smem)
@@ -300,18 +455,26 @@ __global__ void __launch_bounds__(kNT) k_leverage(LevArgs A) {
       s_t[t + k * kTM] = (t0 + t < A.tv.nt) ? tcoord(A.tv, t0 + t, k) : 0.0;
     }
     __syncthreads();
-    for (int e = tid; e < kTM * m; e += kNT) {
-      const int t = e / m, j = e - t * m;
+    const int64_t rows_left = A.tv.nt - t0;
+    for (int t = t_init, j = j_init; t < kTM;) {
       double kv = 0.0;
-      if (t0 + t < A.tv.nt) {
+      if (t < rows_left) {
         double sq = 0.0;
-        for (int k = 0; k < d; ++k) {
+#pragma unroll
+        for (int k = 0; k < (D ? D : 64); ++k) {
+          if (!D && k >= d) break;
           const double diff = __dsub_rn(s_t[t + k * kTM], s_src[j + k * m]);
           sq = __dadd_rn(sq, __dmul_rn(diff, diff));
         }
-        kv = gauss_exact(sq, A.denom);
+        kv = exp_fast(sq * A.negc, s_tab);
       }
       KN[t * SN + j] = kv;
+      j += step_j;
+      t += step_t;
+      if (j >= m) {
+        j -= m;
+        ++t;
+      }
     }
     __syncthreads();
     for (int nb = warp; nb < NBR; nb += kNW) {
@@ -361,6 +524,14 @@ __global__ void k_eval_rows(TargetView tv, int d, const double* __restrict__ src
   }
 }
 
+__global__ void k_exp_check(const double* __restrict__ x, int64_t n, double* __restrict__ y) {
+  __shared__ double s_tab[kExpTab];
+  for (int e = threadIdx.x; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = exp_fast(x[i], s_tab);
+}
+
 TargetView view(const kid_ctx* c) { return TargetView{c->tbase, c->tld, c->tidx, c->nt}; }
 
 #define KID_DISPATCH_D(d, MACRO) \
@@ -386,7 +557,8 @@ int check_block(kid_ctx* c, double h) {
 int row_norms_dev(kid_ctx* c, double h, double* d_w) {
   if (int rc = check_block(c, h)) return rc;
   if (c->nt == 0) return KID_OK;
-  const double denom = 2.0 * h * h;
+  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
+  const double denom = -1.0 / (2.0 * h * h);
   const size_t sm = sizeof(double) * c->m * c->d;
   if (sm > 200 * 1024) return fail(c, KID_E_DIM, "row_norms: m*d too large for shared memory");
   const int blocks = (int)std::min<int64_t>((c->nt + 255) / 256, (int64_t)c->sms * 8);
@@ -395,7 +567,9 @@ int row_norms_dev(kid_ctx* c, double h, double* d_w) {
     cudaFuncSetAttribute(k_row_norms<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     k_row_norms<DD><<<blocks, 256, sm, c->stream>>>(view(c), c->d, c->src, c->m, denom, d_w);   \
   }
+  prof_begin(c);
   KID_DISPATCH_D(c->d, LAUNCH)
+  prof_end(c);
 #undef LAUNCH
   KID_LAUNCHED(c);
   return KID_OK;
@@ -409,39 +583,66 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   const int m = (int)c->m, d = c->d;
   const int meff = (int)(m - r);
   if (meff < 1) {
-    // full-rank skeleton: D == 0 exactly
-    KID_CK(c, cudaMemsetAsync(d_out, 0, sizeof(double) * 2, c->stream));
-    return KID_OK;
+    // full-rank skeleton: D == 0 exactly; ||K||_F^2 still comes from a K-mode pass
+    double* tmp = nullptr;
+    KID_CK(c, cudaMallocAsync((void**)&tmp, sizeof(double) * (2 + (size_t)m * m), c->stream));
+    int rc = gram_dev(c, h, 0, flags, tmp);
+    if (!rc) {
+      KID_CK(c, cudaMemsetAsync(d_out, 0, sizeof(double), c->stream));
+      KID_CK(c, cudaMemcpyAsync(d_out + 1, tmp + 1, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    KID_CK(c, cudaFreeAsync(tmp, c->stream));
+    return rc;
   }
   const int NBN = ceil_to(meff, 8) / 8;
   const int LG = NBN * 8;
-  // upper-triangular 8x8 blocks, row-major (a <= b), grouped per warp
-  std::vector<int2> blocks;
-  for (int a = 0; a < NBN; ++a)
-    for (int b = a; b < NBN; ++b) blocks.push_back(make_int2(a, b));
-  const int nb = (int)blocks.size();
-  int BPW = 4;
-  for (int cand : {4, 8, 12, 16, 24}) {
-    BPW = cand;
-    if ((nb + kNW * cand - 1) / (kNW * cand) <= 1) break;
+  // upper-triangular 16x16 warp tiles (2x2 blocks), row-major
+  const int NBT = (NBN + 1) / 2;
+  std::vector<int2> tiles;
+  for (int a = 0; a < NBT; ++a)
+    for (int b = a; b < NBT; ++b) tiles.push_back(make_int2(a, b));
+  const int nb = (int)tiles.size();
+  int TPW = 1;
+  for (int cand = 1; cand <= 5; ++cand) {
+    TPW = cand;
+    if (nb <= kMW * cand) break;
   }
-  const int per_part = kNW * BPW;
+  const int per_part = kMW * TPW;
   const int nparts = (nb + per_part - 1) / per_part;
   std::vector<int2> blist((size_t)nparts * per_part, make_int2(-1, -1));
-  for (int p = 0; p < nparts; ++p)
-    for (int w = 0; w < kNW; ++w)
-      for (int s = 0; s < BPW; ++s) {
-        // contiguous runs per warp keep the A fragment reused across consecutive slots
-        const int g = p * per_part + w * BPW + s;
-        if (g < nb) blist[((size_t)p * kNW + w) * BPW + s] = blocks[g];
-      }
+  for (int p = 0; p < nparts; ++p) {
+    const int lo = (int)((int64_t)nb * p / nparts), hi = (int)((int64_t)nb * (p + 1) / nparts);
+    const int cnt = hi - lo;
+    for (int w = 0; w < kMW; ++w) {
+      const int wlo = lo + cnt * w / kMW, whi = lo + cnt * (w + 1) / kMW;
+      for (int g = wlo; g < whi; ++g) blist[((size_t)p * kMW + w) * TPW + (g - wlo)] = tiles[g];
+    }
+  }
   const int r4 = ceil_to((int)r, 4);
-  const int SS = frag_stride(r4 > 0 ? r4 : 4), SN = frag_stride(meff);
-  const size_t smem = sizeof(double) * ((size_t)d * m + (size_t)d * kTM + (size_t)kTM * SS + (size_t)kTM * SN +
-                                        (size_t)r4 * SN);
+  const int TS = ceil_to(r4 > 0 ? r4 : 4, 2) * kST, TN = ceil_to(NBN, 2) * 8 * kST;
+  const size_t smem = sizeof(double) * ((size_t)ceil_to(d * m, 2) + (size_t)kStages * (TS + TN) +
+                                        (size_t)r4 * frag_stride(meff));
   if (smem > 220 * 1024) return fail(c, KID_E_DIM, "gram: tile does not fit shared memory (m, r too large)");
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;
-  int per_sm = smem <= 100 * 1024 ? 2 : 1;
+  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
+  int per_sm = 1;
+  {
+    const void* fn = nullptr;
+#define PICK(DD, BB) fn = (const void*)k_gram<DD, BB>;
+#define PICK_D(DD)                 \
+  switch (TPW) {                   \
+    case 1: PICK(DD, 1) break;     \
+    case 2: PICK(DD, 2) break;     \
+    case 3: PICK(DD, 3) break;     \
+    case 4: PICK(DD, 4) break;     \
+    default: PICK(DD, 5) break;    \
+  }
+    KID_DISPATCH_D(d, PICK_D)
+#undef PICK_D
+#undef PICK
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGT, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
+  }
   int nchunks = std::max(1, c->sms * per_sm / nparts);
   nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, ntiles));
   // scratch: blist | partial | partial_sk
@@ -460,7 +661,8 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   A.m = m;
   A.r = (int)r;
   A.meff = meff;
-  A.denom = 2.0 * h * h;
+  A.negc = -1.0 / (2.0 * h * h);
+  A.cscale = std::sqrt(1.0 / (2.0 * h * h));
   A.P2 = r > 0 ? c->P2 : nullptr;
   A.blist = d_blist;
   A.nparts = nparts;
@@ -469,25 +671,66 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   A.partial = partial;
   A.LG = LG;
   A.partial_sk = partial_sk;
+  A.dbg = getenv("KID_GRAM_DEBUG") ? atoi(getenv("KID_GRAM_DEBUG")) : 0;
+  A.trace = nullptr;
+  const bool tracing = getenv("KID_GRAM_TRACE") != nullptr;
+  const size_t trace_n = (size_t)(kMW + kEW) * kTraceTiles * 4;
+  if (tracing) {
+    KID_CK(c, cudaMalloc(&A.trace, sizeof(long long) * trace_n));
+    KID_CK(c, cudaMemsetAsync(A.trace, 0, sizeof(long long) * trace_n, c->stream));
+  }
   dim3 grid(nchunks, nparts);
 #define LAUNCH_B(DD, BB)                                                                           \
   {                                                                                                \
     cudaFuncSetAttribute(k_gram<DD, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    k_gram<DD, BB><<<grid, kNT, smem, c->stream>>>(A);                                             \
+    k_gram<DD, BB><<<grid, kGT, smem, c->stream>>>(A);                                             \
   }
-#define LAUNCH(DD)                     \
-  switch (BPW) {                       \
-    case 4: LAUNCH_B(DD, 4); break;    \
-    case 8: LAUNCH_B(DD, 8); break;    \
-    case 12: LAUNCH_B(DD, 12); break;  \
-    case 16: LAUNCH_B(DD, 16); break;  \
-    default: LAUNCH_B(DD, 24); break;  \
+#define LAUNCH(DD)                   \
+  switch (TPW) {                     \
+    case 1: LAUNCH_B(DD, 1); break;  \
+    case 2: LAUNCH_B(DD, 2); break;  \
+    case 3: LAUNCH_B(DD, 3); break;  \
+    case 4: LAUNCH_B(DD, 4); break;  \
+    default: LAUNCH_B(DD, 5); break; \
   }
+  prof_begin(c);
   KID_DISPATCH_D(d, LAUNCH)
 #undef LAUNCH
 #undef LAUNCH_B
+  prof_end(c);
   KID_LAUNCHED(c);
-  k_gram_reduce<<<std::max(1, std::min(c->sms * 4, (meff * meff + 255) / 256)), 256, 0, c->stream>>>(
+  if (tracing) {
+    std::vector<long long> tr(trace_n);
+    KID_CK(c, cudaMemcpyAsync(tr.data(), A.trace, sizeof(long long) * trace_n, cudaMemcpyDeviceToHost, c->stream));
+    KID_CK(c, cudaStreamSynchronize(c->stream));
+    cudaFree(A.trace);
+    // per-phase mean cycles over tiles 4..kTraceTiles-1 (steady state), MMA warp 0 and eval warp kMW
+    auto at = [&](int w, int it, int ev) { return tr[((size_t)w * kTraceTiles + it) * 4 + ev]; };
+    double mw_full = 0, mw_g1 = 0, mw_syrk = 0, ew_empty = 0, ew_eval = 0, tile = 0;
+    int n = 0;
+    for (int it = 4; it + 1 < kTraceTiles; ++it) {
+      if (!at(0, it + 1, 0)) break;
+      mw_full += at(0, it, 1) - at(0, it, 0);
+      mw_g1 += at(0, it, 2) - at(0, it, 1);
+      mw_syrk += at(0, it, 3) - at(0, it, 2);
+      ew_empty += at(kMW, it, 1) - at(kMW, it, 0);
+      ew_eval += at(kMW, it, 2) - at(kMW, it, 1);
+      tile += at(0, it + 1, 0) - at(0, it, 0);
+      ++n;
+    }
+    for (int it = 10; it < 12; ++it) {
+      fprintf(stderr, "[kid trace] tile %d, stamps rel. to MMA warp 0 event 0:", it);
+      for (int w = 0; w < kMW + kEW; ++w)
+        fprintf(stderr, " w%d[%lld %lld %lld %lld]", w, at(w, it, 0) - at(0, it, 0), at(w, it, 1) - at(0, it, 0),
+                at(w, it, 2) - at(0, it, 0), at(w, it, 3) - at(0, it, 0));
+      fprintf(stderr, "\n");
+    }
+    if (n)
+      fprintf(stderr, "[kid trace] cycles/tile: tile %.0f | mma: wait_full %.0f gemm1+bar %.0f syrk %.0f | "
+                      "eval: wait_empty %.0f eval %.0f (n=%d)\n",
+              tile / n, mw_full / n, mw_g1 / n, mw_syrk / n, ew_empty / n, ew_eval / n, n);
+  }
+  k_gram_reduce<<<std::max(1, std::min(c->sms * 2, (meff * meff + 31) / 32)), 1024, 0, c->stream>>>(
       partial, nchunks, LG, meff, partial_sk, d_out);
   KID_LAUNCHED(c);
   k_gram_finish<<<1, 32, 0, c->stream>>>(partial_sk, nchunks, meff, d_out);
@@ -506,7 +749,8 @@ int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_s
   bool w_in_smem = smem + wbytes <= 200 * 1024;
   if (w_in_smem) smem += wbytes;
   if (smem > 220 * 1024) return fail(c, KID_E_DIM, "leverage: tile does not fit shared memory");
-  LevArgs A{view(c), d, c->src, m, rr, 2.0 * h * h, d_W, w_in_smem, d_scores};
+  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
+  LevArgs A{view(c), d, c->src, m, rr, -1.0 / (2.0 * h * h), d_W, w_in_smem, d_scores};
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;
   const int blocks = (int)std::min<int64_t>(ntiles, (int64_t)c->sms * 2);
 #define LAUNCH(DD)                                                                                \
@@ -514,8 +758,17 @@ int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_s
     cudaFuncSetAttribute(k_leverage<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     k_leverage<DD><<<blocks, kNT, smem, c->stream>>>(A);                                          \
   }
+  prof_begin(c);
   KID_DISPATCH_D(d, LAUNCH)
+  prof_end(c);
 #undef LAUNCH
+  KID_LAUNCHED(c);
+  return KID_OK;
+}
+
+int exp_check_dev(kid_ctx* c, const double* d_x, int64_t n, double* d_y) {
+  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
+  k_exp_check<<<(int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sms * 8), 256, 0, c->stream>>>(d_x, n, d_y);
   KID_LAUNCHED(c);
   return KID_OK;
 }

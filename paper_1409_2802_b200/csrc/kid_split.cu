@@ -294,7 +294,9 @@ int split_candidates(kid_ctx* c, const double* center_h, int64_t n, double* cand
     cudaFree(tmp);
   }
   const int blocks = c->sms * 8;
+  prof_begin(c);
   k_dist_cand<<<blocks, 256, 0, c->stream>>>(c->pts, N, d, center, T_key, c->dist, ck, ci, count, cap);
+  prof_end(c);
   KID_LAUNCHED(c);
   unsigned long long cnt = 0;
   KID_CK(c, cudaMemcpyAsync(&cnt, count, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
@@ -370,8 +372,10 @@ int split_finish(kid_ctx* c, const int64_t* src_idx_h, int64_t n, const double* 
   KID_CK(c, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ntiles, c->stream));
   KID_CK(c, cudaMemsetAsync(c->counter, 0, sizeof(int64_t) * 2, c->stream));
   const double cutoff = xi * rho;  // geometry.hpp:57
+  prof_begin(c);
   k_compact<<<(unsigned)ntiles, kCT, 0, c->stream>>>(c->dist, N, cutoff, rho, src_local, nloc, c->tgt_idx, status,
                                                      (unsigned int*)c->counter, c->counter + 1, ntiles);
+  prof_end(c);
   KID_LAUNCHED(c);
   int64_t nt = 0;
   KID_CK(c, cudaMemcpyAsync(&nt, c->counter + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));

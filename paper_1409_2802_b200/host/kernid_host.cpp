@@ -1,0 +1,1045 @@
+// kernid_host.cpp -- host side of the B200 far-field path: the C++ mirror of the reference
+// kernid:: API (include/kernid_b200.hpp) over the C-ABI of include/kernid_cuda.h, plus the
+// small host-resident steps the north star keeps on the host (ID / pivoted QR on the
+// sampled rows, epsilon-rank, weighted draws). Built with -ffp-contract=off like the
+// reference (proj/CMakeLists.txt:12-15) so host-evaluated K_s rows are bit-identical.
+#include "kernid_b200.hpp"
+
+#include <algorithm>
+#include <charconv>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <map>
+#include <numeric>
+#include <sstream>
+#include <tuple>
+
+namespace kernid_b200 {
+
+// ------------------------------------------------------------------ errors
+void throw_status(int code, const std::string& msg) {
+  switch (code) {
+    case KID_E_RANGE: throw RangeError(msg);
+    case KID_E_DIM: throw DimensionError(msg);
+    case KID_E_NO_TARGETS: throw NoTargetsError(msg);
+    case KID_E_NUMERICAL: throw NumericalError(msg);
+    case KID_E_ILLCOND: throw IllConditionedSkeletonError(msg);
+    case KID_E_CONFIG: throw ConfigError(msg);
+    default: throw Error(msg);
+  }
+}
+
+// ------------------------------------------------------------------ rng.hpp
+std::uint64_t splitmix64(std::uint64_t& state) {
+  std::uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+std::uint64_t derive_seed(std::uint64_t master, std::uint64_t key_a, std::uint64_t key_b) {
+  std::uint64_t state = master;
+  state ^= splitmix64(state) + key_a;
+  state ^= splitmix64(state) + key_b;
+  return splitmix64(state);
+}
+
+std::uint64_t Rng::below(std::uint64_t n) {
+  const std::uint64_t limit = n * ((~std::uint64_t{0}) / n);
+  std::uint64_t x;
+  do {
+    x = engine_();
+  } while (x >= limit);
+  return x % n;
+}
+
+double Rng::normal() {
+  if (has_spare_) {
+    has_spare_ = false;
+    return spare_;
+  }
+  const double u1 = 1.0 - uniform01();
+  const double u2 = uniform01();
+  const double radius = std::sqrt(-2.0 * std::log(u1));
+  const double angle = 2.0 * M_PI * u2;
+  spare_ = radius * std::sin(angle);
+  has_spare_ = true;
+  return radius * std::cos(angle);
+}
+
+// ------------------------------------------------------------------ kernel / datagen
+void KernelSpec::validate() const {
+  if (!(h > 0.0)) throw ConfigError("Gaussian kernel requires bandwidth h > 0");
+}
+
+PointSet gen_normal(int d, int64_t N, std::uint64_t seed) {
+  if (d < 1 || N < 1) throw RangeError("gen_normal: requires d >= 1 and N >= 1");
+  Rng rng(seed);
+  PointSet ps(N, d);
+  for (int64_t i = 0; i < N; ++i)
+    for (int j = 0; j < d; ++j) ps(i, j) = rng.normal();
+  return ps;
+}
+
+double silverman_bandwidth(int d, long long N) {
+  if (d < 1 || N < 1) throw RangeError("silverman_bandwidth: requires d >= 1 and N >= 1");
+  const double e = 1.0 / (static_cast<double>(d) + 4.0);
+  return std::pow(4.0 / (2.0 * d + 1.0), e) * std::pow(static_cast<double>(N), -e);
+}
+
+double eval_kernel(const KernelSpec& spec, const double* x, int64_t sx, const double* y, int64_t sy, int d) {
+  double acc = 0.0;  // kernel.hpp:60-68
+  for (int k = 0; k < d; ++k) {
+    const double diff = x[k * sx] - y[k * sy];
+    acc += diff * diff;
+  }
+  return std::exp(-acc / (2.0 * spec.h * spec.h));  // kernel.hpp:77-79
+}
+
+// ------------------------------------------------------------------ device
+Device::Device(int device) {
+  const int rc = kid_create(&ctx_, device);
+  if (rc) throw_status(rc, "kid_create: no usable CUDA device " + std::to_string(device));
+}
+Device::~Device() { kid_destroy(ctx_); }
+void Device::check(int status) const {
+  if (status) throw_status(status, kid_last_error(ctx_));
+}
+
+// ------------------------------------------------------------------ geometry
+SourceTargetSplit split_sources_targets(Device& dev, const PointSet& ps, const std::vector<double>& x_c, int64_t n,
+                                        double xi) {
+  const int64_t N = ps.rows;
+  if (n < 1 || n >= N) throw RangeError("split_sources_targets: requires 1 <= n < N");
+  if (xi < 0.0) throw RangeError("split_sources_targets: requires xi >= 0");
+  if (static_cast<int64_t>(x_c.size()) != ps.cols)
+    throw DimensionError("split_sources_targets: center dimension mismatch");
+  dev.check(kid_set_points(dev.ctx(), ps.data(), N, static_cast<int32_t>(ps.cols), 0));
+  SourceTargetSplit split;
+  split.center = x_c;
+  split.xi = xi;
+  split.source_indices.resize(static_cast<size_t>(n));
+  int64_t nt = 0;
+  dev.check(kid_split(dev.ctx(), x_c.data(), n, xi, split.source_indices.data(), &split.rho, &nt));
+  split.target_indices.resize(static_cast<size_t>(nt));
+  dev.check(kid_get_targets(dev.ctx(), split.target_indices.data(), nt));
+  return split;
+}
+
+KernelBlock::KernelBlock(Device& dev, KernelSpec spec, const PointSet& points, const SourceTargetSplit& split)
+    : dev_(&dev), spec_(spec), points_(&points), split_(&split) {
+  spec_.validate();
+}
+
+Matrix KernelBlock::rows_exact(const std::vector<int64_t>& idx) const {
+  const int64_t m = cols();
+  const int d = static_cast<int>(points_->cols);
+  const int64_t N = points_->rows;
+  Matrix sub(static_cast<int64_t>(idx.size()), m);
+  for (size_t i = 0; i < idx.size(); ++i) {
+    if (idx[i] < 0 || idx[i] >= rows()) throw RangeError("row sample index out of range");
+    const double* t = points_->data() + split_->target_indices[static_cast<size_t>(idx[i])];
+    for (int64_t j = 0; j < m; ++j) {
+      const double* s = points_->data() + split_->source_indices[static_cast<size_t>(j)];
+      sub(static_cast<int64_t>(i), j) = eval_kernel(spec_, t, N, s, N, d);
+    }
+  }
+  return sub;
+}
+
+std::vector<double> KernelBlock::row_norms() const {
+  std::vector<double> w(static_cast<size_t>(rows()));
+  dev_->check(kid_row_norms(dev_->ctx(), spec_.h, w.data()));
+  return w;
+}
+
+Matrix KernelBlock::gram(double* sumsq) const {
+  Matrix G(cols(), cols());
+  dev_->check(kid_gram(dev_->ctx(), spec_.h, G.data(), sumsq));
+  return G;
+}
+
+double KernelBlock::spectral_norm() const {
+  std::vector<double> ev;
+  sym_eig(gram(), ev, nullptr);
+  return ev.empty() ? 0.0 : std::sqrt(std::max(ev[0], 0.0));
+}
+
+// ------------------------------------------------------------------ lowrank (host)
+namespace {
+
+// Householder QR R factor of a tall (rows >= cols) matrix.
+Matrix qr_r(const Matrix& A_in) {
+  Matrix A = A_in;
+  const int64_t rows = A.rows, cols = A.cols;
+  std::vector<double> v(static_cast<size_t>(rows));
+  for (int64_t j = 0; j < cols; ++j) {
+    double nrm = 0.0;
+    for (int64_t i = j; i < rows; ++i) nrm += A(i, j) * A(i, j);
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) continue;
+    const double alpha = A(j, j);
+    const double beta = alpha >= 0.0 ? -nrm : nrm;
+    const double v0 = alpha - beta;
+    const double tau = -v0 / beta;
+    const int64_t len = rows - j;
+    v[0] = 1.0;
+    for (int64_t i = 1; i < len; ++i) v[static_cast<size_t>(i)] = A(j + i, j) / v0;
+    A(j, j) = beta;
+    for (int64_t k = j + 1; k < cols; ++k) {
+      double w = 0.0;
+      for (int64_t i = 0; i < len; ++i) w += v[static_cast<size_t>(i)] * A(j + i, k);
+      w *= tau;
+      for (int64_t i = 0; i < len; ++i) A(j + i, k) -= w * v[static_cast<size_t>(i)];
+    }
+  }
+  Matrix R(cols, cols);
+  for (int64_t c = 0; c < cols; ++c)
+    for (int64_t r = 0; r <= c; ++r) R(r, c) = A(r, c);
+  return R;
+}
+
+// One-sided Jacobi: singular values (descending) of a square matrix.
+std::vector<double> jacobi_sv(Matrix U) {
+  const int64_t n = U.cols, rows = U.rows;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    int64_t rotated = 0;
+    for (int64_t p = 0; p + 1 < n; ++p)
+      for (int64_t q = p + 1; q < n; ++q) {
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int64_t i = 0; i < rows; ++i) {
+          a += U(i, p) * U(i, p);
+          b += U(i, q) * U(i, q);
+          g += U(i, p) * U(i, q);
+        }
+        if (g == 0.0 || std::fabs(g) <= 1e-15 * std::sqrt(a) * std::sqrt(b)) continue;
+        ++rotated;
+        const double zeta = (b - a) / (2.0 * g);
+        const double t = std::fabs(zeta) > 1e150 ? 0.5 / zeta
+                                                   : (zeta >= 0.0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), s = c * t;
+        for (int64_t i = 0; i < rows; ++i) {
+          const double x = U(i, p), y = U(i, q);
+          U(i, p) = c * x - s * y;
+          U(i, q) = s * x + c * y;
+        }
+      }
+    if (!rotated) break;
+  }
+  std::vector<double> sv(static_cast<size_t>(n));
+  for (int64_t j = 0; j < n; ++j) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < rows; ++i) acc += U(i, j) * U(i, j);
+    sv[static_cast<size_t>(j)] = std::sqrt(acc);
+  }
+  std::sort(sv.begin(), sv.end(), std::greater<double>());
+  return sv;
+}
+
+Matrix transpose(const Matrix& A) {
+  Matrix T(A.cols, A.rows);
+  for (int64_t j = 0; j < A.cols; ++j)
+    for (int64_t i = 0; i < A.rows; ++i) T(j, i) = A(i, j);
+  return T;
+}
+
+}  // namespace
+
+std::vector<double> singular_values(const Matrix& A) {
+  if (A.rows == 0 || A.cols == 0) throw RangeError("singular_values: empty matrix");
+  if (A.rows >= A.cols) return jacobi_sv(qr_r(A));
+  return jacobi_sv(qr_r(transpose(A)));
+}
+
+int64_t epsilon_rank(const std::vector<double>& sv, double eps, std::optional<double> reference_sigma1) {
+  if (!(eps > 0.0 && eps < 1.0)) throw RangeError("epsilon_rank: requires eps in (0, 1)");
+  if (sv.empty()) return 0;
+  const double ref = reference_sigma1.value_or(sv[0]);
+  if (!(ref > 0.0)) return 0;
+  for (size_t r = 0; r < sv.size(); ++r)
+    if (sv[r] < eps * ref) return static_cast<int64_t>(r);
+  return static_cast<int64_t>(sv.size());
+}
+
+// lowrank.hpp:135-262, restated with sequential single-accumulator reductions.
+IDFactorization interpolative_decomposition(const Matrix& A, int64_t r) {
+  const int64_t m = A.rows, n = A.cols;
+  if (r < 1 || r > std::min(m, n)) throw RangeError("interpolative_decomposition: requires 1 <= r <= min(m, n)");
+  Matrix W = A;
+  std::vector<int64_t> perm(static_cast<size_t>(n));
+  std::iota(perm.begin(), perm.end(), int64_t{0});
+  std::vector<double> colnorm2(static_cast<size_t>(n)), refnorm2;
+  for (int64_t j = 0; j < n; ++j) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < m; ++i) acc += W(i, j) * W(i, j);
+    colnorm2[static_cast<size_t>(j)] = acc;
+  }
+  refnorm2 = colnorm2;
+  std::vector<double> v(static_cast<size_t>(m)), w(static_cast<size_t>(n));
+  constexpr double recompute_ratio = 2.3e-16;
+  for (int64_t k = 0; k < r; ++k) {
+    int64_t piv = k;
+    for (int64_t j = k + 1; j < n; ++j)
+      if (colnorm2[static_cast<size_t>(j)] > colnorm2[static_cast<size_t>(piv)]) piv = j;
+    if (piv != k) {
+      for (int64_t i = 0; i < m; ++i) std::swap(W(i, k), W(i, piv));
+      std::swap(colnorm2[static_cast<size_t>(k)], colnorm2[static_cast<size_t>(piv)]);
+      std::swap(refnorm2[static_cast<size_t>(k)], refnorm2[static_cast<size_t>(piv)]);
+      std::swap(perm[static_cast<size_t>(k)], perm[static_cast<size_t>(piv)]);
+    }
+    const int64_t len = m - k;
+    double normx = 0.0;
+    for (int64_t i = k; i < m; ++i) normx += W(i, k) * W(i, k);
+    normx = std::sqrt(normx);
+    if (normx == 0.0) continue;
+    const double alpha = W(k, k);
+    const double beta = (alpha >= 0.0) ? -normx : normx;
+    const double v0 = alpha - beta;
+    const double tau = -v0 / beta;
+    for (int64_t i = 1; i < len; ++i) W(k + i, k) /= v0;
+    W(k, k) = beta;
+    if (k + 1 < n && len > 0) {
+      v[0] = 1.0;
+      for (int64_t i = 1; i < len; ++i) v[static_cast<size_t>(i)] = W(k + i, k);
+      for (int64_t j = k + 1; j < n; ++j) {
+        double acc = 0.0;
+        for (int64_t i = 0; i < len; ++i) acc += v[static_cast<size_t>(i)] * W(k + i, j);
+        w[static_cast<size_t>(j)] = tau * acc;
+      }
+      for (int64_t j = k + 1; j < n; ++j)
+        for (int64_t i = 0; i < len; ++i) W(k + i, j) -= v[static_cast<size_t>(i)] * w[static_cast<size_t>(j)];
+    }
+    for (int64_t j = k + 1; j < n; ++j) {
+      const double t = W(k, j);
+      double& cn = colnorm2[static_cast<size_t>(j)];
+      cn -= t * t;
+      if (cn < recompute_ratio * refnorm2[static_cast<size_t>(j)] || cn < 0.0) {
+        double acc = 0.0;
+        for (int64_t i = k + 1; i < m; ++i) acc += W(i, j) * W(i, j);
+        cn = (m - k - 1 > 0) ? acc : 0.0;
+        refnorm2[static_cast<size_t>(j)] = cn;
+      }
+    }
+  }
+  const double lead = std::fabs(W(0, 0));
+  const double tail = std::fabs(W(r - 1, r - 1));
+  if (!(lead > 0.0) || tail < 10.0 * std::numeric_limits<double>::epsilon() * lead)
+    throw IllConditionedSkeletonError("interpolative_decomposition: pivot " + std::to_string(r) +
+                                      " is numerically negligible; reduce the requested rank");
+  IDFactorization id;
+  id.rank = r;
+  id.skeleton.assign(perm.begin(), perm.begin() + r);
+  id.projection = Matrix(r, n);
+  for (int64_t i = 0; i < r; ++i) id.projection(i, perm[static_cast<size_t>(i)]) = 1.0;
+  std::vector<double> x(static_cast<size_t>(r));
+  for (int64_t j = 0; j < n - r; ++j) {
+    for (int64_t i = 0; i < r; ++i) x[static_cast<size_t>(i)] = W(i, r + j);
+    for (int64_t i = r - 1; i >= 0; --i) {
+      x[static_cast<size_t>(i)] /= W(i, i);
+      for (int64_t k = 0; k < i; ++k) x[static_cast<size_t>(k)] -= x[static_cast<size_t>(i)] * W(k, i);
+    }
+    const int64_t col = perm[static_cast<size_t>(r + j)];
+    for (int64_t i = 0; i < r; ++i) id.projection(i, col) = x[static_cast<size_t>(i)];
+  }
+  return id;
+}
+
+// Cyclic Jacobi eigen-solver for the symmetric m x m Grams (descending eigenvalues).
+void sym_eig(const Matrix& A_in, std::vector<double>& evals, Matrix* evecs) {
+  Matrix A = A_in;
+  const int64_t n = A.rows;
+  Matrix V(n, n);
+  for (int64_t i = 0; i < n; ++i) V(i, i) = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int64_t p = 0; p < n; ++p) {
+      diag += A(p, p) * A(p, p);
+      for (int64_t q = p + 1; q < n; ++q) off += A(p, q) * A(p, q);
+    }
+    if (off == 0.0 || off <= 1e-32 * diag) break;
+    for (int64_t p = 0; p < n; ++p)
+      for (int64_t q = p + 1; q < n; ++q) {
+        const double apq = A(p, q);
+        if (apq == 0.0) continue;
+        const double theta = (A(q, q) - A(p, p)) / (2.0 * apq);
+        const double t = std::fabs(theta) > 1e150
+                             ? 0.5 / theta
+                             : (theta >= 0.0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int64_t k = 0; k < n; ++k) {
+          const double akp = A(k, p), akq = A(k, q);
+          A(k, p) = c * akp - s * akq;
+          A(k, q) = s * akp + c * akq;
+        }
+        for (int64_t k = 0; k < n; ++k) {
+          const double apk = A(p, k), aqk = A(q, k);
+          A(p, k) = c * apk - s * aqk;
+          A(q, k) = s * apk + c * aqk;
+        }
+        if (evecs)
+          for (int64_t k = 0; k < n; ++k) {
+            const double vkp = V(k, p), vkq = V(k, q);
+            V(k, p) = c * vkp - s * vkq;
+            V(k, q) = s * vkp + c * vkq;
+          }
+      }
+  }
+  std::vector<int64_t> order(static_cast<size_t>(n));
+  std::iota(order.begin(), order.end(), int64_t{0});
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return A(a, a) > A(b, b); });
+  evals.resize(static_cast<size_t>(n));
+  if (evecs) *evecs = Matrix(n, n);
+  for (int64_t i = 0; i < n; ++i) {
+    evals[static_cast<size_t>(i)] = A(order[static_cast<size_t>(i)], order[static_cast<size_t>(i)]);
+    if (evecs)
+      for (int64_t k = 0; k < n; ++k) (*evecs)(k, i) = V(k, order[static_cast<size_t>(i)]);
+  }
+}
+
+LeverageScores row_leverage_scores(const KernelBlock& K, int64_t r) {
+  const int64_t mn = std::min(K.rows(), K.cols());
+  if (r < 1 || r > mn) throw RangeError("row_leverage_scores: requires 1 <= r <= min(m, n)");
+  std::vector<double> ev;
+  Matrix V;
+  sym_eig(K.gram(), ev, &V);
+  const int64_t m = K.cols();
+  std::vector<double> sv(static_cast<size_t>(m));
+  for (int64_t i = 0; i < m; ++i) sv[static_cast<size_t>(i)] = std::sqrt(std::max(ev[static_cast<size_t>(i)], 0.0));
+  if (!(sv[static_cast<size_t>(r - 1)] > 0.0))
+    throw NumericalError("row_leverage_scores: sigma_r vanishes; scores undefined");
+  Matrix W(m, r);  // lowrank.hpp:304
+  for (int64_t j = 0; j < r; ++j)
+    for (int64_t i = 0; i < m; ++i) W(i, j) = V(i, j) * (1.0 / sv[static_cast<size_t>(j)]);
+  LeverageScores out;
+  out.scores.resize(static_cast<size_t>(K.rows()));
+  K.device().check(kid_leverage(K.device().ctx(), K.spec().h, W.data(), r, out.scores.data()));
+  out.degenerate_gap = (r < m) && (sv[static_cast<size_t>(r - 1)] - sv[static_cast<size_t>(r)] <=
+                                   1e-12 * sv[static_cast<size_t>(r - 1)]);
+  return out;
+}
+
+// ------------------------------------------------------------------ sampling
+std::string SamplingScheme::name() const {
+  std::string base;
+  switch (kind) {
+    case SchemeKind::Uniform: base = "uniform"; break;
+    case SchemeKind::Bernoulli: base = "bernoulli"; break;
+    case SchemeKind::EuclideanNorm: base = "euclidean_norm"; break;
+    case SchemeKind::Distance: base = distance_direct ? "distance_direct" : "distance"; break;
+    case SchemeKind::Leverage: base = "leverage"; break;
+    case SchemeKind::NearestNeighbor: base = "nearest_neighbor"; break;
+  }
+  if (replacement && (kind == SchemeKind::Uniform || kind == SchemeKind::EuclideanNorm)) base += "_wr";
+  return base;
+}
+
+int64_t sample_count(double s, int64_t m) {
+  if (!(s > 0.0 && s <= 1.0)) throw RangeError("sample fraction must lie in (0, 1]");
+  const int64_t c = static_cast<int64_t>(std::ceil(s * static_cast<double>(m)));
+  return std::max<int64_t>(1, std::min(c, m));
+}
+
+namespace {
+class WeightTree {  // Fenwick tree (sampling.hpp:78-104)
+ public:
+  explicit WeightTree(const std::vector<double>& w) : n_(w.size()), tree_(w.size() + 1, 0.0) {
+    for (size_t i = 0; i < n_; ++i) add(i, w[i]);
+  }
+  size_t find(double u) const {
+    size_t pos = 0, mask = 1;
+    while ((mask << 1) <= n_) mask <<= 1;
+    for (; mask > 0; mask >>= 1) {
+      const size_t next = pos + mask;
+      if (next <= n_ && tree_[next] <= u) {
+        u -= tree_[next];
+        pos = next;
+      }
+    }
+    return std::min(pos, n_ - 1);
+  }
+  void add(size_t i, double delta) {
+    for (size_t k = i + 1; k <= n_; k += k & (~k + 1)) tree_[k] += delta;
+  }
+
+ private:
+  size_t n_;
+  std::vector<double> tree_;
+};
+
+double center_distance(const PointSet& ps, int64_t pt, const std::vector<double>& c) {
+  double diff = ps(pt, 0) - c[0];
+  double acc = diff * diff;
+  for (int64_t k = 1; k < ps.cols; ++k) {
+    diff = ps(pt, k) - c[static_cast<size_t>(k)];
+    acc += diff * diff;
+  }
+  return std::sqrt(acc);
+}
+}  // namespace
+
+std::vector<int64_t> weighted_draw(const std::vector<double>& weights, int64_t count, bool replacement, Rng& rng) {
+  const size_t m = weights.size();
+  double total = std::accumulate(weights.begin(), weights.end(), 0.0);
+  for (double w : weights)
+    if (w < 0.0 || !std::isfinite(w)) throw RangeError("sample_rows: invalid (negative or non-finite) weight");
+  if (!(total > 0.0)) throw Error("sample_rows: zero total weight");
+  std::vector<int64_t> out;
+  out.reserve(static_cast<size_t>(count));
+  if (replacement) {
+    std::vector<double> cum(m);
+    std::partial_sum(weights.begin(), weights.end(), cum.begin());
+    for (int64_t k = 0; k < count; ++k) {
+      const double u = rng.uniform01() * total;
+      size_t idx = static_cast<size_t>(std::upper_bound(cum.begin(), cum.end(), u) - cum.begin());
+      if (idx >= m) idx = m - 1;
+      out.push_back(static_cast<int64_t>(idx));
+    }
+    return out;
+  }
+  WeightTree tree(weights);
+  std::vector<double> live = weights;
+  for (int64_t k = 0; k < count; ++k) {
+    const double u = rng.uniform01() * total;
+    size_t idx = tree.find(u);
+    if (live[idx] <= 0.0) {
+      size_t probe = idx;
+      while (probe + 1 < m && live[probe] <= 0.0) ++probe;
+      while (probe > 0 && live[probe] <= 0.0) --probe;
+      idx = probe;
+    }
+    out.push_back(static_cast<int64_t>(idx));
+    total -= live[idx];
+    tree.add(idx, -live[idx]);
+    live[idx] = 0.0;
+    if (!(total > 0.0) && k + 1 < count) throw Error("sample_rows: weights exhausted before reaching the requested count");
+  }
+  return out;
+}
+
+RowSample sample_rows(const SamplingScheme& scheme, const SampleContext& ctx, double s, std::uint64_t seed) {
+  if (ctx.m < 1) throw RangeError("sample_rows: context must have m >= 1 rows");
+  RowSample out;
+  out.fraction = s;
+  out.seed = seed;
+  Rng rng(seed);
+  const int64_t m = ctx.m;
+  switch (scheme.kind) {
+    case SchemeKind::Uniform: {
+      const int64_t count = sample_count(s, m);
+      if (scheme.replacement) {
+        for (int64_t k = 0; k < count; ++k) out.indices.push_back(static_cast<int64_t>(rng.below(static_cast<std::uint64_t>(m))));
+      } else {
+        std::vector<int64_t> pool(static_cast<size_t>(m));
+        std::iota(pool.begin(), pool.end(), int64_t{0});
+        for (int64_t k = 0; k < count; ++k) {
+          const size_t j = static_cast<size_t>(k) + static_cast<size_t>(rng.below(static_cast<std::uint64_t>(m - k)));
+          std::swap(pool[static_cast<size_t>(k)], pool[j]);
+          out.indices.push_back(pool[static_cast<size_t>(k)]);
+        }
+      }
+      break;
+    }
+    case SchemeKind::Bernoulli: {
+      if (!(s > 0.0 && s <= 1.0)) throw RangeError("sample fraction must lie in (0, 1]");
+      for (int64_t i = 0; i < m; ++i)
+        if (rng.uniform01() < s) out.indices.push_back(i);
+      break;
+    }
+    case SchemeKind::EuclideanNorm: {
+      if (ctx.K == nullptr) throw Error("sample_rows: EuclideanNorm scheme requires the matrix K");
+      if (ctx.K->rows() != m) throw DimensionError("sample_rows: K row count disagrees with context m");
+      const std::vector<double> w = ctx.K->row_norms();  // pass 2a on the device
+      out.indices = weighted_draw(w, sample_count(s, m), scheme.replacement, rng);
+      break;
+    }
+    case SchemeKind::Distance: {
+      if (ctx.split == nullptr || ctx.points == nullptr)
+        throw Error("sample_rows: Distance scheme requires the source/target split and points");
+      if (static_cast<int64_t>(ctx.split->target_indices.size()) != m)
+        throw DimensionError("sample_rows: split target count disagrees with context m");
+      std::vector<double> w(static_cast<size_t>(m));
+      for (int64_t i = 0; i < m; ++i) {
+        const double dist = center_distance(*ctx.points, ctx.split->target_indices[static_cast<size_t>(i)], ctx.split->center);
+        w[static_cast<size_t>(i)] = scheme.distance_direct ? dist : 1.0 / std::max(dist, std::numeric_limits<double>::min());
+      }
+      out.indices = weighted_draw(w, sample_count(s, m), false, rng);
+      break;
+    }
+    case SchemeKind::Leverage: {
+      if (ctx.K == nullptr) throw Error("sample_rows: Leverage scheme requires the matrix K");
+      if (ctx.K->rows() != m) throw DimensionError("sample_rows: K row count disagrees with context m");
+      if (scheme.rank_for_leverage < 1) throw RangeError("sample_rows: rank_for_leverage must be >= 1");
+      const int64_t r = std::min(scheme.rank_for_leverage, std::min(ctx.K->rows(), ctx.K->cols()));
+      const std::vector<double> w = row_leverage_scores(*ctx.K, r).scores;  // pass 2b on the device
+      out.indices = weighted_draw(w, sample_count(s, m), false, rng);
+      break;
+    }
+    case SchemeKind::NearestNeighbor: {
+      if (ctx.split == nullptr || ctx.points == nullptr)
+        throw Error("sample_rows: NearestNeighbor scheme requires the source/target split and points");
+      if (static_cast<int64_t>(ctx.split->target_indices.size()) != m)
+        throw DimensionError("sample_rows: split target count disagrees with context m");
+      const int64_t count = sample_count(s, m);
+      std::vector<std::pair<double, int64_t>> by_dist;
+      by_dist.reserve(static_cast<size_t>(m));
+      for (int64_t i = 0; i < m; ++i)
+        by_dist.emplace_back(center_distance(*ctx.points, ctx.split->target_indices[static_cast<size_t>(i)], ctx.split->center), i);
+      std::sort(by_dist.begin(), by_dist.end());
+      for (int64_t k = 0; k < count; ++k) out.indices.push_back(by_dist[static_cast<size_t>(k)].second);
+      break;
+    }
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ compress
+int64_t RankRule::resolve(const std::vector<double>& sv) const {
+  if (fixed_r) {
+    if (*fixed_r < 0) throw RangeError("rank rule: fixed rank must be nonnegative");
+    return std::min<int64_t>(*fixed_r, static_cast<int64_t>(sv.size()));
+  }
+  if (!eps) throw ConfigError("rank rule: either eps or fixed_r must be set");
+  return epsilon_rank(sv, *eps, reference_sigma1);
+}
+
+double bound_id_value(int64_t n, int64_t r, double sigma_r1) {
+  if (r < 0 || r > n) throw RangeError("bound_id_value: requires 0 <= r <= n");
+  const double nn = static_cast<double>(n), rr = static_cast<double>(r);
+  return std::sqrt(1.0 + nn * rr * (nn - rr)) * sigma_r1;
+}
+
+double reconstruction_bound(int64_t m, int64_t s_count, double eps, double sigma_r1) {
+  if (s_count < 1) throw RangeError("reconstruction_bound: requires s_count >= 1");
+  if (!(eps > 0.0 && eps < 1.0)) throw RangeError("reconstruction_bound: requires eps in (0, 1)");
+  if (sigma_r1 < 0.0) throw RangeError("reconstruction_bound: requires sigma_r1 >= 0");
+  const double ratio = static_cast<double>(m) / static_cast<double>(s_count);
+  return std::sqrt(1.0 + ratio * (1.0 + eps) / ((1.0 - eps) * (1.0 - eps))) * sigma_r1;
+}
+
+namespace {
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+// compress.hpp:168-215 with the error pass on the device.
+std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, const RowSample& sample,
+                                                          const RankRule& rule, const CompressOptions& opts) {
+  if (sample.indices.empty()) throw RangeError("compress_id: empty row sample");
+  CompressionReport rep;
+  rep.fraction = sample.fraction;
+  rep.seed = sample.seed;
+  double t0 = now_ms();
+  const Matrix sub = K.rows_exact(sample.indices);
+  rep.timings.sample_ms = now_ms() - t0;
+  t0 = now_ms();
+  const std::vector<double> sv = singular_values(sub);
+  const int64_t r = rule.resolve(sv);
+  rep.rank = r;
+  rep.sigma1_sample = sv[0];
+  rep.sigma_r1_sample = (r < static_cast<int64_t>(sv.size())) ? sv[static_cast<size_t>(r)] : 0.0;
+  rep.bound_id = bound_id_value(K.cols(), r, rep.sigma_r1_sample);
+  IDFactorization id;
+  if (r == 0) {
+    rep.rank_zero = true;
+    rep.timings.factor_ms = now_ms() - t0;
+    rep.rel_error = 1.0;
+    rep.rel_error_fro = 1.0;
+  } else {
+    id = interpolative_decomposition(sub, r);
+    rep.timings.factor_ms = now_ms() - t0;
+    t0 = now_ms();
+    const int64_t m = K.cols();
+    Matrix DtD(m, m);
+    double sd = 0.0, sk = 0.0;
+    K.device().check(kid_recon_error(K.device().ctx(), K.spec().h, id.skeleton.data(), r, id.projection.data(),
+                                     KID_RECON_DTD, &sd, &sk, DtD.data(), nullptr));
+    std::vector<double> ev;
+    sym_eig(DtD, ev, nullptr);
+    const double num = std::sqrt(std::max(ev.empty() ? 0.0 : ev[0], 0.0));
+    const double den = opts.k_norm ? *opts.k_norm : K.spectral_norm();
+    rep.rel_error = (den > 0.0) ? num / den : 0.0;
+    rep.rel_error_fro = (sk > 0.0) ? std::sqrt(sd / sk) : 0.0;
+    rep.timings.error_ms = now_ms() - t0;
+  }
+  if (opts.full_spectrum) {
+    const auto& fs = *opts.full_spectrum;
+    const double sig = (r < static_cast<int64_t>(fs.size())) ? fs[static_cast<size_t>(r)] : 0.0;
+    rep.bound_sampling = reconstruction_bound(K.rows(), static_cast<int64_t>(sample.indices.size()), opts.theorem_eps, sig);
+  }
+  return {std::move(id), rep};
+}
+
+// ------------------------------------------------------------------ harness
+std::string format_double(double v) {
+  char buf[64];
+  const auto res = std::to_chars(buf, buf + sizeof(buf), v);
+  return std::string(buf, res.ptr);
+}
+
+namespace {
+std::string format_int(long long v) {
+  char buf[32];
+  const auto res = std::to_chars(buf, buf + sizeof(buf), v);
+  return std::string(buf, res.ptr);
+}
+double mean_of(const std::vector<double>& v) {
+  if (v.empty()) return 0.0;
+  double sum = 0.0;
+  for (double x : v) sum += x;
+  return sum / static_cast<double>(v.size());
+}
+double stddev_of(const std::vector<double>& v) {
+  if (v.size() < 2) return 0.0;
+  const double mu = mean_of(v);
+  double acc = 0.0;
+  for (double x : v) acc += (x - mu) * (x - mu);
+  return std::sqrt(acc / static_cast<double>(v.size() - 1));
+}
+std::string csv_join(const std::vector<std::string>& cells) {
+  std::string line;
+  for (size_t i = 0; i < cells.size(); ++i) {
+    if (i) line += ',';
+    line += cells[i];
+  }
+  return line;
+}
+const std::vector<std::string>& compress_csv_header() {
+  static const std::vector<std::string> header = {"dataset", "d", "N", "n", "xi", "kernel", "h", "method", "scheme",
+                                                  "s", "trial", "seed", "rank", "rel_error", "mc_error", "bound_id",
+                                                  "bound_sampling", "elapsed_ms"};
+  return header;
+}
+}  // namespace
+
+// harness.hpp:143-328 (Normal dataset, RandomPoint center, method "id").
+void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out, std::ostream* log) {
+  struct Accum {
+    std::vector<double> errors, ranks;
+  };
+  std::map<std::tuple<size_t, size_t>, Accum> accum;
+  struct Row {
+    std::tuple<size_t, size_t, int> key;
+    std::vector<std::string> cells;
+  };
+  std::vector<Row> rows;
+  for (size_t scheme_idx = 0; scheme_idx < cfg.schemes.size(); ++scheme_idx) {
+    for (int trial = 0; trial < cfg.trials; ++trial) {
+      const std::uint64_t data_seed = derive_seed(cfg.seed, static_cast<std::uint64_t>(trial), scheme_idx);
+      // prepare_trial (harness.hpp:107-129)
+      const PointSet points = gen_normal(cfg.d, cfg.N, derive_seed(data_seed, 0xDA7A));
+      Rng crng(derive_seed(data_seed, 0xCE));
+      const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(points.rows)));
+      std::vector<double> center(static_cast<size_t>(cfg.d));
+      for (int k = 0; k < cfg.d; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+      SourceTargetSplit split;
+      bool trial_failed = false;
+      try {
+        split = split_sources_targets(dev, points, center, cfg.n_sources, cfg.xi);
+      } catch (const NoTargetsError& e) {
+        trial_failed = true;
+        if (log) *log << "trial " << trial << " scheme " << cfg.schemes[scheme_idx].name() << ": " << e.what() << "\n";
+      }
+      const double h_abs = cfg.h_in_silverman_units ? cfg.h_value * silverman_bandwidth(cfg.d, cfg.N) : cfg.h_value;
+      SamplingScheme scheme = cfg.schemes[scheme_idx];
+      std::optional<std::vector<double>> full_sv;
+      RankRule rule = cfg.rank_rule;
+      std::optional<KernelBlock> K;
+      if (!trial_failed) {
+        K.emplace(dev, KernelSpec::gaussian(h_abs), points, split);
+        const bool auto_rank = scheme.kind == SchemeKind::Leverage && cfg.scheme_rank_auto[scheme_idx];
+        const bool need_full = cfg.rank_reference_full || cfg.emit_bound_sampling || auto_rank;
+        if (need_full) {  // Gram route for the full spectrum (harness.hpp:176-184)
+          std::vector<double> ev;
+          sym_eig(K->gram(), ev, nullptr);
+          std::vector<double> sv(ev.size());
+          for (size_t i = 0; i < ev.size(); ++i) sv[i] = std::sqrt(std::max(ev[i], 0.0));
+          full_sv = sv;
+        }
+        if (cfg.rank_reference_full) rule.reference_sigma1 = (*full_sv)[0];
+        if (auto_rank) scheme.rank_for_leverage = std::max<int64_t>(1, rule.resolve(*full_sv));
+      }
+      for (size_t s_idx = 0; s_idx < cfg.s_grid.size(); ++s_idx) {
+        const double s = cfg.s_grid[s_idx];
+        const std::uint64_t sample_seed = derive_seed(data_seed, s_idx, 1);
+        std::optional<RowSample> sample;
+        std::string sample_error;
+        if (!trial_failed) {
+          SampleContext ctx;
+          ctx.m = K->rows();
+          ctx.K = &*K;
+          ctx.split = &split;
+          ctx.points = &points;
+          try {
+            RowSample drawn = sample_rows(scheme, ctx, s, sample_seed);
+            if (drawn.indices.empty()) sample_error = "empty Bernoulli draw";
+            else sample = std::move(drawn);
+          } catch (const Error& e) {
+            sample_error = e.what();
+          }
+          if (!sample_error.empty() && log) *log << "trial " << trial << " s=" << s << ": " << sample_error << "\n";
+        }
+        std::vector<std::string> cells(compress_csv_header().size());
+        cells[0] = "normal";
+        cells[1] = format_int(cfg.d);
+        cells[2] = format_int(static_cast<long long>(cfg.N));
+        cells[3] = format_int(static_cast<long long>(cfg.n_sources));
+        cells[4] = format_double(cfg.xi);
+        cells[5] = "gaussian";
+        cells[6] = trial_failed ? "" : format_double(h_abs);
+        cells[7] = "id";
+        cells[8] = cfg.schemes[scheme_idx].name();
+        cells[9] = format_double(s);
+        cells[10] = format_int(trial);
+        cells[11] = format_int(static_cast<long long>(sample_seed));
+        if (!trial_failed && sample) {
+          CompressOptions opts;
+          opts.theorem_eps = cfg.theorem_eps;
+          if (full_sv && cfg.emit_bound_sampling) opts.full_spectrum = *full_sv;
+          if (full_sv) opts.k_norm = (*full_sv)[0];
+          const double t0 = now_ms();
+          auto [id, rep] = compress_id(*K, *sample, rule, opts);
+          const double elapsed = now_ms() - t0;
+          cells[12] = format_int(static_cast<long long>(rep.rank));
+          cells[13] = format_double(rep.rel_error);
+          cells[15] = rep.bound_id ? format_double(*rep.bound_id) : "";
+          cells[16] = rep.bound_sampling ? format_double(*rep.bound_sampling) : "";
+          cells[17] = cfg.emit_timings ? format_double(elapsed) : "";
+          auto& acc = accum[{scheme_idx, s_idx}];
+          acc.errors.push_back(rep.rel_error);
+          acc.ranks.push_back(static_cast<double>(rep.rank));
+        }
+        rows.push_back({{scheme_idx, s_idx, trial}, std::move(cells)});
+      }
+    }
+  }
+  std::sort(rows.begin(), rows.end(), [](const Row& a, const Row& b) { return a.key < b.key; });
+  out << csv_join(compress_csv_header()) << "\n";
+  for (const Row& row : rows) out << csv_join(row.cells) << "\n";
+  for (size_t scheme_idx = 0; scheme_idx < cfg.schemes.size(); ++scheme_idx)
+    for (size_t s_idx = 0; s_idx < cfg.s_grid.size(); ++s_idx) {
+      const auto it = accum.find({scheme_idx, s_idx});
+      if (it == accum.end() || it->second.errors.empty()) continue;
+      const Accum& acc = it->second;
+      for (const char* stat : {"mean", "std"}) {
+        const bool is_mean = std::string(stat) == "mean";
+        if (!is_mean && acc.errors.size() < 2) continue;
+        std::vector<std::string> cells(compress_csv_header().size());
+        cells[0] = "normal";
+        cells[1] = format_int(cfg.d);
+        cells[2] = format_int(static_cast<long long>(cfg.N));
+        cells[3] = format_int(static_cast<long long>(cfg.n_sources));
+        cells[4] = format_double(cfg.xi);
+        cells[5] = "gaussian";
+        cells[7] = "id";
+        cells[8] = cfg.schemes[scheme_idx].name();
+        cells[9] = format_double(cfg.s_grid[s_idx]);
+        cells[10] = stat;
+        cells[12] = is_mean ? format_int(static_cast<long long>(std::llround(mean_of(acc.ranks)))) : "";
+        cells[13] = is_mean ? format_double(mean_of(acc.errors)) : format_double(stddev_of(acc.errors));
+        out << csv_join(cells) << "\n";
+      }
+    }
+}
+
+}  // namespace kernid_b200
+
+// ====================================================================== C exports
+// Flat entry points over the mirror for the Python test/bench harness (ctypes).
+using namespace kernid_b200;
+
+namespace {
+thread_local std::string g_err;
+int guard(const std::function<void()>& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const RangeError& e) {
+    g_err = e.what(); return KID_E_RANGE;
+  } catch (const DimensionError& e) {
+    g_err = e.what(); return KID_E_DIM;
+  } catch (const NoTargetsError& e) {
+    g_err = e.what(); return KID_E_NO_TARGETS;
+  } catch (const NumericalError& e) {
+    g_err = e.what(); return KID_E_NUMERICAL;
+  } catch (const IllConditionedSkeletonError& e) {
+    g_err = e.what(); return KID_E_ILLCOND;
+  } catch (const ConfigError& e) {
+    g_err = e.what(); return KID_E_CONFIG;
+  } catch (const std::exception& e) {
+    g_err = e.what(); return KID_E_ERROR;
+  }
+}
+Matrix wrap(const double* a, int64_t rows, int64_t cols) {
+  Matrix M(rows, cols);
+  std::memcpy(M.data(), a, sizeof(double) * static_cast<size_t>(rows * cols));
+  return M;
+}
+}  // namespace
+
+extern "C" {
+
+const char* kidh_last_error(void) { return g_err.c_str(); }
+
+uint64_t kidh_derive_seed(uint64_t master, uint64_t a, uint64_t b) { return derive_seed(master, a, b); }
+
+// resolve_center RandomPoint row (harness.hpp:95-100)
+int64_t kidh_center_index(int64_t N, uint64_t data_seed) {
+  Rng rng(derive_seed(data_seed, 0xCE));
+  return static_cast<int64_t>(rng.below(static_cast<std::uint64_t>(N)));
+}
+
+int kidh_gen_normal(int32_t d, int64_t N, uint64_t seed, double* out) {
+  return guard([&] {
+    PointSet ps = gen_normal(d, N, seed);
+    std::memcpy(out, ps.data(), sizeof(double) * static_cast<size_t>(N * d));
+  });
+}
+
+int kidh_singular_values(const double* A, int64_t rows, int64_t cols, double* sv) {
+  return guard([&] {
+    const auto s = singular_values(wrap(A, rows, cols));
+    std::memcpy(sv, s.data(), sizeof(double) * s.size());
+  });
+}
+
+int kidh_epsilon_rank(const double* sv, int64_t n, double eps, double ref_sigma1, int64_t* r) {
+  return guard([&] {
+    std::vector<double> v(sv, sv + n);
+    *r = epsilon_rank(v, eps, ref_sigma1 > 0.0 ? std::optional<double>(ref_sigma1) : std::nullopt);
+  });
+}
+
+int kidh_interpolative_decomposition(const double* A, int64_t m, int64_t n, int64_t r, int64_t* skel, double* P) {
+  return guard([&] {
+    const IDFactorization id = interpolative_decomposition(wrap(A, m, n), r);
+    std::memcpy(skel, id.skeleton.data(), sizeof(int64_t) * static_cast<size_t>(r));
+    std::memcpy(P, id.projection.data(), sizeof(double) * static_cast<size_t>(r * n));
+  });
+}
+
+int kidh_sym_eig(const double* A, int64_t n, double* evals, double* evecs) {
+  return guard([&] {
+    std::vector<double> ev;
+    Matrix V;
+    sym_eig(wrap(A, n, n), ev, evecs ? &V : nullptr);
+    std::memcpy(evals, ev.data(), sizeof(double) * ev.size());
+    if (evecs) std::memcpy(evecs, V.data(), sizeof(double) * static_cast<size_t>(n * n));
+  });
+}
+
+// kind: 0 Uniform, 1 Bernoulli, 2 EuclideanNorm, 4 Leverage (weights given: host draw only)
+int kidh_draw(int32_t kind, int32_t replacement, int64_t m, const double* weights, double s, uint64_t seed,
+              int64_t* out, int64_t* count) {
+  return guard([&] {
+    Rng rng(seed);
+    std::vector<int64_t> idx;
+    if (kind == 0 || kind == 1) {
+      SamplingScheme sc;
+      sc.kind = kind == 0 ? SchemeKind::Uniform : SchemeKind::Bernoulli;
+      sc.replacement = replacement != 0;
+      SampleContext ctx;
+      ctx.m = m;
+      idx = sample_rows(sc, ctx, s, seed).indices;
+    } else {
+      std::vector<double> w(weights, weights + m);
+      idx = weighted_draw(w, sample_count(s, m), kind == 2 && replacement, rng);
+    }
+    std::memcpy(out, idx.data(), sizeof(int64_t) * idx.size());
+    *count = static_cast<int64_t>(idx.size());
+  });
+}
+
+// Host K rows with the reference arithmetic: K(rows, :) for targets/sources given by
+// indices into a col-major N x d point set.
+int kidh_kernel_rows(const double* pts, int64_t N, int32_t d, const int64_t* tgt_idx, const int64_t* rows,
+                     int64_t count, const int64_t* src_idx, int64_t m, double h, double* out) {
+  return guard([&] {
+    const KernelSpec spec = KernelSpec::gaussian(h);
+    spec.validate();
+    for (int64_t i = 0; i < count; ++i)
+      for (int64_t j = 0; j < m; ++j)
+        out[i + j * count] = eval_kernel(spec, pts + tgt_idx[rows[i]], N, pts + src_idx[j], N, d);
+  });
+}
+
+// One compress trial through the mirror on device `device` (harness prepare_trial + sample_rows
+// + compress_id). scheme: 0 uniform, 2 euclidean_norm, 4 leverage (rank lev_rank; <= 0: auto).
+int kidh_compress_trial(int32_t device, int32_t d, int64_t N, int64_t n, double xi, double h_value,
+                        uint64_t data_seed, int32_t scheme, int64_t lev_rank, double s, uint64_t sample_seed,
+                        double eps, int64_t* n_targets, int64_t* rank, double* rel_error, double* rel_error_fro,
+                        int64_t* skel_out, int64_t* sample_out, int64_t* sample_count_out) {
+  return guard([&] {
+    Device dev(device);
+    const PointSet points = gen_normal(d, N, derive_seed(data_seed, 0xDA7A));
+    Rng crng(derive_seed(data_seed, 0xCE));
+    const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(N)));
+    std::vector<double> center(static_cast<size_t>(d));
+    for (int k = 0; k < d; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+    const SourceTargetSplit split = split_sources_targets(dev, points, center, n, xi);
+    const KernelBlock K(dev, KernelSpec::gaussian(h_value * silverman_bandwidth(d, N)), points, split);
+    *n_targets = K.rows();
+    SamplingScheme sc;
+    sc.kind = scheme == 2 ? SchemeKind::EuclideanNorm : scheme == 4 ? SchemeKind::Leverage : SchemeKind::Uniform;
+    RankRule rule = RankRule::from_eps(eps);
+    if (sc.kind == SchemeKind::Leverage) {
+      if (lev_rank > 0) {
+        sc.rank_for_leverage = lev_rank;
+      } else {
+        std::vector<double> ev;
+        sym_eig(K.gram(), ev, nullptr);
+        std::vector<double> sv(ev.size());
+        for (size_t i = 0; i < ev.size(); ++i) sv[i] = std::sqrt(std::max(ev[i], 0.0));
+        sc.rank_for_leverage = std::max<int64_t>(1, rule.resolve(sv));
+      }
+    }
+    SampleContext ctx;
+    ctx.m = K.rows();
+    ctx.K = &K;
+    ctx.split = &split;
+    ctx.points = &points;
+    const RowSample sample = sample_rows(sc, ctx, s, sample_seed);
+    std::memcpy(sample_out, sample.indices.data(), sizeof(int64_t) * sample.indices.size());
+    *sample_count_out = static_cast<int64_t>(sample.indices.size());
+    auto [id, rep] = compress_id(K, sample, rule);
+    *rank = rep.rank;
+    *rel_error = rep.rel_error;
+    *rel_error_fro = rep.rel_error_fro;
+    std::memcpy(skel_out, id.skeleton.data(), sizeof(int64_t) * id.skeleton.size());
+  });
+}
+
+// run_experiment through the mirror; CSV written to `path`.
+int kidh_run_experiment(int32_t device, int32_t d, int64_t N, int64_t n, double xi, double h_value, int32_t scheme,
+                        int64_t lev_rank, const double* s_grid, int32_t n_s, double eps, int32_t trials,
+                        uint64_t seed, const char* path) {
+  return guard([&] {
+    Device dev(device);
+    ExperimentConfig cfg;
+    cfg.d = d;
+    cfg.N = N;
+    cfg.n_sources = n;
+    cfg.xi = xi;
+    cfg.h_value = h_value;
+    SamplingScheme sc;
+    sc.kind = scheme == 2 ? SchemeKind::EuclideanNorm : scheme == 4 ? SchemeKind::Leverage : SchemeKind::Uniform;
+    if (lev_rank > 0) sc.rank_for_leverage = lev_rank;
+    cfg.schemes = {sc};
+    cfg.scheme_rank_auto = {sc.kind == SchemeKind::Leverage && lev_rank <= 0};
+    cfg.s_grid.assign(s_grid, s_grid + n_s);
+    cfg.rank_rule = RankRule::from_eps(eps);
+    cfg.trials = trials;
+    cfg.seed = seed;
+    std::ostringstream os;
+    run_experiment(dev, cfg, os, nullptr);
+    FILE* f = std::fopen(path, "w");
+    if (!f) throw Error(std::string("cannot open ") + path);
+    std::fputs(os.str().c_str(), f);
+    std::fclose(f);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+"""Python front-end of the host C++ mirror (libkernid_host.so, include/kernid_b200.hpp).
+
+Names follow the reference `kernid::` API (/root/reference/proj/include/kernid/) so the
+parity tests read like the reference's own tests. Device work goes through
+libkernid_cuda.so; there is no CPU fallback for the O(N_T m) passes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import ERROR_NAMES, KidError, cuda_lib  # noqa: F401  (cuda_lib loads libkernid_cuda.so first)
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+HOST_SO = os.path.join(PKG, "libkernid_host.so")
+_host = None
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+
+UNIFORM, BERNOULLI, EUCLIDEAN_NORM, LEVERAGE = 0, 1, 2, 4
+
+
+def host_lib():
+    global _host
+    if _host is None:
+        cuda_lib()
+        if not os.path.exists(HOST_SO):
+            raise OSError(f"{HOST_SO} missing: run __graft_entry__.build()")
+        L = C.CDLL(HOST_SO)
+        i64, i32, u64, dbl, P = C.c_int64, C.c_int32, C.c_uint64, C.c_double, C.POINTER
+        L.kidh_last_error.restype = C.c_char_p
+        L.kidh_derive_seed.restype = u64
+        L.kidh_derive_seed.argtypes = [u64, u64, u64]
+        L.kidh_center_index.restype = i64
+        L.kidh_center_index.argtypes = [i64, u64]
+        L.kidh_gen_normal.argtypes = [i32, i64, u64, _dp]
+        L.kidh_singular_values.argtypes = [_dp, i64, i64, _dp]
+        L.kidh_epsilon_rank.argtypes = [_dp, i64, dbl, dbl, P(i64)]
+        L.kidh_interpolative_decomposition.argtypes = [_dp, i64, i64, i64, _ip, _dp]
+        L.kidh_sym_eig.argtypes = [_dp, i64, _dp, C.c_void_p]
+        L.kidh_draw.argtypes = [i32, i32, i64, C.c_void_p, dbl, u64, _ip, P(i64)]
+        L.kidh_kernel_rows.argtypes = [_dp, i64, i32, _ip, _ip, i64, _ip, i64, dbl, _dp]
+        L.kidh_compress_trial.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, i32, i64, dbl, u64, dbl, P(i64), P(i64),
+                                          P(dbl), P(dbl), _ip, _ip, P(i64)]
+        L.kidh_run_experiment.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, i64, _dp, i32, dbl, i32, u64, C.c_char_p]
+        _host = L
+    return _host
+
+
+def _ck(rc, what):
+    if rc:
+        raise KidError(rc, f"{what}: {host_lib().kidh_last_error().decode(errors='replace')}")
+
+
+def _cm(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64).T).ravel()
+
+
+def _uncm(flat, rows, cols):
+    return np.asarray(flat).reshape(cols, rows).T.copy()
+
+
+def derive_seed(master: int, a: int, b: int = 0) -> int:
+    return int(host_lib().kidh_derive_seed(master, a, b))
+
+
+def center_index(N: int, data_seed: int) -> int:
+    """RandomPoint center row (harness.hpp:95-100)."""
+    return int(host_lib().kidh_center_index(N, data_seed))
+
+
+def gen_normal(d: int, N: int, seed: int) -> np.ndarray:
+    out = np.zeros(N * d)
+    _ck(host_lib().kidh_gen_normal(d, N, seed, out), "gen_normal")
+    return _uncm(out, N, d)
+
+
+def singular_values(A) -> np.ndarray:
+    A = np.asarray(A, dtype=np.float64)
+    sv = np.zeros(min(A.shape))
+    _ck(host_lib().kidh_singular_values(_cm(A), A.shape[0], A.shape[1], sv), "singular_values")
+    return sv
+
+
+def epsilon_rank(sv, eps: float, ref_sigma1: float | None = None) -> int:
+    sv = np.ascontiguousarray(sv, dtype=np.float64)
+    r = C.c_int64()
+    _ck(host_lib().kidh_epsilon_rank(sv, sv.size, eps, ref_sigma1 or -1.0, C.byref(r)), "epsilon_rank")
+    return r.value
+
+
+def interpolative_decomposition(A, r: int):
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    skel = np.zeros(max(r, 1), np.int64)
+    P = np.zeros(max(r, 1) * n)
+    _ck(host_lib().kidh_interpolative_decomposition(_cm(A), m, n, r, skel, P), "interpolative_decomposition")
+    return skel[:r].copy(), _uncm(P[: r * n], r, n)
+
+
+def sym_eig(A):
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    ev = np.zeros(n)
+    V = np.zeros(n * n)
+    _ck(host_lib().kidh_sym_eig(_cm(A), n, ev, V.ctypes.data), "sym_eig")
+    return ev, _uncm(V, n, n)
+
+
+def draw(kind: int, m: int, s: float, seed: int, weights=None, replacement: bool = False) -> np.ndarray:
+    """sample_rows' draw step (sampling.hpp:156-243) for given weights (host)."""
+    out = np.zeros(max(m, 1), np.int64)
+    cnt = C.c_int64()
+    wp = None
+    if weights is not None:
+        weights = np.ascontiguousarray(weights, dtype=np.float64)
+        wp = weights.ctypes.data
+    _ck(host_lib().kidh_draw(kind, int(replacement), m, wp, s, seed, out, C.byref(cnt)), "sample_rows")
+    return out[: cnt.value].copy()
+
+
+def kernel_rows(points_colmajor: np.ndarray, N: int, d: int, tgt_idx, rows, src_idx, h: float) -> np.ndarray:
+    """Host K rows with the reference arithmetic (gather_rows of kernel_matrix)."""
+    tgt_idx = np.ascontiguousarray(tgt_idx, dtype=np.int64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    src_idx = np.ascontiguousarray(src_idx, dtype=np.int64)
+    out = np.zeros(max(rows.size * src_idx.size, 1))
+    _ck(host_lib().kidh_kernel_rows(points_colmajor, N, d, tgt_idx, rows, rows.size, src_idx, src_idx.size, h, out),
+        "kernel_rows")
+    return _uncm(out[: rows.size * src_idx.size], rows.size, src_idx.size)
+
+
+@dataclass
+class TrialResult:
+    n_targets: int
+    rank: int
+    rel_error: float
+    rel_error_fro: float
+    skeleton: np.ndarray
+    sample: np.ndarray
+
+
+def compress_trial(d, N, n, xi, data_seed, scheme, s, sample_seed, eps, h_value=1.0, lev_rank=0, device=0):
+    """prepare_trial + sample_rows + compress_id through the C++ mirror on the GPU."""
+    nt, rank, cnt = C.c_int64(), C.c_int64(), C.c_int64()
+    rel, relf = C.c_double(), C.c_double()
+    skel = np.zeros(n, np.int64)
+    sample = np.zeros(N, np.int64)
+    _ck(host_lib().kidh_compress_trial(device, d, N, n, xi, h_value, data_seed, scheme, lev_rank, s, sample_seed, eps,
+                                       C.byref(nt), C.byref(rank), C.byref(rel), C.byref(relf), skel, sample,
+                                       C.byref(cnt)), "compress_trial")
+    return TrialResult(nt.value, rank.value, rel.value, relf.value, skel[: rank.value].copy(), sample[: cnt.value].copy())
+
+
+def run_experiment(path: str, d, N, n, xi, scheme, s_grid, eps, trials=1, seed=1, h_value=1.0, lev_rank=0, device=0):
+    s_grid = np.ascontiguousarray(s_grid, dtype=np.float64)
+    _ck(host_lib().kidh_run_experiment(device, d, N, n, xi, h_value, scheme, lev_rank, s_grid, s_grid.size, eps, trials,
+                                       seed, path.encode()), "run_experiment")
+    with open(path) as f:
+        return f.read()

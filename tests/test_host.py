@@ -1,0 +1,119 @@
+"""CPU tests of the product's host side (libkernid_host.so) and of the C-ABI library.
+
+The host steps the north star keeps on the host (K_s rows, epsilon-rank, CPQR/ID,
+weighted draws, Gram eigen-solve) are checked against the oracle: draws and the ID
+skeleton must be bit-identical given identical inputs.
+No GPU is needed here.
+"""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_1409_2802_b200 import kernid
+    kernid.host_lib()
+    return kernid
+
+
+def test_cuda_library_exports_every_declared_symbol():
+    from paper_1409_2802_b200 import _lib
+    header = open(os.path.join(ROOT, "include", "kernid_cuda.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|void|const char\*|int64_t)\s+(kid_\w+)\s*\(", header, re.M))
+    assert len(declared) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.CUDA_SO], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (kid_\w+)", out))
+    assert declared <= exported, declared - exported
+    assert set(_lib.SYMBOLS) <= exported
+    L = _lib.cuda_lib()  # loads without a GPU (cudart is linked statically)
+    assert L.kid_abi_version() == 1
+
+
+def test_no_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1409_2802_b200._lib import Device, KidError
+    with pytest.raises(KidError):
+        Device(0)
+
+
+def test_host_rng_and_points_match_oracle(H, oracle):
+    for seed in (1, 42, 2**63 + 5):
+        assert H.derive_seed(seed, 3, 1) == oracle.derive_seed(seed, 3, 1)
+    a = H.gen_normal(3, 1000, 77)
+    b = oracle.gen_normal(3, 1000, 77)
+    assert np.array_equal(a, b)
+
+
+def test_host_draws_match_oracle(H, oracle):
+    rng = np.random.default_rng(0)
+    w = rng.random(5000) ** 4
+    for seed in range(5):
+        for s in (0.001, 0.02, 0.3):
+            assert np.array_equal(H.draw(H.UNIFORM, 5000, s, seed), oracle.sample_rows(oracle.SCHEME_UNIFORM, 5000, s, seed))
+            assert np.array_equal(H.draw(H.EUCLIDEAN_NORM, 5000, s, seed, w),
+                                  oracle.sample_rows(oracle.SCHEME_EUCLIDEAN, 5000, s, seed, w))
+            assert np.array_equal(H.draw(H.EUCLIDEAN_NORM, 5000, s, seed, w, replacement=True),
+                                  oracle.sample_rows(oracle.SCHEME_EUCLIDEAN, 5000, s, seed, w, replacement=True))
+
+
+def test_host_kernel_rows_bit_exact(H, oracle):
+    t = oracle.prepare_trial(3, 5000, 50, 2.0, oracle.derive_seed(1, 0, 0))
+    K = oracle.kernel_matrix(t.targets, t.sources, t.h)
+    rows = np.array([0, 3, 99, K.shape[0] - 1])
+    pts = np.ascontiguousarray(t.points.T).ravel()
+    Ks = H.kernel_rows(pts, t.points.shape[0], 3, t.split.target_indices, rows, t.split.source_indices, t.h)
+    assert np.array_equal(Ks, K[rows])
+
+
+@pytest.mark.parametrize("d,eps", [(2, 1e-2), (2, 1e-8), (3, 1e-8), (3, 1e-14), (5, 1e-4)])
+def test_host_id_skeleton_identical_to_oracle(H, oracle, d, eps):
+    t = oracle.prepare_trial(d, 20000, 100, 2.0, oracle.derive_seed(1, 0, 0))
+    K = oracle.kernel_matrix(t.targets, t.sources, t.h)
+    rows = oracle.sample_rows(oracle.SCHEME_UNIFORM, K.shape[0], 0.05, 11)
+    sub = K[rows]
+    sv_h = H.singular_values(sub)
+    sv_o = oracle.singular_values(sub)
+    assert np.all(np.abs(sv_h - sv_o) <= 1e-13 * sv_o[0])
+    r = oracle.epsilon_rank(sv_o, eps)
+    assert H.epsilon_rank(sv_h, eps) == r
+    try:
+        skel_o, P_o = oracle.interpolative_decomposition(sub, r)
+    except oracle.OracleError as e:
+        from paper_1409_2802_b200._lib import KidError
+        with pytest.raises(KidError) as ee:
+            H.interpolative_decomposition(sub, r)
+        assert ee.value.code == e.code
+        return
+    skel_h, P_h = H.interpolative_decomposition(sub, r)
+    assert np.array_equal(skel_h, skel_o)
+    assert np.array_equal(P_h, P_o)
+
+
+def test_host_sym_eig(H):
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((60, 40))
+    G = A.T @ A
+    ev, V = H.sym_eig(G)
+    ref = np.linalg.eigvalsh(G)[::-1]
+    assert np.allclose(ev, ref, rtol=1e-12, atol=1e-12 * ref[0])
+    assert np.allclose(V.T @ V, np.eye(40), atol=1e-12)
+
+
+def test_host_errors_mirror_reference(H):
+    from paper_1409_2802_b200._lib import KidError, KID_E_RANGE, KID_E_ILLCOND
+    with pytest.raises(KidError) as e:
+        H.epsilon_rank([1.0, 0.5], 1.5)
+    assert e.value.code == KID_E_RANGE
+    u = np.arange(1.0, 9.0).reshape(8, 1)
+    v = np.arange(1.0, 6.0).reshape(5, 1)
+    with pytest.raises(KidError) as e:
+        H.interpolative_decomposition(u @ v.T, 3)
+    assert e.value.code == KID_E_ILLCOND
