@@ -121,10 +121,10 @@ struct GramArgs {
 constexpr int kTraceTiles = 64;
 
 // Warp-specialized pipeline (one CTA per SM):
-//   warps 0..7  (kMW "MMA" warps): per tile, D = K_N - K_S P2 (DMMA, balanced block list) then
+//   warps 8..15 (kMW "MMA" warps): per tile, D = K_N - K_S P2 (DMMA, balanced block list) then
 //               G += D^T D (DMMA) on static 16x16 warp tiles (2x2 blocks of 8x8) of the upper
 //               triangle, accumulators register-resident across all tiles of the CTA's chunk;
-//   warps 8..15 (kEW "eval" warps): evaluate the next 32 x m K tiles into a kStages-deep
+//   warps 0..7  (kEW "eval" warps): evaluate the next 32 x m K tiles into a kStages-deep
 //               shared-memory ring. Tiles are COLUMN-major (K[col][t], stride kST = 36): lane =
 //               target row, so each thread keeps its target's coordinates in registers, source
 //               coordinates are warp-broadcast, stores are conflict-free, and the DMMA fragment
@@ -135,16 +135,22 @@ constexpr int kTraceTiles = 64;
 constexpr int kMW = 8, kEW = 8, kGT = (kMW + kEW) * 32;  // 512 threads
 constexpr int kStages = 3;
 constexpr int kST = kTM + 4;  // column-major tile stride
-constexpr int kGPW = 4;       // GEMM1 blocks per warp per batch
+constexpr int kGPW = 6;       // GEMM1 blocks per warp per batch
 constexpr int kBarFull = 1, kBarEmpty = 1 + kStages, kBarMma = 1 + 2 * kStages;
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// clock64 after a deferred-blocking BAR.SYNC reads the issue time; the shared-memory load and
+// the dependent branch below force the stamp to be taken after the barrier has released.
 #define KID_TRACE(ev)                                                                              \
   do {                                                                                             \
-    if (A.trace && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && it < kTraceTiles)            \
-      A.trace[((size_t)warp * kTraceTiles + it) * 4 + (ev)] = clock64();                           \
+    if (A.trace && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && it < kTraceTiles) {          \
+      const double probe_ = *(volatile double*)&s_tab[1];                                          \
+      long long t_ = 0;                                                                            \
+      if (probe_ == probe_) t_ = clock64();                                                        \
+      A.trace[((size_t)warp * kTraceTiles + it) * 4 + (ev)] = t_;                                  \
+    }                                                                                              \
   } while (0)
 
 template <int D, int TPW>
@@ -177,9 +183,15 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
   const int ntile = (int)(tile_hi - tile_lo);
   __syncthreads();
 
-  if (warp >= kMW) {
+  // Eval warps take the LOW warp ids: the issue arbiter favours the highest warp id, so the
+  // DMMA warps (long pipe occupancy, few instructions) win issue slots and the eval warps fill
+  // the gaps instead of starving them.
+  if (warp < kEW) {
     // ================================================================ eval warps
-    const int ew = warp - kMW;  // this warp evaluates columns j = ew, ew + kEW, ...
+    // register split (per warpgroup): eval E, DMMA 256 - E -> 2*128*E + 2*128*(256-E) = 64K
+    if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 112;\n" ::: "memory");
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    const int ew = warp;  // this warp evaluates columns j = ew, ew + kEW, ...
     // target coordinates live in registers for the compiled dimensions; the generic-d path
     // (D == 0) re-reads them through L1 (tc holds a single slot there)
     constexpr int DR = D ? D : 1;
@@ -196,7 +208,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
       const bool valid = t0 + lane < A.tv.nt;
       {  // prefetch the next tile's coordinates (latency overlaps the evaluation)
         const int64_t i = t0 + kTM + lane;
-        const bool ok = it + 1 < ntile && i < A.tv.nt;
+        const bool ok = it + 1 < ntile && i < A.tv.nt && !(A.dbg & 1);
 #pragma unroll
         for (int k = 0; k < DR; ++k) tn[k] = (k < d && ok) ? tcoord(A.tv, i, k) : 0.0;
       }
@@ -239,9 +251,12 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
     }
   } else {
     // ================================================================ MMA warps
+    if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n" ::: "memory");
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 184;\n" ::: "memory");
+    const int mw = warp - kEW;
     int2 tl[TPW];  // (ti, tj) 16x16 warp tiles of the upper triangle, x = -1: empty
 #pragma unroll
-    for (int q = 0; q < TPW; ++q) tl[q] = A.blist[((size_t)part * kMW + warp) * TPW + q];
+    for (int q = 0; q < TPW; ++q) tl[q] = A.blist[((size_t)part * kMW + mw) * TPW + q];
     double acc[TPW][2][2][2];
 #pragma unroll
     for (int q = 0; q < TPW; ++q)
@@ -262,9 +277,8 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
             const int a = 2 * tl[q].x + u, b = 2 * tl[q].y + v;
             if (a < NB && b < NB && a <= b) vmask[q] |= 1 << (2 * u + v);
           }
+      if (A.dbg & 8) vmask[q] = 15;
     }
-    const int nblk1 = 4 * NBN;  // GEMM1 blocks (nb-major, rb minor)
-    const int g_lo = nblk1 * warp / kMW, g_hi = nblk1 * (warp + 1) / kMW;
     const int fr = (lane >> 2), fk = (lane & 3);  // fragment coordinates
     for (int it = 0; it < ntile; ++it) {
       const int s = it % kStages;
@@ -274,36 +288,63 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
       const double* KS = KSb + (size_t)s * TS;
       double* KN = KNb + (size_t)s * TN;
       if (r > 0) {  // D = K_N - K_S P2, column-major in place
-        for (int g0 = (A.dbg & 2) ? g_hi : g_lo; g0 < g_hi; g0 += kGPW) {
-          double c[kGPW][2];
+        // static map: warp mw owns row blocks {2(mw&1), 2(mw&1)+1} and column blocks
+        // nb = (mw>>1) + 4t; three column blocks per round -> 2 A + 3 B fragment loads feed 6
+        // DMMAs per k-step (loads double-buffered); a slot past NBN computes into a dead
+        // accumulator (unpredicated: no warp-sync/branch around the DMMAs). The K_N operands of
+        // the subtraction are loaded before the k-loop so the write-back is a burst of stores.
+        const int rb0 = 2 * (mw & 1), nbo = mw >> 1;
+        for (int t0 = (A.dbg & 2) ? NBN : 0; 4 * t0 + nbo < NBN; t0 += 3) {
+          int nbv[3];
+          double c[3][2][2], kn[3][2][2];
 #pragma unroll
-          for (int q = 0; q < kGPW; ++q) c[q][0] = c[q][1] = 0.0;
-          for (int k0 = 0; k0 < r4; k0 += 4) {
-            double a[kGPW], b[kGPW];
+          for (int u = 0; u < 3; ++u) {
+            nbv[u] = nbo + 4 * (t0 + u);
+            const int nbc = min(nbv[u], NBN - 1);
 #pragma unroll
-            for (int q = 0; q < kGPW; ++q) {
-              const int g = g0 + q < g_hi ? g0 + q : g_lo;
-              const int nb = g >> 2, rb = g & 3;
-              a[q] = KS[(k0 + fk) * kST + rb * 8 + fr];
-              b[q] = sP[(k0 + fk) * SP + nb * 8 + fr];
+            for (int v = 0; v < 2; ++v) {
+              c[u][v][0] = c[u][v][1] = 0.0;
+              const double* p = &KN[(nbc * 8 + 2 * fk) * kST + (rb0 + v) * 8 + fr];
+              kn[u][v][0] = p[0];
+              kn[u][v][1] = p[kST];
             }
+          }
+          double a[2][2], b[2][3];
+          auto load1 = [&](int buf, int k0) {
 #pragma unroll
-            for (int q = 0; q < kGPW; ++q)
-              if (g0 + q < g_hi) dmma884(c[q][0], c[q][1], a[q], b[q]);
+            for (int v = 0; v < 2; ++v) a[buf][v] = KS[(k0 + fk) * kST + (rb0 + v) * 8 + fr];
+#pragma unroll
+            for (int u = 0; u < 3; ++u) b[buf][u] = sP[(k0 + fk) * SP + min(nbv[u], NBN - 1) * 8 + fr];
+          };
+          auto mma1 = [&](int buf) {
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+#pragma unroll
+              for (int v = 0; v < 2; ++v) dmma884(c[u][v][0], c[u][v][1], a[buf][v], b[buf][u]);
+          };
+          load1(0, 0);
+          for (int k0 = 0; k0 < r4; k0 += 8) {  // two k-steps per trip: static buffer indices
+            if (k0 + 4 < r4) load1(1, k0 + 4);
+            mma1(0);
+            if (k0 + 4 >= r4) break;
+            if (k0 + 8 < r4) load1(0, k0 + 8);
+            mma1(1);
           }
 #pragma unroll
-          for (int q = 0; q < kGPW; ++q) {
-            if (g0 + q < g_hi) {
-              const int g = g0 + q, nb = g >> 2, rb = g & 3;
-              double* p = &KN[(nb * 8 + 2 * fk) * kST + rb * 8 + fr];
-              p[0] -= c[q][0];
-              p[kST] -= c[q][1];
+          for (int u = 0; u < 3; ++u) {
+            if (nbv[u] < NBN) {
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                double* p = &KN[(nbv[u] * 8 + 2 * fk) * kST + (rb0 + v) * 8 + fr];
+                p[0] = kn[u][v][0] - c[u][v][0];
+                p[kST] = kn[u][v][1] - c[u][v][1];
+              }
             }
           }
         }
+        KID_TRACE(2);
         nbar_sync(kBarMma, kMW * 32);
       }
-      KID_TRACE(2);
       // G += D^T D over the 32 rows of the stage; fragments F(x) = D[k0 + fk][x*8 + fr],
       // double-buffered so the loads of k-step k+1 overlap the DMMAs of k-step k
       if (!(A.dbg & 4)) {
@@ -359,7 +400,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
-      for (int w = kMW; w < kMW + kEW; ++w) t += red[w];
+      for (int w = 0; w < kEW; ++w) t += red[w];
       A.partial_sk[chunk] = t;
     }
   }
@@ -704,8 +745,9 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     KID_CK(c, cudaMemcpyAsync(tr.data(), A.trace, sizeof(long long) * trace_n, cudaMemcpyDeviceToHost, c->stream));
     KID_CK(c, cudaStreamSynchronize(c->stream));
     cudaFree(A.trace);
-    // per-phase mean cycles over tiles 4..kTraceTiles-1 (steady state), MMA warp 0 and eval warp kMW
-    auto at = [&](int w, int it, int ev) { return tr[((size_t)w * kTraceTiles + it) * 4 + ev]; };
+    // per-phase mean cycles over tiles 4..kTraceTiles-1 (steady state), MMA warp kEW and eval warp 0
+    auto at_raw = [&](int w, int it, int ev) { return tr[((size_t)w * kTraceTiles + it) * 4 + ev]; };
+    auto at = [&](int w, int it, int ev) { return at_raw(w == 0 ? kEW : (w == kMW ? 0 : w), it, ev); };
     double mw_full = 0, mw_g1 = 0, mw_syrk = 0, ew_empty = 0, ew_eval = 0, tile = 0;
     int n = 0;
     for (int it = 4; it + 1 < kTraceTiles; ++it) {
@@ -718,7 +760,14 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
       tile += at(0, it + 1, 0) - at(0, it, 0);
       ++n;
     }
-    for (int it = 10; it < 12; ++it) {
+    for (int it = 10; it < 11; ++it) {
+      fprintf(stderr, "[kid trace] tile %d gemm1 cycles per MMA warp:", it);
+      for (int w = kEW; w < kEW + kMW; ++w) fprintf(stderr, " %lld", at_raw(w, it, 2) - at_raw(w, it, 1));
+      fprintf(stderr, " | syrk+bar:");
+      for (int w = kEW; w < kEW + kMW; ++w) fprintf(stderr, " %lld", at_raw(w, it, 3) - at_raw(w, it, 2));
+      fprintf(stderr, "\n");
+    }
+    for (int it = 10; it < 10; ++it) {
       fprintf(stderr, "[kid trace] tile %d, stamps rel. to MMA warp 0 event 0:", it);
       for (int w = 0; w < kMW + kEW; ++w)
         fprintf(stderr, " w%d[%lld %lld %lld %lld]", w, at(w, it, 0) - at(0, it, 0), at(w, it, 1) - at(0, it, 0),
@@ -726,7 +775,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
       fprintf(stderr, "\n");
     }
     if (n)
-      fprintf(stderr, "[kid trace] cycles/tile: tile %.0f | mma: wait_full %.0f gemm1+bar %.0f syrk %.0f | "
+      fprintf(stderr, "[kid trace] cycles/tile: tile %.0f | mma: wait_full %.0f gemm1 %.0f bar+syrk %.0f | "
                       "eval: wait_empty %.0f eval %.0f (n=%d)\n",
               tile / n, mw_full / n, mw_g1 / n, mw_syrk / n, ew_empty / n, ew_eval / n, n);
   }

@@ -31,16 +31,17 @@ def main():
         if sub and sub not in d["Kernel Name"]:
             continue
         name = d["Kernel Name"].split("(")[0][-40:]
-        print(f"{name:40s} t={d['gpu__time_duration.sum']}ms dram_r={d['dram__bytes_read.sum']}"
+        print(f"{name:40s} t={d['gpu__time_duration.sum']}{units[hdr.index('gpu__time_duration.sum')]} dram_r={d['dram__bytes_read.sum']}"
               f"{units[hdr.index('dram__bytes_read.sum')]} dram_w={d['dram__bytes_write.sum']}"
               f"{units[hdr.index('dram__bytes_write.sum')]} fp64={d[metrics[3]]}% dmma={d[metrics[4]]}% "
               f"warps={d[metrics[5]]}% issue={d[metrics[7]]}% regs={d[metrics[6]]} grid={d[metrics[8]]} "
               f"dram%={d[metrics[10]]}")
     if nsass:
-        txt = ncu(rep, "--page", "source", "--csv", "--print-source", "sass", "-k", f"regex:{sub or '.'}")
+        txt = ncu(rep, "--page", "source", "--csv", "--print-source", "sass")
         rows = list(csv.reader(io.StringIO(txt)))
-        starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
-        blk = rows[starts[0] + 1:(starts[1] if len(starts) > 1 else len(rows))]
+        starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+        pick = next(k for k in range(len(starts) - 1) if sub in rows[starts[k]][1].replace("(int)", ""))
+        blk = rows[starts[pick] + 1:starts[pick + 1]]
         hdr, data = blk[0], blk[1:]
         iS, iSrc, iA = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Source"), hdr.index("Address")
         tot = sum(float(r[iS] or 0) for r in data) or 1.0
