@@ -163,29 +163,9 @@ class Problem:
             src, rho, nt = dev.split(self.center, m, xi)
             self.src, self.rho, self.nt = src, rho, nt
             return
-        torch = self.torch
-        cd, ci = dev.split_candidates(self.center, m)
-        k = cd.size
-        d = self.wl["d"]
-        local_rows = ci - self.offset
-        coords = self.points[local_rows]  # (k, d)
-        pack = np.zeros((m, 2 + d))
-        pack[:, 0] = np.inf
-        pack[:k, 0] = cd
-        pack[:k, 1] = ci.astype(np.float64)
-        pack[:k, 2:] = coords
-        t = torch.tensor(pack, device="cuda")
-        allp = [torch.empty_like(t) for _ in range(self.ws)]
-        torch.distributed.all_gather(allp, t)
-        allp = torch.cat(allp).cpu().numpy()
-        order = np.lexsort((allp[:, 1], allp[:, 0]))[:m]  # (dist, idx), geometry.hpp:39-45
-        sel = allp[order]
-        rho = float(sel[:, 0].max())
-        idx = sel[:, 1].astype(np.int64)
-        srt = np.argsort(idx)
-        self.src = idx[srt]
-        nt = dev.split_finish(self.src, rho, xi, src_points=sel[srt, 2:])
-        self.rho, self.nt = rho, nt
+        from paper_1409_2802_b200 import dist as D
+        src, rho, src_pts, nt = D.sharded_split(dev, self.points, self.offset, self.center, m, xi, device="cuda")
+        self.src, self.rho, self.nt, self._src_pts = src, rho, nt, src_pts
 
     def skeleton(self):
         """EuclideanNorm sampling + host ID on rank 0 (product host path), broadcast."""
@@ -230,8 +210,7 @@ class Problem:
         return H.kernel_rows(pts_cm, pts.shape[0], d, tgt_local, sample, src_idx, self.h)
 
     def _src_points_global(self):
-        # recompute from the candidates exchanged in split(): cached by split_finish caller
-        return self._src_pts
+        return self._src_pts  # gathered with the split's candidates (dist.sharded_split)
 
     def entries(self):
         return self.nt * self.wl["m"]
@@ -241,15 +220,6 @@ def setup(wl, ws, rank, local, torch):
     from paper_1409_2802_b200._lib import Device
     dev = Device(local)
     prob = Problem(wl, dev, torch, ws, rank)
-    if ws > 1:
-        # keep the gathered source coordinates for the host K_s rows
-        orig_finish = dev.split_finish
-
-        def finish(src_idx, rho, xi, src_points=None):
-            prob._src_pts = np.asarray(src_points)
-            return orig_finish(src_idx, rho, xi, src_points)
-
-        dev.split_finish = finish
     prob.split()
     prob.skeleton()
     dev.recon_prepare(prob.skel, prob.P)

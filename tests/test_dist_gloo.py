@@ -1,0 +1,109 @@
+"""World-size-2 gloo tests of the multi-GPU host layer (paper_1409_2802_b200/dist.py) on CPU.
+
+The device is replaced by a CPU stand-in with the reference's arithmetic (sequential squared
+differences, no FMA, correctly rounded sqrt) so the exchange logic -- candidate packing,
+all_gather, global (dist, idx) selection, per-shard compaction, ordered Gram reduction -- is
+checked against the single-process oracle without a GPU.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+class CpuShard:
+    """Test double for Device.split_candidates / split_finish on one shard."""
+
+    def __init__(self, pts, offset):
+        self.pts, self.offset = pts, offset
+        self.dist = None
+        self.targets = None
+
+    def split_candidates(self, center, n):
+        p = self.pts
+        acc = (p[:, 0] - center[0]) * (p[:, 0] - center[0])
+        for k in range(1, p.shape[1]):
+            acc = acc + (p[:, k] - center[k]) * (p[:, k] - center[k])
+        self.dist = np.sqrt(acc)
+        idx = np.arange(p.shape[0]) + self.offset
+        order = np.lexsort((idx, self.dist))[: min(n, p.shape[0])]
+        return self.dist[order], idx[order]
+
+    def split_finish(self, src_idx, rho, xi, src_points=None):
+        local = np.arange(self.pts.shape[0]) + self.offset
+        keep = (self.dist >= xi * rho) & ~np.isin(local, src_idx)
+        self.targets = local[keep]
+        return int(keep.sum())
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, ws, port, d, N, n, xi, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from oracle import oracle as O
+    from paper_1409_2802_b200 import dist as D
+    allpts = O.gen_normal(d, N, 12345)
+    lo, hi = N * rank // ws, N * (rank + 1) // ws
+    shard = CpuShard(allpts[lo:hi], lo)
+    center = allpts[77]
+    src, rho, src_pts, nt = D.sharded_split(shard, allpts[lo:hi], lo, center, n, xi)
+    # per-shard fused-pass partials (oracle arithmetic), reduced in rank order
+    t = O.split_sources_targets(allpts, center, n, xi)
+    K_local = O.kernel_matrix(allpts[shard.targets], src_pts, 0.3)
+    skel = np.array([0, 5, 9])
+    P = np.random.default_rng(0).standard_normal((3, n))
+    P[:, skel] = np.eye(3)
+    sd, sk, DtD, KtK = O.residual_stats(K_local, skel, P)
+    red = D.ordered_sum(np.concatenate([[sd, sk], DtD.ravel()]))
+    q.put((rank, src, rho, shard.targets, red))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d,N,n,xi", [(2, 4001, 50, 2.0), (3, 3000, 100, 1.0)])
+def test_sharded_split_and_reduction_match_single_process(oracle, d, N, n, xi):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, d, N, n, xi, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    allpts = oracle.gen_normal(d, N, 12345)
+    ref = oracle.split_sources_targets(allpts, allpts[77], n, xi)
+    for _, src, rho, _, _ in res:
+        assert np.array_equal(src, ref.source_indices)
+        assert rho == ref.rho
+    tg = np.concatenate([r[3] for r in res])
+    assert np.array_equal(tg, ref.target_indices)
+    # reduced partial Grams == the full-data Grams
+    K = oracle.kernel_matrix(allpts[ref.target_indices], allpts[ref.source_indices], 0.3)
+    skel = np.array([0, 5, 9])
+    P = np.random.default_rng(0).standard_normal((3, n))
+    P[:, skel] = np.eye(3)
+    sd, sk, DtD, _ = oracle.residual_stats(K, skel, P)
+    red = res[0][4]
+    assert np.array_equal(red, res[1][4])  # every rank holds the identical reduction
+    assert red[0] == pytest.approx(sd, rel=1e-12) and red[1] == pytest.approx(sk, rel=1e-12)
+    assert np.allclose(red[2:].reshape(n, n), DtD, rtol=1e-11, atol=1e-14 * np.abs(DtD).max())
+
+
+def test_merge_candidates_tie_break():
+    from paper_1409_2802_b200 import dist as D
+    a = D.pack_candidates([1.0, 2.0], [5, 7], np.array([[0.5], [0.7]]), 3)
+    b = D.pack_candidates([1.0, 1.5], [3, 9], np.array([[0.3], [0.9]]), 3)
+    src, rho, pts = D.merge_candidates(np.concatenate([a, b]), 3)
+    assert list(src) == [3, 5, 9] and rho == 1.5 and np.allclose(pts[:, 0], [0.3, 0.5, 0.9])
