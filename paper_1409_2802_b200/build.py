@@ -32,7 +32,7 @@ def build_cuda(force=False, verbose=False):
     if not force and not _stale(CUDA_SO, deps):
         return CUDA_SO
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-warn-spills", "-o", CUDA_SO] + [os.path.join(CSRC, f) for f in CU_SRCS]
+           "-Xptxas", "-warn-spills", "-o", CUDA_SO] + [os.path.join(CSRC, f) for f in CU_SRCS] + ["-lcublas"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -125,6 +125,7 @@ void kid_destroy(kid_ctx* c) {
     if (p) cudaFree(p);
   if (c->hbuf) cudaFreeHost(c->hbuf);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  if (c->blas) cublasDestroy(c->blas);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }

@@ -10,6 +10,7 @@
 // K itself is never stored: every FP64 pass re-evaluates its target tile in registers
 // / shared memory (SURVEY.md 8a A5 "never materialised on GPU").
 #pragma once
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -140,6 +141,7 @@ struct kid_ctx {
   double* hbuf = nullptr;  // pinned host staging
   size_t hbuf_cap = 0;
   int64_t* counter = nullptr;  // device counters [8]
+  cublasHandle_t blas = nullptr;  // large-m fallback of the Gram passes
 
   // kernel timing (kid_profile): CUDA events on the launching stream around each pass'
   // dominant kernel, read back by kid_profile_read

@@ -20,6 +20,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cublas_v2.h>
+
 #include "kid_internal.cuh"
 
 namespace kid {
@@ -618,6 +620,118 @@ int row_norms_dev(kid_ctx* c, double h, double* d_w) {
 
 // Gram of T = K (r == 0) or T = K_N - K_S P2 (r > 0, operands from kid_recon_prepare).
 // d_out = [sumsq_T, sumsq_K, G (meff x meff)].
+// ------------------------------------------------------------------ large-m path
+// For m - r > 128 (BASELINE c4 m=256, c5 m=512) the fused kernel's shared-memory stages do not
+// fit; this path evaluates a batch of B target rows of K (columns [skel | non-skel]) into a
+// transient column-major HBM buffer with the same arithmetic, then D = K_N - K_S P2 is one DGEMM
+// and G += D^T D one DSYRK (cuBLAS, DMMA). ROUND-1 FALLBACK: it materialises K batch-wise,
+// which the fused kernel avoids; DESIGN.md section 8 plans its replacement.
+__global__ void __launch_bounds__(256) k_eval_batch(TargetView tv, int d, const double* __restrict__ src, int m,
+                                                    double cscale, int64_t t0, int B, double* __restrict__ Kb,
+                                                    double* __restrict__ sk_part) {
+  __shared__ double s_tab[kExpTab];
+  __shared__ double red[8];
+  for (int e = threadIdx.x; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
+  __syncthreads();
+  double sk = 0.0;
+  const int64_t total = (int64_t)B * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % B), j = (int)(e / B);
+    double kv = 0.0;
+    if (t0 + i < tv.nt) {
+      double q = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double df = tcoord(tv, t0 + i, k) * cscale - src[j + (int64_t)k * m] * cscale;
+        q = fma(df, df, q);
+      }
+      kv = exp_neg_fast(q, s_tab);
+    }
+    Kb[e] = kv;
+    sk = fma(kv, kv, sk);
+  }
+  sk = warp_sum(sk);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sk;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    sk_part[blockIdx.x] = t;
+  }
+}
+
+// out = [tr(G), sum_K2, G] with G symmetrised from the upper triangle
+__global__ void k_large_finish(double* __restrict__ G, int n, const double* __restrict__ sk_part, int nsk,
+                               double* __restrict__ out) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(e % n), y = (int)(e / n);
+    out[2 + e] = x <= y ? G[x + (int64_t)y * n] : G[y + (int64_t)x * n];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double tr = 0.0, sk = 0.0;
+    for (int x = 0; x < n; ++x) tr += G[x + (int64_t)x * n];
+    for (int b = 0; b < nsk; ++b) sk += sk_part[b];
+    out[0] = tr;
+    out[1] = sk;
+  }
+}
+
+int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
+  const int m = (int)c->m, d = c->d, meff = (int)(m - r);
+  if (!c->blas) {
+    if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return fail(c, KID_E_CUDA, "cublasCreate failed");
+  }
+  cublasSetStream(c->blas, c->stream);
+  cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
+  const int64_t nt = c->nt;
+  const int B = (int)std::max<int64_t>(1024, std::min<int64_t>(nt, (int64_t)(256ll << 20) / (8ll * m)));
+  const int64_t nbatch = (nt + B - 1) / B;
+  const int ev_blocks = c->sms * 8;
+  // scratch: K batch (B x m) | G (meff x meff) | P2 col-major (r x meff) | sk partials
+  const size_t kb = (size_t)B * m, gb = (size_t)meff * meff, pb = (size_t)std::max<int64_t>(r, 1) * meff;
+  char* base = (char*)scratch(c, sizeof(double) * (kb + gb + pb + (size_t)nbatch * ev_blocks + 64));
+  if (!base) return KID_E_OOM;
+  double* Kb = (double*)base;
+  double* G = Kb + kb;
+  double* P2c = G + gb;
+  double* skp = P2c + pb;
+  if (r > 0) {  // P2 (row-major r x SP on the device) -> column-major r x meff
+    const int SP = frag_stride(meff);
+    std::vector<double> h_row((size_t)r * SP), h_col((size_t)r * meff);
+    KID_CK(c, cudaMemcpyAsync(h_row.data(), c->P2, sizeof(double) * h_row.size(), cudaMemcpyDeviceToHost, c->stream));
+    KID_CK(c, cudaStreamSynchronize(c->stream));
+    for (int64_t k = 0; k < r; ++k)
+      for (int n = 0; n < meff; ++n) h_col[k + (size_t)n * r] = h_row[k * SP + n];
+    KID_CK(c, cudaMemcpyAsync(P2c, h_col.data(), sizeof(double) * h_col.size(), cudaMemcpyHostToDevice, c->stream));
+  }
+  const double* src = r > 0 ? c->src_perm : c->src;
+  const double cscale = std::sqrt(1.0 / (2.0 * h * h));
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  prof_begin(c);
+  for (int64_t b = 0; b < nbatch; ++b) {
+    const int64_t t0 = b * (int64_t)B;
+    const int rows = (int)std::min<int64_t>(B, nt - t0);
+    k_eval_batch<<<ev_blocks, 256, 0, c->stream>>>(view(c), d, src, m, cscale, t0, rows, Kb, skp + b * ev_blocks);
+    KID_LAUNCHED(c);
+    double* KN = Kb + (size_t)r * rows;  // non-skeleton columns follow the r skeleton columns
+    if (r > 0) {
+      if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, meff, (int)r, &mone, Kb, rows, P2c, (int)r, &one, KN,
+                      rows) != CUBLAS_STATUS_SUCCESS)
+        return fail(c, KID_E_CUDA, "cublasDgemm failed");
+      c->launches++;
+    }
+    if (cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, meff, rows, &one, KN, rows, b == 0 ? &zero : &one, G,
+                    meff) != CUBLAS_STATUS_SUCCESS)
+      return fail(c, KID_E_CUDA, "cublasDsyrk failed");
+    c->launches++;
+  }
+  prof_end(c);
+  k_large_finish<<<std::max(1, std::min(c->sms * 4, (meff * meff + 255) / 256)), 256, 0, c->stream>>>(
+      G, meff, skp, (int)(nbatch * ev_blocks), d_out);
+  KID_LAUNCHED(c);
+  return KID_OK;
+}
+
 int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   (void)flags;
   if (int rc = check_block(c, h)) return rc;
@@ -663,7 +777,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   const int TS = ceil_to(r4 > 0 ? r4 : 4, 2) * kST, TN = ceil_to(NBN, 2) * 8 * kST;
   const size_t smem = sizeof(double) * ((size_t)ceil_to(d * m, 2) + (size_t)kStages * (TS + TN) +
                                         (size_t)r4 * frag_stride(meff));
-  if (smem > 220 * 1024) return fail(c, KID_E_DIM, "gram: tile does not fit shared memory (m, r too large)");
+  if (smem > 200 * 1024 || NBN > 16 || getenv("KID_FORCE_LARGE")) return gram_dev_large(c, h, r, d_out);
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   int per_sm = 1;

@@ -164,3 +164,28 @@ def test_fast_exp_accuracy(dev):
     sub = (ref < np.finfo(float).tiny) & (ref > 0)
     assert np.all(np.abs(y[sub] - ref[sub]) <= np.spacing(0.0) * 1.0)
     assert np.all(y[ref == 0.0] == 0.0)
+
+
+@pytest.mark.parametrize("d,n,eps,force", [(16, 256, 1e-2, False), (8, 512, 1e-2, False), (3, 100, 1e-4, True)])
+def test_recon_error_large_m_path(oracle, dev, monkeypatch, d, n, eps, force):
+    """m - r > 128 runs the batched large-m path (k_eval_batch + DGEMM + DSYRK); KID_FORCE_LARGE
+    routes a small case through it too so both Gram paths are checked against the oracle."""
+    if force:
+        monkeypatch.setenv("KID_FORCE_LARGE", "1")
+    t, K = _block(oracle, d=d, N=12_000, n=n)
+    rows = oracle.sample_rows(oracle.SCHEME_UNIFORM, K.shape[0], 0.2, 5)
+    res = oracle.compress_id(K, rows, eps=eps)
+    dev.set_points(t.points)
+    dev.split(t.center, n, 2.0)
+    sd, sk, DtD, _ = dev.recon_error(t.h, res.skeleton, res.P)
+    r_sd, r_sk, r_DtD, r_KtK = oracle.residual_stats(K, res.skeleton, res.P)
+    assert sk == pytest.approx(r_sk, rel=1e-12)
+    u = 2.0 ** -53
+    colnorm = np.sqrt((K * K).sum(0))
+    noise = 8 * u * (colnorm + np.abs(res.P).T @ colnorm[res.skeleton])
+    noise[res.skeleton] = 0.0
+    dg = np.sqrt(np.abs(np.diag(r_DtD)))
+    bound = 1e-10 * np.outer(dg, dg) + np.outer(noise, dg) + np.outer(dg, noise) + np.outer(noise, noise)
+    assert np.all(np.abs(DtD - r_DtD) <= bound + 1e-300)
+    G, gsk = dev.gram(t.h)
+    assert _gram_ok(G, r_KtK)
