@@ -110,7 +110,7 @@ struct GramArgs {
   double negc;         // -1 / (2 h^2)
   double cscale;       // 1 / (sqrt(2) h): coordinates pre-scaled so that exp(-||x' - y'||^2)
   const double* P2;    // r x meff row-major, stride SP (device); nullptr when r == 0
-  const int2* blist;   // [nparts][kMW][TPW] (ti, tj) 16x16 warp tiles, x = -1: empty slot
+  const int2* blist;   // [nparts][kMW][TPW] (a0, b0) first 8x8 block of each WA x 2-block warp tile, x = -1: empty
   int nparts;
   int64_t ntiles;
   int nchunks;
@@ -123,10 +123,10 @@ struct GramArgs {
 constexpr int kTraceTiles = 64;
 
 // Warp-specialized pipeline (one CTA per SM):
-//   warps 8..15 (kMW "MMA" warps): per tile, D = K_N - K_S P2 (DMMA, balanced block list) then
+//   warps 12..19 (kMW "MMA" warps): per tile, D = K_N - K_S P2 (DMMA, balanced block list) then
 //               G += D^T D (DMMA) on static 16x16 warp tiles (2x2 blocks of 8x8) of the upper
 //               triangle, accumulators register-resident across all tiles of the CTA's chunk;
-//   warps 0..7  (kEW "eval" warps): evaluate the next 32 x m K tiles into a kStages-deep
+//   warps 0..11 (kEW "eval" warps): evaluate the next 32 x m K tiles into a kStages-deep
 //               shared-memory ring. Tiles are COLUMN-major (K[col][t], stride kST = 36): lane =
 //               target row, so each thread keeps its target's coordinates in registers, source
 //               coordinates are warp-broadcast, stores are conflict-free, and the DMMA fragment
@@ -134,7 +134,10 @@ constexpr int kTraceTiles = 64;
 // Hand-off by named barriers: FULL[s] (eval arrive, MMA sync), EMPTY[s] (MMA arrive, eval sync),
 // one MMA-group barrier between the two DMMA phases. Both groups share the FP64 datapath
 // (DMMA and DFMA do not overlap on sm_100: tools/fp64_overlap.cu); the split hides latency.
-constexpr int kMW = 8, kEW = 8, kGT = (kMW + kEW) * 32;  // 512 threads
+constexpr int kMW = 8, kEW = 12, kGT = (kMW + kEW) * 32;  // 640 threads
+#ifndef KID_EVAL_ILP
+#define KID_EVAL_ILP 2
+#endif
 constexpr int kStages = 3;
 constexpr int kST = kTM + 4;  // column-major tile stride
 constexpr int kGPW = 6;       // GEMM1 blocks per warp per batch
@@ -155,14 +158,17 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
     }                                                                                              \
   } while (0)
 
-template <int D, int TPW>
+static_assert(kGT == 640, "setmaxnreg budget below assumes 640 threads (96 registers each at launch)");
+static_assert(3 * 128 * (96 - 64) >= 2 * 128 * (144 - 96) && 3 * 128 * (96 - 72) >= 2 * 128 * (128 - 96),
+              "setmaxnreg.inc must not exceed what setmaxnreg.dec releases");
+template <int D, int TPW, int WA>
 __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
   const int d = D ? D : A.d;
   const int m = A.m, r = A.r, meff = A.meff;
   const int r4 = ceil_to(r, 4);
   const int NBN = ceil_to(meff, 8) / 8;
   const int SP = frag_stride(meff);
-  const int TS = ceil_to(r4 > 0 ? r4 : 4, 2) * kST, TN = ceil_to(NBN, 2) * 8 * kST;  // one stage of K_S / K_N
+  const int TS = ceil_to(r4 > 0 ? r4 : 4, 2) * kST, TN = ceil_to(NBN + 1, 2) * 8 * kST;  // one stage of K_S / K_N
   extern __shared__ __align__(16) double smem[];
   double* s_src = smem;                        // d x m (scaled)
   double* KSb = s_src + ceil_to(d * m, 2);     // kStages x (r4 x kST), column-major
@@ -190,9 +196,10 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
   // the gaps instead of starving them.
   if (warp < kEW) {
     // ================================================================ eval warps
-    // register split (per warpgroup): eval E, DMMA 256 - E -> 2*128*E + 2*128*(256-E) = 64K
-    if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 112;\n" ::: "memory");
-    else asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    // register split: the launch allocates 96/thread (640 threads); setmaxnreg.inc can only take
+    // what the decreasing warpgroups release, so 384 (96 - E) >= 256 (M - 96) must hold
+    if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
     const int ew = warp;  // this warp evaluates columns j = ew, ew + kEW, ...
     // target coordinates live in registers for the compiled dimensions; the generic-d path
     // (D == 0) re-reads them through L1 (tc holds a single slot there)
@@ -220,25 +227,31 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
       double* KS = KSb + (size_t)s * TS;
       double* KN = KNb + (size_t)s * TN;
       if (!(A.dbg & 1)) {
-        // two independent exp chains per iteration (columns j, j + kEW)
-        for (int j = ew; j < m; j += 2 * kEW) {
-          const int j1 = j + kEW < m ? j + kEW : j;
-          double q0 = 0.0, q1 = 0.0;
+        // KID_EVAL_ILP independent exp chains per iteration (columns j + u*kEW)
+        constexpr int U = KID_EVAL_ILP;
+        for (int j = ew; j < m; j += U * kEW) {
+          double q[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) q[u] = 0.0;
 #pragma unroll
           for (int k = 0; k < (D ? D : d); ++k) {
             const double tk = D ? tc[D ? k : 0] : (valid ? tcoord(A.tv, t0 + lane, k) * A.cscale : 0.0);
-            const double d0 = tk - s_src[j + k * m];
-            const double d1 = tk - s_src[j1 + k * m];
-            q0 = fma(d0, d0, q0);
-            q1 = fma(d1, d1, q1);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int ju = min(j + u * kEW, m - 1);
+              const double df = tk - s_src[ju + k * m];
+              q[u] = fma(df, df, q[u]);
+            }
           }
-          double k0v = exp_neg_fast(q0, s_tab), k1v = exp_neg_fast(q1, s_tab);
-          if (!valid) k0v = k1v = 0.0;
-          sk = fma(k0v, k0v, sk);
-          *((j < r) ? &KS[j * kST + lane] : &KN[(j - r) * kST + lane]) = k0v;
-          if (j + kEW < m) {
-            sk = fma(k1v, k1v, sk);
-            *((j1 < r) ? &KS[j1 * kST + lane] : &KN[(j1 - r) * kST + lane]) = k1v;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int ju = j + u * kEW;
+            double kv = exp_neg_fast(q[u], s_tab);
+            if (!valid) kv = 0.0;
+            if (ju < m) {
+              sk = fma(kv, kv, sk);
+              *((ju < r) ? &KS[ju * kST + lane] : &KN[(ju - r) * kST + lane]) = kv;
+            }
           }
         }
       }
@@ -253,38 +266,26 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
     }
   } else {
     // ================================================================ MMA warps
-    if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n" ::: "memory");
-    else asm volatile("setmaxnreg.inc.sync.aligned.u32 184;\n" ::: "memory");
+    if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;\n" ::: "memory");
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n" ::: "memory");
     const int mw = warp - kEW;
-    int2 tl[TPW];  // (ti, tj) 16x16 warp tiles of the upper triangle, x = -1: empty
+    int2 tl[TPW];  // (a0, b0) block coordinates of WA x 2-block warp tiles, x = -1: empty slot
 #pragma unroll
     for (int q = 0; q < TPW; ++q) tl[q] = A.blist[((size_t)part * kMW + mw) * TPW + q];
-    double acc[TPW][2][2][2];
+    double acc[TPW][WA][2][2];
 #pragma unroll
     for (int q = 0; q < TPW; ++q)
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < WA; ++u)
 #pragma unroll
         for (int v = 0; v < 2; ++v) acc[q][u][v][0] = acc[q][u][v][1] = 0.0;
     const int NB = NBN;
-    int vmask[TPW];  // which of the 4 blocks of each warp tile lie in the upper triangle
-#pragma unroll
-    for (int q = 0; q < TPW; ++q) {
-      vmask[q] = 0;
-      if (tl[q].x >= 0)
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int a = 2 * tl[q].x + u, b = 2 * tl[q].y + v;
-            if (a < NB && b < NB && a <= b) vmask[q] |= 1 << (2 * u + v);
-          }
-      if (A.dbg & 8) vmask[q] = 15;
-    }
     const int fr = (lane >> 2), fk = (lane & 3);  // fragment coordinates
     for (int it = 0; it < ntile; ++it) {
       const int s = it % kStages;
+#ifndef KID_TRACE_G1
       KID_TRACE(0);
+#endif
       nbar_sync(kBarFull + s, kGT);
       KID_TRACE(1);
       const double* KS = KSb + (size_t)s * TS;
@@ -325,6 +326,9 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
               for (int v = 0; v < 2; ++v) dmma884(c[u][v][0], c[u][v][1], a[buf][v], b[buf][u]);
           };
           load1(0, 0);
+#ifdef KID_TRACE_G1
+          KID_TRACE(0);
+#endif
           for (int k0 = 0; k0 < r4; k0 += 8) {  // two k-steps per trip: static buffer indices
             if (k0 + 4 < r4) load1(1, k0 + 4);
             mma1(0);
@@ -332,6 +336,11 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
             if (k0 + 8 < r4) load1(0, k0 + 8);
             mma1(1);
           }
+#ifdef KID_TRACE_G1
+          { double z = 0; for (int u = 0; u < 3; ++u) z += c[u][0][0] + c[u][1][1];
+            if (z == 12345.678) KN[0] = z; }
+          KID_TRACE(2);
+#endif
 #pragma unroll
           for (int u = 0; u < 3; ++u) {
             if (nbv[u] < NBN) {
@@ -344,23 +353,24 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
             }
           }
         }
+#ifndef KID_TRACE_G1
         KID_TRACE(2);
+#endif
         nbar_sync(kBarMma, kMW * 32);
       }
       // G += D^T D over the 32 rows of the stage; fragments F(x) = D[k0 + fk][x*8 + fr],
       // double-buffered so the loads of k-step k+1 overlap the DMMAs of k-step k
       if (!(A.dbg & 4)) {
         const double* col = KN + fr * kST + fk;
-        double fa[2][TPW][2], fb[2][TPW][2];
+        double fa[2][TPW][WA], fb[2][TPW][2];
         auto load = [&](int buf, int k0) {
 #pragma unroll
           for (int q = 0; q < TPW; ++q) {
-            const int ti = tl[q].x >= 0 ? tl[q].x : 0, tj = tl[q].x >= 0 ? tl[q].y : 0;
+            const int a0 = tl[q].x >= 0 ? tl[q].x : 0, b0 = tl[q].x >= 0 ? tl[q].y : 0;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              fa[buf][q][u] = col[(2 * ti + u) * 8 * kST + k0];
-              fb[buf][q][u] = col[(2 * tj + u) * 8 * kST + k0];
-            }
+            for (int u = 0; u < WA; ++u) fa[buf][q][u] = col[(a0 + u) * 8 * kST + k0];
+#pragma unroll
+            for (int v = 0; v < 2; ++v) fb[buf][q][v] = col[(b0 + v) * 8 * kST + k0];
           }
         };
         load(0, 0);
@@ -369,12 +379,15 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
           if (kk + 1 < kTM / 4) load((kk + 1) & 1, (kk + 1) * 4);
 #pragma unroll
           for (int q = 0; q < TPW; ++q) {
+            // unpredicated: a per-DMMA predicate makes ptxas wrap every DMMA in a warp-sync and
+            // branch, which costs more than the masked-out blocks (diagonal lower halves, padding,
+            // empty slots) compute; their accumulators are simply never stored
+            // (tools/syrk_probe.cu: masked 6.2 cycles/useful DMMA vs unpredicated 4.0/slot)
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < WA; ++u)
 #pragma unroll
               for (int v = 0; v < 2; ++v)
-                if (vmask[q] & (1 << (2 * u + v)))
-                  dmma884(acc[q][u][v][0], acc[q][u][v][1], fa[kk & 1][q][u], fb[kk & 1][q][v]);
+                dmma884(acc[q][u][v][0], acc[q][u][v][1], fa[kk & 1][q][u], fb[kk & 1][q][v]);
           }
         }
       }
@@ -386,10 +399,10 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
     for (int q = 0; q < TPW; ++q) {
       if (tl[q].x < 0) continue;
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < WA; ++u)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int a = 2 * tl[q].x + u, b = 2 * tl[q].y + v;
+          const int a = tl[q].x + u, b = tl[q].y + v;
           if (a < NB && b < NB && a <= b) {
             const int row = a * 8 + fr, colx = b * 8 + 2 * fk;
             G[row + (size_t)colx * A.LG] = acc[q][u][v][0];
@@ -577,6 +590,25 @@ __global__ void k_exp_check(const double* __restrict__ x, int64_t n, double* __r
 
 TargetView view(const kid_ctx* c) { return TargetView{c->tbase, c->tld, c->tidx, c->nt}; }
 
+// (WA, TPW) warp-tile layouts of the fused pass' SYRK
+#define KID_LAYOUT_SWITCH(DD, M)               \
+  if (WA == 1) {                               \
+    switch (TPW) {                             \
+      case 1: M(DD, 1, 1) break;               \
+      case 2: M(DD, 2, 1) break;               \
+      case 3: M(DD, 3, 1) break;               \
+      case 4: M(DD, 4, 1) break;               \
+      case 5: M(DD, 5, 1) break;               \
+      default: M(DD, 6, 1) break;              \
+    }                                          \
+  } else {                                     \
+    switch (TPW) {                             \
+      case 1: case 2: case 3: M(DD, 3, 2) break; \
+      case 4: M(DD, 4, 2) break;               \
+      default: M(DD, 5, 2) break;              \
+    }                                          \
+  }
+
 #define KID_DISPATCH_D(d, MACRO) \
   switch (d) {                   \
     case 1: MACRO(1); break;     \
@@ -751,17 +783,26 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   }
   const int NBN = ceil_to(meff, 8) / 8;
   const int LG = NBN * 8;
-  // upper-triangular 16x16 warp tiles (2x2 blocks), row-major
-  const int NBT = (NBN + 1) / 2;
+  // upper-triangular warp tiles of WA x 2 blocks (8x16 when NBN <= 12, else 16x16), row-major,
+  // as (a0, b0) block coordinates; fewer padded slots than 16x16 tiles for the small-m configs
+  const int WA = NBN <= 12 ? 1 : 2;
   std::vector<int2> tiles;
-  for (int a = 0; a < NBT; ++a)
-    for (int b = a; b < NBT; ++b) tiles.push_back(make_int2(a, b));
+  if (WA == 1) {
+    for (int a = 0; a < NBN; ++a)
+      for (int b = a; b < NBN; b += 2) tiles.push_back(make_int2(a, b));
+  } else {
+    const int NBT = (NBN + 1) / 2;
+    for (int a = 0; a < NBT; ++a)
+      for (int b = a; b < NBT; ++b) tiles.push_back(make_int2(2 * a, 2 * b));
+  }
   const int nb = (int)tiles.size();
+  const int tpw_max = WA == 1 ? 6 : 5;
   int TPW = 1;
-  for (int cand = 1; cand <= 5; ++cand) {
+  for (int cand = 1; cand <= tpw_max; ++cand) {
     TPW = cand;
     if (nb <= kMW * cand) break;
   }
+  if (WA == 2 && TPW < 3) TPW = 3;  // the instantiated 16x16 layouts (KID_LAYOUT_SWITCH)
   const int per_part = kMW * TPW;
   const int nparts = (nb + per_part - 1) / per_part;
   std::vector<int2> blist((size_t)nparts * per_part, make_int2(-1, -1));
@@ -774,7 +815,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     }
   }
   const int r4 = ceil_to((int)r, 4);
-  const int TS = ceil_to(r4 > 0 ? r4 : 4, 2) * kST, TN = ceil_to(NBN, 2) * 8 * kST;
+  const int TS = ceil_to(r4 > 0 ? r4 : 4, 2) * kST, TN = ceil_to(NBN + 1, 2) * 8 * kST;
   const size_t smem = sizeof(double) * ((size_t)ceil_to(d * m, 2) + (size_t)kStages * (TS + TN) +
                                         (size_t)r4 * frag_stride(meff));
   if (smem > 200 * 1024 || NBN > 16 || getenv("KID_FORCE_LARGE")) return gram_dev_large(c, h, r, d_out);
@@ -783,15 +824,8 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   int per_sm = 1;
   {
     const void* fn = nullptr;
-#define PICK(DD, BB) fn = (const void*)k_gram<DD, BB>;
-#define PICK_D(DD)                 \
-  switch (TPW) {                   \
-    case 1: PICK(DD, 1) break;     \
-    case 2: PICK(DD, 2) break;     \
-    case 3: PICK(DD, 3) break;     \
-    case 4: PICK(DD, 4) break;     \
-    default: PICK(DD, 5) break;    \
-  }
+#define PICK(DD, BB, WW) fn = (const void*)k_gram<DD, BB, WW>;
+#define PICK_D(DD) KID_LAYOUT_SWITCH(DD, PICK)
     KID_DISPATCH_D(d, PICK_D)
 #undef PICK_D
 #undef PICK
@@ -835,19 +869,12 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     KID_CK(c, cudaMemsetAsync(A.trace, 0, sizeof(long long) * trace_n, c->stream));
   }
   dim3 grid(nchunks, nparts);
-#define LAUNCH_B(DD, BB)                                                                           \
-  {                                                                                                \
-    cudaFuncSetAttribute(k_gram<DD, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    k_gram<DD, BB><<<grid, kGT, smem, c->stream>>>(A);                                             \
+#define LAUNCH_B(DD, BB, WW)                                                                           \
+  {                                                                                                    \
+    cudaFuncSetAttribute(k_gram<DD, BB, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    k_gram<DD, BB, WW><<<grid, kGT, smem, c->stream>>>(A);                                             \
   }
-#define LAUNCH(DD)                   \
-  switch (TPW) {                     \
-    case 1: LAUNCH_B(DD, 1); break;  \
-    case 2: LAUNCH_B(DD, 2); break;  \
-    case 3: LAUNCH_B(DD, 3); break;  \
-    case 4: LAUNCH_B(DD, 4); break;  \
-    default: LAUNCH_B(DD, 5); break; \
-  }
+#define LAUNCH(DD) KID_LAYOUT_SWITCH(DD, LAUNCH_B)
   prof_begin(c);
   KID_DISPATCH_D(d, LAUNCH)
 #undef LAUNCH
