@@ -339,7 +339,7 @@ def run_e2e(args, dev, prob, torch, ws, rank):
         e0.record(stream)
         dev.set_points_colmajor_ptr(host.data_ptr(), N, d, prob.offset)
         prob.split()
-        tg = dev.targets()
+        tg = dev.targets(view=True)  # D2H into a page-locked host buffer
         sd, sk, DtD, _ = dev.recon_error(prob.h, prob.skel, prob.P)
         if ws > 1:
             g = torch.tensor(DtD, device="cuda")
@@ -359,7 +359,7 @@ def run_e2e(args, dev, prob, torch, ws, rank):
     d2h = m * 8 + 8 + 8 + prob.nt * 8 + (2 + m * m) * 8 + m * d * 8
     return {"value": prob.entries() * ws / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
-            "path": "kid_set_points(pinned) -> kid_split -> kid_get_targets -> kid_recon_error"}
+            "path": "kid_set_points(pinned) -> kid_split -> kid_get_targets(pinned) -> kid_recon_error"}
 
 
 # ----------------------------------------------------------------- CPU baseline (oracle port)

@@ -48,6 +48,10 @@ extern "C" {
 typedef struct kid_ctx kid_ctx;
 
 int kid_abi_version(void);
+/* Page-locked host memory for the host-buffer entry points (optional; any host buffer works,
+ * pinned ones avoid the driver's staging copy). */
+void* kid_host_alloc(size_t bytes);
+void kid_host_free(void* p);
 /* Create a context on CUDA device `device` (one per process/GPU). */
 int kid_create(kid_ctx** out, int32_t device);
 void kid_destroy(kid_ctx* ctx);

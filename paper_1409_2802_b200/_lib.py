@@ -33,7 +33,7 @@ _cuda = None
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
 
-SYMBOLS = ["kid_abi_version", "kid_create", "kid_destroy", "kid_last_error", "kid_set_stream", "kid_synchronize",
+SYMBOLS = ["kid_abi_version", "kid_host_alloc", "kid_host_free", "kid_create", "kid_destroy", "kid_last_error", "kid_set_stream", "kid_synchronize",
            "kid_set_points", "kid_set_points_device", "kid_split", "kid_split_candidates", "kid_split_finish",
            "kid_get_targets", "kid_set_block", "kid_block_shape", "kid_row_norms", "kid_row_norms_dev", "kid_gram",
            "kid_gram_dev", "kid_leverage", "kid_leverage_dev", "kid_recon_error", "kid_recon_prepare",
@@ -50,6 +50,10 @@ def cuda_lib():
         i64, i32, dbl, vp, u32 = C.c_int64, C.c_int32, C.c_double, C.c_void_p, C.c_uint32
         P = C.POINTER
         L.kid_abi_version.restype = C.c_int
+        L.kid_host_alloc.restype = vp
+        L.kid_host_alloc.argtypes = [C.c_size_t]
+        L.kid_host_free.argtypes = [vp]
+        L.kid_host_free.restype = None
         L.kid_create.argtypes = [P(vp), i32]
         L.kid_destroy.argtypes = [vp]
         L.kid_destroy.restype = None
@@ -101,15 +105,30 @@ class Device:
         if rc:
             raise KidError(rc, f"kid_create(device={device}) failed (no CUDA device?)")
         self.h = h
+        self._pinned = None  # (ptr, bytes) reusable page-locked buffer
         self.N = 0
         self.d = 0
         self.m = 0
         self.nt = 0
 
     def close(self):
+        if self._pinned:
+            self.L.kid_host_free(self._pinned[0])
+            self._pinned = None
         if self.h:
             self.L.kid_destroy(self.h)
             self.h = None
+
+    def pinned(self, nbytes: int) -> int:
+        """A reusable page-locked host buffer of at least nbytes (freed with the Device)."""
+        if not self._pinned or self._pinned[1] < nbytes:
+            if self._pinned:
+                self.L.kid_host_free(self._pinned[0])
+            ptr = self.L.kid_host_alloc(max(nbytes, 1))
+            if not ptr:
+                raise KidError(KID_E_OOM, "kid_host_alloc failed")
+            self._pinned = (ptr, nbytes)
+        return self._pinned[0]
 
     def __del__(self):
         try:
@@ -198,7 +217,14 @@ class Device:
         self.nt, self.m = nt.value, src_idx.size
         return nt.value
 
-    def targets(self) -> np.ndarray:
+    def targets(self, view: bool = False) -> np.ndarray:
+        """Target indices (geometry.hpp:58-60). view=True returns a view of the Device's pinned
+        buffer (no host copy; valid until the next pinned-buffer use)."""
+        if view:
+            ptr = self.pinned(8 * max(self.nt, 1))
+            out = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_int64)), shape=(max(self.nt, 1),))
+            self._ck(self.L.kid_get_targets.__call__(self.h, out, self.nt), "kid_get_targets")
+            return out[: self.nt]
         out = np.zeros(max(self.nt, 1), np.int64)
         self._ck(self.L.kid_get_targets(self.h, out, self.nt), "kid_get_targets")
         return out[: self.nt].copy()

@@ -95,6 +95,21 @@ extern "C" {
 
 int kid_abi_version(void) { return 1; }
 
+// Page-locked host buffers for the host-buffer entry points (a pageable destination makes the
+// driver stage the copy: 8 MB of target indices D2H take ~1.8 ms pageable vs ~0.2 ms pinned).
+void* kid_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes ? bytes : 1) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void kid_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int kid_create(kid_ctx** out, int32_t device) {
   if (!out) return KID_E_ERROR;
   *out = nullptr;

@@ -136,7 +136,15 @@ constexpr int kTraceTiles = 64;
 // (DMMA and DFMA do not overlap on sm_100: tools/fp64_overlap.cu); the split hides latency.
 constexpr int kMW = 8, kEW = 12, kGT = (kMW + kEW) * 32;  // 640 threads
 #ifndef KID_EVAL_ILP
-#define KID_EVAL_ILP 2
+#define KID_EVAL_ILP 3
+#endif
+#ifndef KID_EVAL_HIGH  // 1: eval warps take the high warp ids (the issue arbiter favours them)
+#define KID_EVAL_HIGH 0
+#endif
+constexpr int kEvalW0 = KID_EVAL_HIGH ? 8 : 0, kMmaW0 = KID_EVAL_HIGH ? 0 : 12;
+#ifndef KID_EVAL_REGS  // setmaxnreg split for D < 8 (strings: PTX immediates)
+#define KID_EVAL_REGS "64"
+#define KID_MMA_REGS "144"
 #endif
 constexpr int kStages = 3;
 constexpr int kST = kTM + 4;  // column-major tile stride
@@ -159,8 +167,7 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
   } while (0)
 
 static_assert(kGT == 640, "setmaxnreg budget below assumes 640 threads (96 registers each at launch)");
-static_assert(3 * 128 * (96 - 64) >= 2 * 128 * (144 - 96) && 3 * 128 * (96 - 72) >= 2 * 128 * (128 - 96),
-              "setmaxnreg.inc must not exceed what setmaxnreg.dec releases");
+static_assert(3 * 128 * (96 - 72) >= 2 * 128 * (128 - 96), "setmaxnreg.inc must not exceed what setmaxnreg.dec releases");
 template <int D, int TPW, int WA>
 __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
   const int d = D ? D : A.d;
@@ -194,13 +201,13 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
   // Eval warps take the LOW warp ids: the issue arbiter favours the highest warp id, so the
   // DMMA warps (long pipe occupancy, few instructions) win issue slots and the eval warps fill
   // the gaps instead of starving them.
-  if (warp < kEW) {
+  if (warp >= kEvalW0 && warp < kEvalW0 + kEW) {
     // ================================================================ eval warps
     // register split: the launch allocates 96/thread (640 threads); setmaxnreg.inc can only take
     // what the decreasing warpgroups release, so 384 (96 - E) >= 256 (M - 96) must hold
     if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
-    else asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
-    const int ew = warp;  // this warp evaluates columns j = ew, ew + kEW, ...
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 " KID_EVAL_REGS ";\n" ::: "memory");
+    const int ew = warp - kEvalW0;  // this warp evaluates columns j = ew, ew + kEW, ...
     // target coordinates live in registers for the compiled dimensions; the generic-d path
     // (D == 0) re-reads them through L1 (tc holds a single slot there)
     constexpr int DR = D ? D : 1;
@@ -262,13 +269,13 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
     }
     if (part == 0) {
       sk = warp_sum(sk);
-      if (lane == 0) red[warp] = sk;
+      if (lane == 0) red[ew] = sk;
     }
   } else {
     // ================================================================ MMA warps
     if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;\n" ::: "memory");
-    else asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n" ::: "memory");
-    const int mw = warp - kEW;
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 " KID_MMA_REGS ";\n" ::: "memory");
+    const int mw = warp - kMmaW0;
     int2 tl[TPW];  // (a0, b0) block coordinates of WA x 2-block warp tiles, x = -1: empty slot
 #pragma unroll
     for (int q = 0; q < TPW; ++q) tl[q] = A.blist[((size_t)part * kMW + mw) * TPW + q];
@@ -888,7 +895,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     cudaFree(A.trace);
     // per-phase mean cycles over tiles 4..kTraceTiles-1 (steady state), MMA warp kEW and eval warp 0
     auto at_raw = [&](int w, int it, int ev) { return tr[((size_t)w * kTraceTiles + it) * 4 + ev]; };
-    auto at = [&](int w, int it, int ev) { return at_raw(w == 0 ? kEW : (w == kMW ? 0 : w), it, ev); };
+    auto at = [&](int w, int it, int ev) { return at_raw(w == 0 ? kMmaW0 : (w == kMW ? kEvalW0 : w), it, ev); };
     double mw_full = 0, mw_g1 = 0, mw_syrk = 0, ew_empty = 0, ew_eval = 0, tile = 0;
     int n = 0;
     for (int it = 4; it + 1 < kTraceTiles; ++it) {
@@ -903,9 +910,9 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     }
     for (int it = 10; it < 11; ++it) {
       fprintf(stderr, "[kid trace] tile %d gemm1 cycles per MMA warp:", it);
-      for (int w = kEW; w < kEW + kMW; ++w) fprintf(stderr, " %lld", at_raw(w, it, 2) - at_raw(w, it, 1));
+      for (int w = kMmaW0; w < kMmaW0 + kMW; ++w) fprintf(stderr, " %lld", at_raw(w, it, 2) - at_raw(w, it, 1));
       fprintf(stderr, " | syrk+bar:");
-      for (int w = kEW; w < kEW + kMW; ++w) fprintf(stderr, " %lld", at_raw(w, it, 3) - at_raw(w, it, 2));
+      for (int w = kMmaW0; w < kMmaW0 + kMW; ++w) fprintf(stderr, " %lld", at_raw(w, it, 3) - at_raw(w, it, 2));
       fprintf(stderr, "\n");
     }
     for (int it = 10; it < 10; ++it) {
