@@ -189,3 +189,56 @@ def test_recon_error_large_m_path(oracle, dev, monkeypatch, d, n, eps, force):
     assert np.all(np.abs(DtD - r_DtD) <= bound + 1e-300)
     G, gsk = dev.gram(t.h)
     assert _gram_ok(G, r_KtK)
+
+
+def test_edge_cases(oracle, dev):
+    """Degenerate shapes the reference handles: m = 1 source, full-rank skeleton (r = m: D == 0
+    exactly), rank-1 skeleton, targets fewer than one tile, an empty explicit block, d = 64."""
+    # m = 1
+    t, K = _block(oracle, d=2, N=5000, n=1)
+    dev.set_points(t.points)
+    src, rho, nt = dev.split(t.center, 1, 2.0)
+    assert np.array_equal(src, t.split.source_indices) and nt == K.shape[0]
+    assert np.allclose(dev.row_norms(t.h), oracle.row_norms(K), rtol=1e-12, atol=0)
+    G, sk = dev.gram(t.h)
+    assert G.shape == (1, 1) and G[0, 0] == pytest.approx((K[:, 0] ** 2).sum(), rel=1e-12)
+    # full-rank and rank-1 skeletons
+    t, K = _block(oracle, d=3, N=8000, n=24)
+    dev.set_points(t.points)
+    dev.split(t.center, 24, 2.0)
+    skel = np.arange(24)[::-1].copy()
+    P = np.zeros((24, 24))
+    P[np.arange(24), skel] = 1.0
+    sd, sk, DtD, _ = dev.recon_error(t.h, skel, P)
+    assert sd == 0.0 and np.all(DtD == 0.0) and sk == pytest.approx(np.sum(K * K), rel=1e-12)
+    res = oracle.compress_id(K, np.arange(K.shape[0]), fixed_r=1)
+    sd, sk, DtD, _ = dev.recon_error(t.h, res.skeleton, res.P)
+    r_sd, _, r_DtD, _ = oracle.residual_stats(K, res.skeleton, res.P)
+    assert sd == pytest.approx(r_sd, rel=1e-9)
+    # fewer targets than one 32-row tile, and no targets at all (explicit blocks)
+    tg = oracle.gen_normal(3, 7, 3) + 5.0
+    sr = oracle.gen_normal(3, 11, 4)
+    dev.set_block(tg, sr)
+    Kb = oracle.kernel_matrix(tg, sr, 1.3)
+    G, sk = dev.gram(1.3)
+    assert _gram_ok(G, Kb.T @ Kb)
+    assert np.allclose(dev.row_norms(1.3), oracle.row_norms(Kb), rtol=1e-12, atol=0)
+    dev.set_block(np.zeros((0, 3)), sr)
+    G, sk = dev.gram(1.3)
+    assert sk == 0.0 and np.all(G == 0.0)
+    assert dev.row_norms(1.3).size == 0
+
+
+def test_split_high_dimension(oracle, dev):
+    """d = 64 (BASELINE c4): the generic-d kernels, bit-exact split and parity of the passes."""
+    t, K = _block(oracle, d=64, N=3000, n=64, xi=1.0)
+    dev.set_points(t.points)
+    src, rho, nt = dev.split(t.center, 64, 1.0)
+    assert np.array_equal(src, t.split.source_indices) and rho == t.split.rho
+    assert np.array_equal(dev.targets(), t.split.target_indices)
+    w = dev.row_norms(t.h)
+    ref = oracle.row_norms(K)
+    nz = ref > 0
+    assert np.all(np.abs(w[nz] - ref[nz]) <= 1e-12 * ref[nz])
+    G, _ = dev.gram(t.h)
+    assert _gram_ok(G, K.T @ K)
