@@ -324,6 +324,49 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_split(args):
+    """--pass split: pass 1 (split_sources_targets) on the config's points, HBM roofline of its
+    kernels (algorithmic bytes 8 d N read + 8 N_T written)."""
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    torch.cuda.set_stream(torch.cuda.Stream())
+    wl = WORKLOADS[args.config]
+    from paper_1409_2802_b200._lib import Device
+    dev = Device(local)
+    prob = Problem(wl, dev, torch, 1, 0)
+    dev.set_stream(torch.cuda.current_stream().cuda_stream)
+    N, d, m = wl["N"], wl["d"], wl["m"]
+    for _ in range(args.warmup):
+        prob.split()
+    torch.cuda.synchronize()
+    dev.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record()
+        prob.split()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    kms = dev.profile_read()  # per split: [k_dist_cand, k_compact]
+    dev.profile(False)
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    kd = float(np.mean(kms[0::2])) if len(kms) >= 2 else float("nan")
+    kc = float(np.mean(kms[1::2])) if len(kms) >= 2 else float("nan")
+    peak = 6552.6
+    b_alg = 8.0 * d * N + 8.0 * prob.nt
+    b_dist = 8.0 * d * N + 8.0 * N  # read points, write dist
+    b_comp = 8.0 * N + 8.0 * prob.nt  # read dist, write indices
+    line = {"metric": "split_sources_targets points/s (pass 1)", "value": N / (ms / 1e3), "unit": "points/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "dtype": "f64", "config": {"workload": f"{args.config}: N={N}, d={d}, m={m}, N_T={prob.nt}"},
+            "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak,
+                         "achieved": b_alg / (ms / 1e3) / 1e9, "frac": b_alg / (ms / 1e3) / 1e9 / peak,
+                         "algorithmic_bytes": b_alg,
+                         "k_dist_cand": {"ms": kd, "gbs": b_dist / (kd / 1e3) / 1e9},
+                         "k_compact": {"ms": kc, "gbs": b_comp / (kc / 1e3) / 1e9}}}
+    print(json.dumps(line), flush=True)
+
+
 def run_e2e(args, dev, prob, torch, ws, rank):
     """Same metric through the C-ABI with host buffers (pinned points H2D every step)."""
     wl = prob.wl
@@ -446,11 +489,14 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=50000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.pass_ == "split":
+        run_split(args)
     else:
         run_ours(args)
 

@@ -135,7 +135,7 @@ void kid_destroy(kid_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   void* bufs[] = {c->pts_own, c->dist, c->tgt_idx, c->blk_tgt, c->src, c->src_perm, c->P2,
-                  c->scratch, c->partial, c->counter};
+                  c->scratch, c->partial, c->counter, c->sort_tmp};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->hbuf) cudaFreeHost(c->hbuf);

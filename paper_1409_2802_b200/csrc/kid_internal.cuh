@@ -142,6 +142,8 @@ struct kid_ctx {
   size_t hbuf_cap = 0;
   int64_t* counter = nullptr;  // device counters [8]
   cublasHandle_t blas = nullptr;  // large-m fallback of the Gram passes
+  void* sort_tmp = nullptr;       // CUB radix-sort temporary storage (pass 1)
+  size_t sort_tmp_cap = 0;
 
   // kernel timing (kid_profile): CUDA events on the launching stream around each pass'
   // dominant kernel, read back by kid_profile_read

@@ -129,7 +129,9 @@ __global__ void k_gather_sources(const double* __restrict__ pts, int64_t N, int 
 }
 
 // (d) decoupled look-back stable compaction ------------------------------------
-constexpr int kCT = 256, kIPT = 8, kTile = kCT * kIPT;
+// 256 threads x 16 items per tile; the tile's first warp resolves its exclusive prefix by a
+// warp-wide look-back over up to 32 predecessors at a time (status word = 2-bit state | count).
+constexpr int kCT = 256, kIPT = 16, kTile = kCT * kIPT;
 constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 __device__ __forceinline__ bool is_source(const int64_t* __restrict__ s, int64_t n, int64_t i) {
@@ -153,78 +155,87 @@ __global__ void __launch_bounds__(kCT) k_compact(const double* __restrict__ dist
   if (threadIdx.x == 0) tile_s = atomicAdd(tile_counter, 1u);
   __syncthreads();
   const int64_t tile = tile_s;
-  const int64_t base = tile * kTile + (int64_t)threadIdx.x * kIPT;
-  unsigned flags = 0;
-  int cnt = 0;
-  if (base + kIPT <= N) {
-    const double2* p2 = reinterpret_cast<const double2*>(dist + base);
-#pragma unroll
-    for (int j = 0; j < kIPT / 2; ++j) {
-      const double2 v = __ldcs(p2 + j);
-      bool f0 = v.x >= cutoff, f1 = v.y >= cutoff;
-      if (f0 && v.x <= rho) f0 = !is_source(src_local, n_src, base + 2 * j);
-      if (f1 && v.y <= rho) f1 = !is_source(src_local, n_src, base + 2 * j + 1);
-      flags |= (unsigned)f0 << (2 * j);
-      flags |= (unsigned)f1 << (2 * j + 1);
-    }
-  } else {
-    for (int j = 0; j < kIPT; ++j) {
-      const int64_t i = base + j;
-      if (i < N) {
-        const double v = dist[i];
-        bool f = v >= cutoff;
-        if (f && v <= rho) f = !is_source(src_local, n_src, i);
-        flags |= (unsigned)f << j;
-      }
-    }
-  }
-  cnt = __popc(flags);
-  // block-wide exclusive scan of cnt
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = cnt;
+  // coalesced loads: item j of thread t is element tile*kTile + j*kCT + t
+  const int64_t base = tile * kTile + threadIdx.x;
+  unsigned flags = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
+  for (int j = 0; j < kIPT; ++j) {
+    const int64_t i = base + (int64_t)j * kCT;
+    if (i < N) {
+      const double v = __ldcs(dist + i);
+      bool f = v >= cutoff;
+      if (f && v <= rho) f = !is_source(src_local, n_src, i);
+      flags |= (unsigned)f << j;
+    }
   }
-  if (lane == 31) warp_tot[warp] = incl;
+  // per-(j) rank within the tile: items are ordered by (j, t); count flagged items of each j
+  // across the block with one warp-ballot pass per j
+  __shared__ int jcount[kIPT][kCT / 32];
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    const unsigned b = __ballot_sync(0xffffffffu, (flags >> j) & 1u);
+    if (lane == 0) jcount[j][warp] = __popc(b);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     long long run = 0;
-    for (int w = 0; w < kCT / 32; ++w) {
-      const long long t = warp_tot[w];
-      warp_tot[w] = run;
-      run += t;
-    }
-    const long long total = run;
-    long long excl = 0;
-    if (tile == 0) {
-      __threadfence();
-      atomicExch(&tile_status[0], kStInc | (unsigned long long)total);
-    } else {
-      __threadfence();
-      atomicExch(&tile_status[tile], kStAgg | (unsigned long long)total);
-      int64_t p = tile - 1;
-      for (;;) {
-        const unsigned long long s = *((volatile unsigned long long*)&tile_status[p]);
-        const unsigned long long st = s & ~kValMask;
-        if (st == 0) continue;
-        excl += (long long)(s & kValMask);
-        if (st == kStInc) break;
-        --p;
+    for (int j = 0; j < kIPT; ++j)
+      for (int w = 0; w < kCT / 32; ++w) {
+        const int t = jcount[j][w];
+        jcount[j][w] = (int)run;
+        run += t;
       }
-      __threadfence();
-      atomicExch(&tile_status[tile], kStInc | (unsigned long long)(excl + total));
-    }
-    excl_s = excl;
-    if (tile == ntiles - 1) *total_out = excl + total;
+    warp_tot[0] = run;
   }
   __syncthreads();
-  int64_t pos = excl_s + warp_tot[warp] + (incl - cnt);
-  while (flags) {
-    const int j = __ffs(flags) - 1;
-    flags &= flags - 1;
-    out[pos++] = base + j;
+  const long long total = warp_tot[0];
+  if (warp == 0) {
+    long long excl = 0;
+    if (tile == 0) {
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&tile_status[0], kStInc | (unsigned long long)total);
+      }
+    } else {
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&tile_status[tile], kStAgg | (unsigned long long)total);
+      }
+      int64_t p = tile - 1;
+      for (;;) {
+        const int64_t q = p - lane;
+        unsigned long long sv = kStInc;  // before tile 0: inclusive 0
+        if (q >= 0) {
+          do {
+            sv = *((volatile unsigned long long*)&tile_status[q]);
+          } while ((sv & ~kValMask) == 0);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, (sv & ~kValMask) == kStInc);
+        const int first = inc ? __ffs(inc) - 1 : 31;
+        long long v = lane <= first ? (long long)(sv & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (inc) break;
+        p -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&tile_status[tile], kStInc | (unsigned long long)(excl + total));
+      }
+    }
+    if (lane == 0) {
+      excl_s = excl;
+      if (tile == ntiles - 1) *total_out = excl + total;
+    }
+  }
+  __syncthreads();
+  const long long excl = excl_s;
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    const unsigned b = __ballot_sync(0xffffffffu, (flags >> j) & 1u);
+    if ((flags >> j) & 1u) out[excl + jcount[j][warp] + __popc(b & ((1u << lane) - 1u))] = base + (int64_t)j * kCT;
   }
 }
 
@@ -234,16 +245,13 @@ int sort_candidates(kid_ctx* c, unsigned long long* key, unsigned long long* idx
   size_t tmp1 = 0, tmp2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp1, idx, idx_alt, key, key_alt, (int)count, 0, end_bit_idx, c->stream);
   cub::DeviceRadixSort::SortPairs(nullptr, tmp2, key_alt, key, idx_alt, idx, (int)count, 0, 64, c->stream);
-  void* tmp = nullptr;
-  size_t cap = 0;
   const size_t need = std::max(tmp1, tmp2);
-  if (ensure(c, &tmp, &cap, need)) return KID_E_OOM;
+  if (ensure(c, &c->sort_tmp, &c->sort_tmp_cap, need)) return KID_E_OOM;
+  void* tmp = c->sort_tmp;
   KID_CK(c, cub::DeviceRadixSort::SortPairs(tmp, tmp1, idx, idx_alt, key, key_alt, (int)count, 0, end_bit_idx, c->stream));
   c->launches += 2;
   KID_CK(c, cub::DeviceRadixSort::SortPairs(tmp, tmp2, key_alt, key, idx_alt, idx, (int)count, 0, 64, c->stream));
   c->launches += 2;
-  KID_CK(c, cudaStreamSynchronize(c->stream));
-  cudaFree(tmp);
   return KID_OK;
 }
 
@@ -283,15 +291,11 @@ int split_candidates(kid_ctx* c, const double* center_h, int64_t n, double* cand
   {
     size_t tmpb = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tmpb, skeys, skeys2, (int)S, 0, 64, c->stream);
-    void* tmp = nullptr;
-    size_t tcap = 0;
-    if (ensure(c, &tmp, &tcap, tmpb)) return KID_E_OOM;
-    KID_CK(c, cub::DeviceRadixSort::SortKeys(tmp, tmpb, skeys, skeys2, (int)S, 0, 64, c->stream));
+    if (ensure(c, &c->sort_tmp, &c->sort_tmp_cap, tmpb)) return KID_E_OOM;
+    KID_CK(c, cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmpb, skeys, skeys2, (int)S, 0, 64, c->stream));
     c->launches += 4;
     KID_CK(c, cudaMemcpyAsync(T_key, skeys2 + (nl - 1), sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
                               c->stream));
-    KID_CK(c, cudaStreamSynchronize(c->stream));
-    cudaFree(tmp);
   }
   const int blocks = c->sms * 8;
   prof_begin(c);
