@@ -48,10 +48,13 @@ __device__ __forceinline__ double gauss_exact(double sq, double denom) {
 //   2^(k+600) on the exponent field and one multiply by 2^-600 (exact for normal results,
 //   correctly rounded into the subnormal range; k is clamped where the result rounds to 0).
 // 11 FP64-pipe ops against ~20 for libdevice exp() plus the caller's divide; max error 1 ulp
-// against glibc (tests/test_gpu_parity.py::test_fast_exp_accuracy). Valid for q < 1.4e6.
+// against glibc (tests/test_gpu_parity.py::test_fast_exp_accuracy). q >= 0 of any size: q is
+// clamped to <= 2^17 on its high word (one integer min; exp(-2^17) == 0 in double anyway), which
+// keeps the rounded multiple of ln2/1024 inside int32.
 constexpr int kExpTab = 1024;
 __device__ __forceinline__ double exp_neg_fast(double q, const double* __restrict__ tab) {
   const double shifter = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest-integer
+  q = __hiloint2double(min(__double2hiint(q), 0x41000000), __double2loint(q));  // q <= ~2^17
   double kd = fma(q, -1477.3197218702985, shifter);  // round(-q * 1024 / ln2)
   const int n = __double2loint(kd);
   kd -= shifter;
@@ -64,6 +67,24 @@ __device__ __forceinline__ double exp_neg_fast(double q, const double* __restric
   const double t = tab[n & (kExpTab - 1)];
   const double y = fma(t, p, t);
   const int k = max(n >> 10, -1100);  // floor(n / 1024), clamped: 2^(k+600) stays normal
+  return __hiloint2double(__double2hiint(y) + ((k + 600) << 20), __double2loint(y)) * 0x1p-600;
+}
+
+// profiling aid only (KID_GRAM_DEBUG 32): exp_neg_fast with the table entry replaced by 1
+__device__ __forceinline__ double exp_neg_notab(double q) {
+  const double shifter = 6755399441055744.0;
+  double kd = fma(q, -1477.3197218702985, shifter);
+  const int n = __double2loint(kd);
+  kd -= shifter;
+  double r = fma(kd, -0.0006769015433292225, -q);
+  r = fma(kd, -1.8634911418658083e-13, r);
+  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p *= r;
+  const double t = 1.0 + (n & 1023) * 1e-300;
+  const double y = fma(t, p, t);
+  const int k = max(n >> 10, -1100);
   return __hiloint2double(__double2hiint(y) + ((k + 600) << 20), __double2loint(y)) * 0x1p-600;
 }
 

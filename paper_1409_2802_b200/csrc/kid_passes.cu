@@ -107,52 +107,55 @@ struct GramArgs {
   int d;
   const double* src;   // m x d col-major, columns already in [skel | non-skel] order
   int m, r, meff;      // meff = m - r
-  double negc;         // -1 / (2 h^2)
-  double cscale;       // 1 / (sqrt(2) h): coordinates pre-scaled so that exp(-||x' - y'||^2)
-  const double* P2;    // r x meff row-major, stride SP (device); nullptr when r == 0
+  double cscale;       // 1 / (sqrt(2) h): coordinates pre-scaled so that K = exp(-||x' - y'||^2)
+  const double* P2;    // r x SP row-major, SP = frag_stride(meff) (device); nullptr when r == 0
   const int2* blist;   // [nparts][kMW][TPW] (a0, b0) first 8x8 block of each WA x 2-block warp tile, x = -1: empty
+  const short* elist;  // [kEW][kEItems]: nA, nB, A items (skeleton columns), B items (4-column groups)
   int nparts;
   int64_t ntiles;
   int nchunks;
   double* partial;     // [nchunks][LG][LG]
   int LG;              // padded Gram leading dimension = ceil8(meff)
   double* partial_sk;  // [nchunks] (written by part 0)
-  int dbg;             // profiling aid (KID_GRAM_DEBUG): 1 skip eval math, 2 skip D = K_N - K_S P2, 4 skip SYRK
+  int dbg;             // profiling aid (KID_GRAM_DEBUG): 1 skip eval math, 2 skip the K_S P2 FMAs, 4 skip SYRK,
+                       // 16 no coordinate copies (ring slots keep tile 0's targets), 32 exp without the table load
   long long* trace;    // profiling aid (KID_GRAM_TRACE): [warp][tile][4] clock64 stamps of CTA 0
 };
 constexpr int kTraceTiles = 64;
 
-// Warp-specialized pipeline (one CTA per SM):
-//   warps 12..19 (kMW "MMA" warps): per tile, D = K_N - K_S P2 (DMMA, balanced block list) then
-//               G += D^T D (DMMA) on static 16x16 warp tiles (2x2 blocks of 8x8) of the upper
-//               triangle, accumulators register-resident across all tiles of the CTA's chunk;
-//   warps 0..11 (kEW "eval" warps): evaluate the next 32 x m K tiles into a kStages-deep
-//               shared-memory ring. Tiles are COLUMN-major (K[col][t], stride kST = 36): lane =
-//               target row, so each thread keeps its target's coordinates in registers, source
-//               coordinates are warp-broadcast, stores are conflict-free, and the DMMA fragment
-//               gathers [(x*8 + (lane>>2)) * kST + (lane&3)] stay conflict-free (36 = 4 mod 16).
+// Warp-specialized pipeline (one CTA per SM), per 32-target tile:
+//   warps 0..11 (kEW "eval" warps) own a host-balanced list of work items:
+//     A item j      : K_S column j of the NEXT tile (exp) -> KS ring (2 slots, eval-private)
+//     B item g      : non-skeleton columns 4g..4g+3 of THIS tile: K_N by exp (4 independent
+//                     chains), then D = K_N - K_S P2 by DFMA against the K_S row of the target
+//                     (KS ring) and -P2 rows (shared memory, LDS.128 broadcasts) -> KN stage
+//     lane = target row throughout, so stores are conflict-free column-major [col][t] (stride
+//     kST = 36 = 4 mod 16, which also makes the DMMA fragment gathers conflict-free);
+//   warps 12..19 (kMW "MMA" warps): G += D^T D (DMMA.8x8x4) on static WA x 2-block warp tiles of
+//     the upper triangle, accumulators register-resident across the CTA's whole target chunk.
 // Hand-off by named barriers: FULL[s] (eval arrive, MMA sync), EMPTY[s] (MMA arrive, eval sync),
-// one MMA-group barrier between the two DMMA phases. Both groups share the FP64 datapath
-// (DMMA and DFMA do not overlap on sm_100: tools/fp64_overlap.cu); the split hides latency.
+// EVAL (eval warps only: K_S of the next tile and the next coordinates are visible).
+// Target coordinates stream through a 4-slot shared-memory ring by cp.async, issued three tiles
+// ahead (the target index of the copy is itself loaded one tile earlier).
+// DMMA and DFMA share the FP64 datapath (tools/fp64_overlap.cu): the split keeps it fed from
+// both sides -- the MMA warps never wait on a GEMM phase, the eval warps fill the DMMA gaps.
 constexpr int kMW = 8, kEW = 12, kGT = (kMW + kEW) * 32;  // 640 threads
-#ifndef KID_EVAL_ILP
-#define KID_EVAL_ILP 3
-#endif
-#ifndef KID_EVAL_HIGH  // 1: eval warps take the high warp ids (the issue arbiter favours them)
-#define KID_EVAL_HIGH 0
-#endif
-constexpr int kEvalW0 = KID_EVAL_HIGH ? 8 : 0, kMmaW0 = KID_EVAL_HIGH ? 0 : 12;
-#ifndef KID_EVAL_REGS  // setmaxnreg split for D < 8 (strings: PTX immediates)
-#define KID_EVAL_REGS "64"
-#define KID_MMA_REGS "144"
-#endif
+constexpr int kEvalW0 = 0, kMmaW0 = kEW;
 constexpr int kStages = 3;
 constexpr int kST = kTM + 4;  // column-major tile stride
-constexpr int kGPW = 6;       // GEMM1 blocks per warp per batch
-constexpr int kBarFull = 1, kBarEmpty = 1 + kStages, kBarMma = 1 + 2 * kStages;
+constexpr int kRing = 4;      // target-coordinate ring slots
+constexpr int kEItems = 48;   // per eval warp: 2 counts + items
+constexpr int kBarFull = 1, kBarEmpty = 1 + kStages, kBarEval = 1 + 2 * kStages;
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // clock64 after a deferred-blocking BAR.SYNC reads the issue time; the shared-memory load and
 // the dependent branch below force the stamp to be taken after the barrier has released.
@@ -166,119 +169,259 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
     }                                                                                              \
   } while (0)
 
+// register split: 640 threads launch with 96 registers each; setmaxnreg.inc can only take what
+// the decreasing warps release: 384 (96 - E) >= 256 (M - 96)
+constexpr int kEvalRegs = 72, kMmaRegs = 128;
 static_assert(kGT == 640, "setmaxnreg budget below assumes 640 threads (96 registers each at launch)");
-static_assert(3 * 128 * (96 - 72) >= 2 * 128 * (128 - 96), "setmaxnreg.inc must not exceed what setmaxnreg.dec releases");
+static_assert(kEW * 32 * (96 - kEvalRegs) >= kMW * 32 * (kMmaRegs - 96), "setmaxnreg.inc exceeds what .dec releases");
+
+// SYRK over one stage for the first N warp tiles: fragments F(x) = D[k0 + fk][x*8 + fr]
+// (A and B operands of D^T D use the same gather), double-buffered across the 8 k-steps.
+template <int N, int TPW, int WA>
+__device__ __forceinline__ void syrk_stage(double (&acc)[TPW][WA][2][2], const int (&fa0)[TPW], const int (&fb0)[TPW],
+                                           const double* __restrict__ col) {
+  double fa[2][N][WA], fb[2][N][2];
+  auto load = [&](int buf, int k0) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+#pragma unroll
+      for (int u = 0; u < WA; ++u) fa[buf][q][u] = col[fa0[q] + u * 8 * kST + k0];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) fb[buf][q][v] = col[fb0[q] + v * 8 * kST + k0];
+    }
+  };
+  load(0, 0);
+#pragma unroll
+  for (int kk = 0; kk < kTM / 4; ++kk) {
+    if (kk + 1 < kTM / 4) load((kk + 1) & 1, (kk + 1) * 4);
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int u = 0; u < WA; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) dmma884(acc[q][u][v][0], acc[q][u][v][1], fa[kk & 1][q][u], fb[kk & 1][q][v]);
+  }
+}
+
 template <int D, int TPW, int WA>
 __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
   const int d = D ? D : A.d;
   const int m = A.m, r = A.r, meff = A.meff;
-  const int r4 = ceil_to(r, 4);
   const int NBN = ceil_to(meff, 8) / 8;
-  const int SP = frag_stride(meff);
-  const int TS = ceil_to(r4 > 0 ? r4 : 4, 2) * kST, TN = ceil_to(NBN + 1, 2) * 8 * kST;  // one stage of K_S / K_N
+  const int r4 = ceil_to(r, 4);
+  const int rS = ceil_to(r > 0 ? r : 1, 2), mN = NBN * 8;
+  const int SPn = frag_stride(meff);  // -P2 row stride (= 4 or 12 mod 16: conflict-free B fragments)
+  const int TS = (r4 > 0 ? r4 : 4) * kST, TN = ceil_to(NBN + 1, 2) * 8 * kST;  // one KS slot / one KN stage
   extern __shared__ __align__(16) double smem[];
-  double* s_src = smem;                        // d x m (scaled)
-  double* KSb = s_src + ceil_to(d * m, 2);     // kStages x (r4 x kST), column-major
-  double* KNb = KSb + (size_t)kStages * TS;    // kStages x (NBN*8 x kST), column-major
-  double* sP = KNb + (size_t)kStages * TN;     // r4 x SP (row-major P2)
-  __shared__ double red[kMW + kEW];
+  double* s_srcS = smem;                         // d x rS: skeleton sources, [k][j]
+  double* s_srcN = s_srcS + (size_t)d * rS;      // d x mN: non-skeleton sources, [k][j]; pad: far away
+  double* sP = s_srcN + (size_t)d * mN;          // r4 x SPn: -P2, row-major (pad rows / columns 0)
+  double* KSb = sP + (size_t)r4 * SPn;           // 2 x (r4 x kST): K_S, column-major [k][t]; rows >= r are 0
+  double* KNb = KSb + 2 * (size_t)TS;            // kStages x (.. x kST): D, column-major [col][t]
+  double* ring = KNb + (size_t)kStages * TN;     // kRing x d x 32 target coordinates (unscaled)
+  __shared__ double red[kEW];
   __shared__ double s_tab[kExpTab];
+  __shared__ short s_el[kEW * kEItems];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = blockIdx.x, part = blockIdx.y;
-  for (int e = tid; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
-  for (int e = tid; e < m * d; e += kGT) s_src[e] = A.src[e] * A.cscale;
-  for (int e = tid; e < kStages * TS; e += kGT) KSb[e] = 0.0;
-  for (int e = tid; e < kStages * TN; e += kGT) KNb[e] = 0.0;
-  for (int e = tid; e < r4 * SP; e += kGT) {
-    const int k = e / SP, n = e % SP;
-    sP[e] = (k < r && n < meff) ? A.P2[(size_t)k * SP + n] : 0.0;
+  for (int e = tid; e < kExpTab; e += kGT) s_tab[e] = c_exp2_tab[e];
+  for (int e = tid; e < kEW * kEItems; e += kGT) s_el[e] = A.elist[e];
+  for (int e = tid; e < d * rS; e += kGT) {
+    const int k = e / rS, j = e % rS;
+    s_srcS[e] = A.src[(size_t)k * m + min(j, max(r - 1, 0))] * A.cscale;
   }
+  // padding sources sit far away: their K entries are exactly 0 (exp_neg_fast clamps q), so the
+  // padding columns of D are 0 and add nothing to sum K^2
+  for (int e = tid; e < d * mN; e += kGT) {
+    const int k = e / mN, j = e % mN;
+    s_srcN[e] = j < meff ? A.src[(size_t)k * m + r + j] * A.cscale : 1.0e4;
+  }
+  const int SP = frag_stride(meff);
+  for (int e = tid; e < r4 * SPn; e += kGT) {
+    const int k = e / SPn, n = e % SPn;
+    sP[e] = (k < r && n < meff) ? -A.P2[(size_t)k * SP + n] : 0.0;
+  }
+  for (int e = tid; e < 2 * TS; e += kGT) KSb[e] = 0.0;
+  for (int e = tid; e < kStages * TN; e += kGT) KNb[e] = 0.0;
+  for (int e = tid; e < kRing * d * kTM; e += kGT) ring[e] = 0.0;
   const int64_t tile_lo = A.ntiles * chunk / A.nchunks, tile_hi = A.ntiles * (chunk + 1) / A.nchunks;
   const int ntile = (int)(tile_hi - tile_lo);
   __syncthreads();
 
-  // Eval warps take the LOW warp ids: the issue arbiter favours the highest warp id, so the
-  // DMMA warps (long pipe occupancy, few instructions) win issue slots and the eval warps fill
-  // the gaps instead of starving them.
   if (warp >= kEvalW0 && warp < kEvalW0 + kEW) {
     // ================================================================ eval warps
-    // register split: the launch allocates 96/thread (640 threads); setmaxnreg.inc can only take
-    // what the decreasing warpgroups release, so 384 (96 - E) >= 256 (M - 96) must hold
-    if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
-    else asm volatile("setmaxnreg.dec.sync.aligned.u32 " KID_EVAL_REGS ";\n" ::: "memory");
-    const int ew = warp - kEvalW0;  // this warp evaluates columns j = ew, ew + kEW, ...
-    // target coordinates live in registers for the compiled dimensions; the generic-d path
-    // (D == 0) re-reads them through L1 (tc holds a single slot there)
-    constexpr int DR = D ? D : 1;
-    double tc[DR], tn[DR];
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kEvalRegs) : "memory");
+    const int ew = warp - kEvalW0;
+    const short* el = s_el + ew * kEItems;
+    const int nA = el[0], nB = el[1];
+    const short* itA = el + 2;
+    const short* itB = el + 2 + nA;
     double sk = 0.0;
-    {
-      const int64_t i = tile_lo * kTM + lane;
-#pragma unroll
-      for (int k = 0; k < DR; ++k) tc[k] = (k < d && ntile > 0 && i < A.tv.nt) ? tcoord(A.tv, i, k) * A.cscale : 0.0;
+    const bool copier = ew < d && !(A.dbg & 16);  // warp ew copies coordinate dims ew, ew + kEW, ...
+    const int64_t nt = A.tv.nt;
+    auto trow = [&](int tl) -> int64_t {  // target row of lane in local tile tl, -1 past the end
+      const int64_t i = (tile_lo + tl) * kTM + lane;
+      return (tl < ntile && i < nt) ? i : -1;
+    };
+    auto row_of = [&](int tl) -> int64_t {
+      const int64_t i = trow(tl);
+      return i < 0 ? -1 : (A.tv.idx ? A.tv.idx[i] : i);
+    };
+    auto issue_copy = [&](int tl, int64_t prow) {  // prow: A.tv row of lane's target (or -1)
+      if (prow >= 0) {
+        double* slot = ring + (size_t)(tl % kRing) * d * kTM;
+        for (int k = ew; k < d; k += kEW) cp_async8(slot + k * kTM + lane, A.tv.base + prow + (int64_t)k * A.tv.ld);
+      }
+      cp_async_commit();
+    };
+    // prologue: coordinates of tiles 0, 1 (visible after the barrier), 2 (in flight); the row of
+    // tile 3 is loaded ahead into a register
+    int64_t next_row = -1;
+    if (copier) {
+      issue_copy(0, row_of(0));
+      issue_copy(1, row_of(1));
+      cp_async_wait<0>();
+      issue_copy(2, row_of(2));
+      next_row = row_of(3);
     }
+    nbar_sync(kBarEval, kEW * 32);
+
+    constexpr int DR = (D > 0 && D <= 8) ? D : 1;  // coordinates held in registers per phase
+    double tc[DR];
+    auto load_coords = [&](int tl) {
+      if constexpr (D > 0 && D <= 8) {
+        const double* slot = ring + (size_t)(tl % kRing) * d * kTM;
+#pragma unroll
+        for (int k = 0; k < DR; ++k) tc[k] = slot[k * kTM + lane] * A.cscale;
+      }
+    };
+    auto coord = [&](int tl, int k) -> double {
+      if constexpr (D > 0 && D <= 8) return tc[k];
+      else return ring[(size_t)(tl % kRing) * d * kTM + k * kTM + lane] * A.cscale;
+    };
+    // A items: K_S columns of local tile tl into KS slot (tl & 1); two columns per pass
+    auto eval_A = [&](int tl) {
+      if (tl >= ntile || nA == 0 || (A.dbg & 1)) return;
+      load_coords(tl);
+      const bool valid = trow(tl) >= 0;
+      double* KS = KSb + (size_t)(tl & 1) * TS;
+      for (int q = 0; q < nA; q += 2) {
+        const int j0 = itA[q], j1 = itA[min(q + 1, nA - 1)];
+        double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < (D ? D : 1); ++k) {
+          for (int kk = k; kk < (D ? k + 1 : d); ++kk) {
+            const double t = coord(tl, kk);
+            const double a0 = t - s_srcS[kk * rS + j0], a1 = t - s_srcS[kk * rS + j1];
+            q0 = fma(a0, a0, q0);
+            q1 = fma(a1, a1, q1);
+          }
+        }
+        double k0 = exp_neg_fast(q0, s_tab), k1 = exp_neg_fast(q1, s_tab);
+        if (!valid) k0 = k1 = 0.0;
+        KS[j0 * kST + lane] = k0;
+        sk = fma(k0, k0, sk);
+        if (q + 1 < nA) {
+          KS[j1 * kST + lane] = k1;
+          sk = fma(k1, k1, sk);
+        }
+      }
+    };
+    eval_A(0);
+    nbar_sync(kBarEval, kEW * 32);
+
+    const int fr = lane >> 2, fk = lane & 3;  // DMMA fragment coordinates
     for (int it = 0; it < ntile; ++it) {
       const int s = it % kStages;
-      const int64_t t0 = (tile_lo + it) * kTM;
-      const bool valid = t0 + lane < A.tv.nt;
-      {  // prefetch the next tile's coordinates (latency overlaps the evaluation)
-        const int64_t i = t0 + kTM + lane;
-        const bool ok = it + 1 < ntile && i < A.tv.nt && !(A.dbg & 1);
-#pragma unroll
-        for (int k = 0; k < DR; ++k) tn[k] = (k < d && ok) ? tcoord(A.tv, i, k) : 0.0;
+      if (copier) {  // coordinates of tile it + 3 (slot of tile it - 1, released by the last EVAL barrier)
+        issue_copy(it + 3, next_row);
+        next_row = row_of(it + 4);
       }
       KID_TRACE(0);
       if (it >= kStages) nbar_sync(kBarEmpty + s, kGT);  // the MMA warps released stage s
       KID_TRACE(1);
-      double* KS = KSb + (size_t)s * TS;
-      double* KN = KNb + (size_t)s * TN;
-      if (!(A.dbg & 1)) {
-        // KID_EVAL_ILP independent exp chains per iteration (columns j + u*kEW)
-        constexpr int U = KID_EVAL_ILP;
-        for (int j = ew; j < m; j += U * kEW) {
-          double q[U];
+      eval_A(it + 1);
+      if (!(A.dbg & 1) && nB > 0) {
+        load_coords(it);
+        const bool valid = trow(it) >= 0;
+        const double* KS = KSb + (size_t)(it & 1) * TS;
+        double* KN = KNb + (size_t)s * TN;
+        for (int q = 0; q < nB; ++q) {
+          // B item: columns 8nb .. 8nb+7 -- K_N by exp (two passes of four independent chains) ...
+          const int j0 = 8 * itB[q];
 #pragma unroll
-          for (int u = 0; u < U; ++u) q[u] = 0.0;
+          for (int hh = 0; hh < 2; ++hh) {
+            const int jh = j0 + 4 * hh;
+            double kv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int k = 0; k < (D ? D : d); ++k) {
-            const double tk = D ? tc[D ? k : 0] : (valid ? tcoord(A.tv, t0 + lane, k) * A.cscale : 0.0);
+            for (int k = 0; k < (D ? D : 1); ++k) {
+              for (int kk = k; kk < (D ? k + 1 : d); ++kk) {
+                const double t = coord(it, kk);
+                const double2 s01 = *reinterpret_cast<const double2*>(&s_srcN[kk * mN + jh]);
+                const double2 s23 = *reinterpret_cast<const double2*>(&s_srcN[kk * mN + jh + 2]);
+                const double a0 = t - s01.x, a1 = t - s01.y, a2 = t - s23.x, a3 = t - s23.y;
+                kv[0] = fma(a0, a0, kv[0]);
+                kv[1] = fma(a1, a1, kv[1]);
+                kv[2] = fma(a2, a2, kv[2]);
+                kv[3] = fma(a3, a3, kv[3]);
+              }
+            }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const int ju = min(j + u * kEW, m - 1);
-              const double df = tk - s_src[ju + k * m];
-              q[u] = fma(df, df, q[u]);
+            for (int u = 0; u < 4; ++u) {
+              const double e = (A.dbg & 32) ? exp_neg_notab(kv[u]) : exp_neg_fast(kv[u], s_tab);
+              kv[u] = valid ? e : 0.0;
+              sk = fma(kv[u], kv[u], sk);
+              KN[(jh + u) * kST + lane] = kv[u];
             }
           }
+          // ... then D = K_N - K_S P2 on DMMA over the block's four 8-target row blocks:
+          // C(rb) = K_N fragment, C += K_S(rb, k-step) x (-P2)(k-step, block), back to KN
+          if (r > 0 && !(A.dbg & 2)) {
+            __syncwarp();
+            double c[4][2];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int ju = j + u * kEW;
-            double kv = exp_neg_fast(q[u], s_tab);
-            if (!valid) kv = 0.0;
-            if (ju < m) {
-              sk = fma(kv, kv, sk);
-              *((ju < r) ? &KS[ju * kST + lane] : &KN[(ju - r) * kST + lane]) = kv;
+            for (int rb = 0; rb < 4; ++rb) {
+              c[rb][0] = KN[(j0 + 2 * fk) * kST + rb * 8 + fr];
+              c[rb][1] = KN[(j0 + 2 * fk + 1) * kST + rb * 8 + fr];
+            }
+            const double* ks = KS + fk * kST + fr;
+            const double* pb = sP + fk * SPn + j0 + fr;
+            for (int k0 = 0; k0 < r4; k0 += 4) {
+              const double b = pb[k0 * SPn];
+#pragma unroll
+              for (int rb = 0; rb < 4; ++rb) dmma884(c[rb][0], c[rb][1], ks[k0 * kST + rb * 8], b);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int rb = 0; rb < 4; ++rb) {
+              KN[(j0 + 2 * fk) * kST + rb * 8 + fr] = c[rb][0];
+              KN[(j0 + 2 * fk + 1) * kST + rb * 8 + fr] = c[rb][1];
             }
           }
         }
       }
       KID_TRACE(2);
-      nbar_arrive(kBarFull + s, kGT);  // stage s holds tile it
-#pragma unroll
-      for (int k = 0; k < DR; ++k) tc[k] = tn[k] * A.cscale;
+      nbar_arrive(kBarFull + s, kGT);  // stage s holds D of tile it
+      if (copier) cp_async_wait<1>();  // coordinates of tile it + 2 landed (this thread's copies)
+      nbar_sync(kBarEval, kEW * 32);   // ... and K_S of tile it + 1 / those coordinates are visible
     }
+    if (copier) cp_async_wait<0>();
     if (part == 0) {
       sk = warp_sum(sk);
       if (lane == 0) red[ew] = sk;
     }
   } else {
     // ================================================================ MMA warps
-    if constexpr (D == 0 || D >= 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;\n" ::: "memory");
-    else asm volatile("setmaxnreg.inc.sync.aligned.u32 " KID_MMA_REGS ";\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kMmaRegs) : "memory");
     const int mw = warp - kMmaW0;
-    int2 tl[TPW];  // (a0, b0) block coordinates of WA x 2-block warp tiles, x = -1: empty slot
+    int2 tl[TPW];  // (a0, b0) block coordinates of WA x 2-block warp tiles; valid ones first
+    int ntl = 0;
 #pragma unroll
-    for (int q = 0; q < TPW; ++q) tl[q] = A.blist[((size_t)part * kMW + mw) * TPW + q];
+    for (int q = 0; q < TPW; ++q) {
+      tl[q] = A.blist[((size_t)part * kMW + mw) * TPW + q];
+      ntl += tl[q].x >= 0;
+    }
     double acc[TPW][WA][2][2];
 #pragma unroll
     for (int q = 0; q < TPW; ++q)
@@ -286,115 +429,27 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
       for (int u = 0; u < WA; ++u)
 #pragma unroll
         for (int v = 0; v < 2; ++v) acc[q][u][v][0] = acc[q][u][v][1] = 0.0;
-    const int NB = NBN;
     const int fr = (lane >> 2), fk = (lane & 3);  // fragment coordinates
+    int fa0[TPW], fb0[TPW];                       // fragment offsets of each tile's first row / column block
+#pragma unroll
+    for (int q = 0; q < TPW; ++q) {
+      fa0[q] = (tl[q].x >= 0 ? tl[q].x : 0) * 8 * kST;
+      fb0[q] = (tl[q].x >= 0 ? tl[q].y : 0) * 8 * kST;
+    }
     for (int it = 0; it < ntile; ++it) {
       const int s = it % kStages;
-#ifndef KID_TRACE_G1
       KID_TRACE(0);
-#endif
       nbar_sync(kBarFull + s, kGT);
       KID_TRACE(1);
-      const double* KS = KSb + (size_t)s * TS;
-      double* KN = KNb + (size_t)s * TN;
-      if (r > 0) {  // D = K_N - K_S P2, column-major in place
-        // static map: warp mw owns row blocks {2(mw&1), 2(mw&1)+1} and column blocks
-        // nb = (mw>>1) + 4t; three column blocks per round -> 2 A + 3 B fragment loads feed 6
-        // DMMAs per k-step (loads double-buffered); a slot past NBN computes into a dead
-        // accumulator (unpredicated: no warp-sync/branch around the DMMAs). The K_N operands of
-        // the subtraction are loaded before the k-loop so the write-back is a burst of stores.
-        const int rb0 = 2 * (mw & 1), nbo = mw >> 1;
-        for (int t0 = (A.dbg & 2) ? NBN : 0; 4 * t0 + nbo < NBN; t0 += 3) {
-          int nbv[3];
-          double c[3][2][2], kn[3][2][2];
-#pragma unroll
-          for (int u = 0; u < 3; ++u) {
-            nbv[u] = nbo + 4 * (t0 + u);
-            const int nbc = min(nbv[u], NBN - 1);
-#pragma unroll
-            for (int v = 0; v < 2; ++v) {
-              c[u][v][0] = c[u][v][1] = 0.0;
-              const double* p = &KN[(nbc * 8 + 2 * fk) * kST + (rb0 + v) * 8 + fr];
-              kn[u][v][0] = p[0];
-              kn[u][v][1] = p[kST];
-            }
-          }
-          double a[2][2], b[2][3];
-          auto load1 = [&](int buf, int k0) {
-#pragma unroll
-            for (int v = 0; v < 2; ++v) a[buf][v] = KS[(k0 + fk) * kST + (rb0 + v) * 8 + fr];
-#pragma unroll
-            for (int u = 0; u < 3; ++u) b[buf][u] = sP[(k0 + fk) * SP + min(nbv[u], NBN - 1) * 8 + fr];
-          };
-          auto mma1 = [&](int buf) {
-#pragma unroll
-            for (int u = 0; u < 3; ++u)
-#pragma unroll
-              for (int v = 0; v < 2; ++v) dmma884(c[u][v][0], c[u][v][1], a[buf][v], b[buf][u]);
-          };
-          load1(0, 0);
-#ifdef KID_TRACE_G1
-          KID_TRACE(0);
-#endif
-          for (int k0 = 0; k0 < r4; k0 += 8) {  // two k-steps per trip: static buffer indices
-            if (k0 + 4 < r4) load1(1, k0 + 4);
-            mma1(0);
-            if (k0 + 4 >= r4) break;
-            if (k0 + 8 < r4) load1(0, k0 + 8);
-            mma1(1);
-          }
-#ifdef KID_TRACE_G1
-          { double z = 0; for (int u = 0; u < 3; ++u) z += c[u][0][0] + c[u][1][1];
-            if (z == 12345.678) KN[0] = z; }
-          KID_TRACE(2);
-#endif
-#pragma unroll
-          for (int u = 0; u < 3; ++u) {
-            if (nbv[u] < NBN) {
-#pragma unroll
-              for (int v = 0; v < 2; ++v) {
-                double* p = &KN[(nbv[u] * 8 + 2 * fk) * kST + (rb0 + v) * 8 + fr];
-                p[0] = kn[u][v][0] - c[u][v][0];
-                p[kST] = kn[u][v][1] - c[u][v][1];
-              }
-            }
-          }
-        }
-#ifndef KID_TRACE_G1
-        KID_TRACE(2);
-#endif
-        nbar_sync(kBarMma, kMW * 32);
-      }
-      // G += D^T D over the 32 rows of the stage; fragments F(x) = D[k0 + fk][x*8 + fr],
-      // double-buffered so the loads of k-step k+1 overlap the DMMAs of k-step k
+      // unpredicated DMMAs: a per-DMMA predicate makes ptxas wrap every DMMA in a warp-sync and
+      // branch (tools/syrk_probe.cu); the tile count is instead dispatched once per stage
+      const double* col = KNb + (size_t)s * TN + fr * kST + fk;
       if (!(A.dbg & 4)) {
-        const double* col = KN + fr * kST + fk;
-        double fa[2][TPW][WA], fb[2][TPW][2];
-        auto load = [&](int buf, int k0) {
-#pragma unroll
-          for (int q = 0; q < TPW; ++q) {
-            const int a0 = tl[q].x >= 0 ? tl[q].x : 0, b0 = tl[q].x >= 0 ? tl[q].y : 0;
-#pragma unroll
-            for (int u = 0; u < WA; ++u) fa[buf][q][u] = col[(a0 + u) * 8 * kST + k0];
-#pragma unroll
-            for (int v = 0; v < 2; ++v) fb[buf][q][v] = col[(b0 + v) * 8 * kST + k0];
-          }
-        };
-        load(0, 0);
-#pragma unroll
-        for (int kk = 0; kk < kTM / 4; ++kk) {
-          if (kk + 1 < kTM / 4) load((kk + 1) & 1, (kk + 1) * 4);
-#pragma unroll
-          for (int q = 0; q < TPW; ++q) {
-            // unpredicated: a per-DMMA predicate makes ptxas wrap every DMMA in a warp-sync and
-            // branch, which costs more than the masked-out blocks (diagonal lower halves, padding,
-            // empty slots) compute; their accumulators are simply never stored
-            // (tools/syrk_probe.cu: masked 6.2 cycles/useful DMMA vs unpredicated 4.0/slot)
-#pragma unroll
-            for (int u = 0; u < WA; ++u)
-#pragma unroll
-              for (int v = 0; v < 2; ++v)
-                dmma884(acc[q][u][v][0], acc[q][u][v][1], fa[kk & 1][q][u], fb[kk & 1][q][v]);
+        if (ntl == TPW) syrk_stage<TPW, TPW, WA>(acc, fa0, fb0, col);
+        else if constexpr (TPW > 1) {
+          if (ntl == TPW - 1) syrk_stage<TPW - 1, TPW, WA>(acc, fa0, fb0, col);
+          else if constexpr (TPW > 2) {
+            if (ntl == TPW - 2) syrk_stage<TPW - 2, TPW, WA>(acc, fa0, fb0, col);
           }
         }
       }
@@ -410,7 +465,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const int a = tl[q].x + u, b = tl[q].y + v;
-          if (a < NB && b < NB && a <= b) {
+          if (a < NBN && b < NBN && a <= b) {
             const int row = a * 8 + fr, colx = b * 8 + 2 * fk;
             G[row + (size_t)colx * A.LG] = acc[q][u][v][0];
             G[row + (size_t)(colx + 1) * A.LG] = acc[q][u][v][1];
@@ -812,20 +867,60 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   if (WA == 2 && TPW < 3) TPW = 3;  // the instantiated 16x16 layouts (KID_LAYOUT_SWITCH)
   const int per_part = kMW * TPW;
   const int nparts = (nb + per_part - 1) / per_part;
+  // per part: floor/ceil share per warp, valid tiles first; the extra tiles go to the lowest
+  // warps, which sit on distinct SMSPs (warp % 4) for the first four -> SMSP-balanced DMMA work
   std::vector<int2> blist((size_t)nparts * per_part, make_int2(-1, -1));
   for (int p = 0; p < nparts; ++p) {
     const int lo = (int)((int64_t)nb * p / nparts), hi = (int)((int64_t)nb * (p + 1) / nparts);
-    const int cnt = hi - lo;
+    const int cnt = hi - lo, base_n = cnt / kMW, extra = cnt % kMW;
+    int g = lo;
     for (int w = 0; w < kMW; ++w) {
-      const int wlo = lo + cnt * w / kMW, whi = lo + cnt * (w + 1) / kMW;
-      for (int g = wlo; g < whi; ++g) blist[((size_t)p * kMW + w) * TPW + (g - wlo)] = tiles[g];
+      const int nw = base_n + (w < extra ? 1 : 0);
+      for (int q = 0; q < nw; ++q) blist[((size_t)p * kMW + w) * TPW + q] = tiles[g++];
     }
   }
-  const int r4 = ceil_to((int)r, 4);
-  const int TS = ceil_to(r4 > 0 ? r4 : 4, 2) * kST, TN = ceil_to(NBN + 1, 2) * 8 * kST;
-  const size_t smem = sizeof(double) * ((size_t)ceil_to(d * m, 2) + (size_t)kStages * (TS + TN) +
-                                        (size_t)r4 * frag_stride(meff));
-  if (smem > 200 * 1024 || NBN > 16 || getenv("KID_FORCE_LARGE")) return gram_dev_large(c, h, r, d_out);
+  // eval work lists: A items = the r skeleton columns, B items = the NBN 8-column blocks of the
+  // non-skeleton columns (exp + the K_S P2 DMMAs); longest-processing-time greedy over the eval
+  // warps (FP64-pipe weights: a DMMA counts 8 warp DFMAs), ties broken by the load of the warp's
+  // SMSP (warp % 4)
+  std::vector<short> elist((size_t)kEW * kEItems, 0);
+  {
+    const int nBg = NBN;
+    const double wA = 3.0 * d + 12.0, wB = 8.0 * (3.0 * d + 12.0) + 8.0 * (double)ceil_to((int)r, 4);
+    std::vector<std::pair<double, int>> items;  // (weight, code): code >= 0 B group, < 0 A column -code-1
+    for (int g = 0; g < nBg; ++g) items.push_back({wB, g});
+    for (int j = 0; j < (int)r; ++j) items.push_back({wA, -j - 1});
+    std::stable_sort(items.begin(), items.end(), [](auto& x, auto& y) { return x.first > y.first; });
+    std::vector<double> wl(kEW, 0.0), sl(4, 0.0);
+    std::vector<std::vector<short>> la(kEW), lb(kEW);
+    for (auto& itx : items) {
+      int best = 0;
+      for (int w = 1; w < kEW; ++w) {
+        const double key = wl[w] + 1e-3 * sl[(kEvalW0 + w) % 4], kb = wl[best] + 1e-3 * sl[(kEvalW0 + best) % 4];
+        if (key < kb) best = w;
+      }
+      wl[best] += itx.first;
+      sl[(kEvalW0 + best) % 4] += itx.first;
+      if (itx.second >= 0) lb[best].push_back((short)itx.second);
+      else la[best].push_back((short)(-itx.second - 1));
+    }
+    for (int w = 0; w < kEW; ++w) {
+      if (2 + la[w].size() + lb[w].size() > (size_t)kEItems) return gram_dev_large(c, h, r, d_out);
+      std::sort(la[w].begin(), la[w].end());
+      std::sort(lb[w].begin(), lb[w].end());
+      short* e = &elist[(size_t)w * kEItems];
+      e[0] = (short)la[w].size();
+      e[1] = (short)lb[w].size();
+      std::copy(la[w].begin(), la[w].end(), e + 2);
+      std::copy(lb[w].begin(), lb[w].end(), e + 2 + la[w].size());
+    }
+  }
+  const int rr = (int)r, r4 = ceil_to(rr, 4);
+  const int rS = ceil_to(rr > 0 ? rr : 1, 2), mN = NBN * 8;
+  const int TS = (r4 > 0 ? r4 : 4) * kST, TN = ceil_to(NBN + 1, 2) * 8 * kST;
+  const size_t smem = sizeof(double) * ((size_t)d * rS + (size_t)d * mN + (size_t)r4 * frag_stride(meff) +
+                                        2 * (size_t)TS + (size_t)kStages * TN + (size_t)kRing * d * kTM);
+  if (smem > 190 * 1024 || NBN > 16 || getenv("KID_FORCE_LARGE")) return gram_dev_large(c, h, r, d_out);
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   int per_sm = 1;
@@ -841,15 +936,21 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   }
   int nchunks = std::max(1, c->sms * per_sm / nparts);
   nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, ntiles));
-  // scratch: blist | partial | partial_sk
-  const size_t bl_bytes = sizeof(int2) * blist.size();
+  // scratch: blist | elist | partial | partial_sk
+  const size_t bl_bytes = sizeof(int2) * blist.size() + sizeof(short) * elist.size();
   const size_t part_bytes = sizeof(double) * (size_t)nchunks * LG * LG;
   char* base = (char*)scratch(c, bl_bytes + 256 + part_bytes + sizeof(double) * (nchunks + 8));
   if (!base) return KID_E_OOM;
   int2* d_blist = (int2*)base;
   double* partial = (double*)(base + ((bl_bytes + 255) / 256) * 256);
   double* partial_sk = partial + (size_t)nchunks * LG * LG;
-  KID_CK(c, cudaMemcpyAsync(d_blist, blist.data(), bl_bytes, cudaMemcpyHostToDevice, c->stream));
+  short* d_elist = (short*)(d_blist + blist.size());
+  {  // pageable source: the runtime stages it before returning, so the local vector may go
+    std::vector<char> hb(bl_bytes);
+    std::memcpy(hb.data(), blist.data(), sizeof(int2) * blist.size());
+    std::memcpy(hb.data() + sizeof(int2) * blist.size(), elist.data(), sizeof(short) * elist.size());
+    KID_CK(c, cudaMemcpyAsync(d_blist, hb.data(), bl_bytes, cudaMemcpyHostToDevice, c->stream));
+  }
   GramArgs A;
   A.tv = view(c);
   A.d = d;
@@ -857,10 +958,10 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   A.m = m;
   A.r = (int)r;
   A.meff = meff;
-  A.negc = -1.0 / (2.0 * h * h);
   A.cscale = std::sqrt(1.0 / (2.0 * h * h));
   A.P2 = r > 0 ? c->P2 : nullptr;
   A.blist = d_blist;
+  A.elist = d_elist;
   A.nparts = nparts;
   A.ntiles = ntiles;
   A.nchunks = nchunks;
@@ -893,39 +994,28 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     KID_CK(c, cudaMemcpyAsync(tr.data(), A.trace, sizeof(long long) * trace_n, cudaMemcpyDeviceToHost, c->stream));
     KID_CK(c, cudaStreamSynchronize(c->stream));
     cudaFree(A.trace);
-    // per-phase mean cycles over tiles 4..kTraceTiles-1 (steady state), MMA warp kEW and eval warp 0
-    auto at_raw = [&](int w, int it, int ev) { return tr[((size_t)w * kTraceTiles + it) * 4 + ev]; };
-    auto at = [&](int w, int it, int ev) { return at_raw(w == 0 ? kMmaW0 : (w == kMW ? kEvalW0 : w), it, ev); };
-    double mw_full = 0, mw_g1 = 0, mw_syrk = 0, ew_empty = 0, ew_eval = 0, tile = 0;
+    // per-phase mean cycles over tiles 4..kTraceTiles-1 (steady state): MMA warp 0, eval warp 0
+    auto at = [&](int w, int it, int ev) { return tr[((size_t)w * kTraceTiles + it) * 4 + ev]; };
+    double mw_full = 0, mw_syrk = 0, ew_empty = 0, ew_eval = 0, tile = 0;
     int n = 0;
     for (int it = 4; it + 1 < kTraceTiles; ++it) {
-      if (!at(0, it + 1, 0)) break;
-      mw_full += at(0, it, 1) - at(0, it, 0);
-      mw_g1 += at(0, it, 2) - at(0, it, 1);
-      mw_syrk += at(0, it, 3) - at(0, it, 2);
-      ew_empty += at(kMW, it, 1) - at(kMW, it, 0);
-      ew_eval += at(kMW, it, 2) - at(kMW, it, 1);
-      tile += at(0, it + 1, 0) - at(0, it, 0);
+      if (!at(kMmaW0, it + 1, 0)) break;
+      mw_full += at(kMmaW0, it, 1) - at(kMmaW0, it, 0);
+      mw_syrk += at(kMmaW0, it, 3) - at(kMmaW0, it, 1);
+      ew_empty += at(kEvalW0, it, 1) - at(kEvalW0, it, 0);
+      ew_eval += at(kEvalW0, it, 2) - at(kEvalW0, it, 1);
+      tile += at(kMmaW0, it + 1, 0) - at(kMmaW0, it, 0);
       ++n;
     }
-    for (int it = 10; it < 11; ++it) {
-      fprintf(stderr, "[kid trace] tile %d gemm1 cycles per MMA warp:", it);
-      for (int w = kMmaW0; w < kMmaW0 + kMW; ++w) fprintf(stderr, " %lld", at_raw(w, it, 2) - at_raw(w, it, 1));
-      fprintf(stderr, " | syrk+bar:");
-      for (int w = kMmaW0; w < kMmaW0 + kMW; ++w) fprintf(stderr, " %lld", at_raw(w, it, 3) - at_raw(w, it, 2));
-      fprintf(stderr, "\n");
-    }
-    for (int it = 10; it < 10; ++it) {
-      fprintf(stderr, "[kid trace] tile %d, stamps rel. to MMA warp 0 event 0:", it);
-      for (int w = 0; w < kMW + kEW; ++w)
-        fprintf(stderr, " w%d[%lld %lld %lld %lld]", w, at(w, it, 0) - at(0, it, 0), at(w, it, 1) - at(0, it, 0),
-                at(w, it, 2) - at(0, it, 0), at(w, it, 3) - at(0, it, 0));
-      fprintf(stderr, "\n");
-    }
+    fprintf(stderr, "[kid trace] tile 10 eval cycles per eval warp:");
+    for (int w = kEvalW0; w < kEvalW0 + kEW; ++w) fprintf(stderr, " %lld", at(w, 10, 2) - at(w, 10, 1));
+    fprintf(stderr, " | syrk per MMA warp:");
+    for (int w = kMmaW0; w < kMmaW0 + kMW; ++w) fprintf(stderr, " %lld", at(w, 10, 3) - at(w, 10, 1));
+    fprintf(stderr, "\n");
     if (n)
-      fprintf(stderr, "[kid trace] cycles/tile: tile %.0f | mma: wait_full %.0f gemm1 %.0f bar+syrk %.0f | "
+      fprintf(stderr, "[kid trace] cycles/tile: tile %.0f | mma: wait_full %.0f syrk %.0f | "
                       "eval: wait_empty %.0f eval %.0f (n=%d)\n",
-              tile / n, mw_full / n, mw_g1 / n, mw_syrk / n, ew_empty / n, ew_eval / n, n);
+              tile / n, mw_full / n, mw_syrk / n, ew_empty / n, ew_eval / n, n);
   }
   k_gram_reduce<<<std::max(1, std::min(c->sms * 2, (meff * meff + 31) / 32)), 1024, 0, c->stream>>>(
       partial, nchunks, LG, meff, partial_sk, d_out);
