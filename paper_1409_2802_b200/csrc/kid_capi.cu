@@ -269,6 +269,7 @@ int kid_set_block(kid_ctx* c, const double* targets, int64_t nt, const double* s
   if (ensure(c, (void**)&c->src, &c->src_cap, sizeof(double) * m * d)) return KID_E_OOM;
   if (nt) KID_CK(c, cudaMemcpyAsync(c->blk_tgt, targets, sizeof(double) * nt * d, cudaMemcpyHostToDevice, c->stream));
   KID_CK(c, cudaMemcpyAsync(c->src, sources, sizeof(double) * m * d, cudaMemcpyHostToDevice, c->stream));
+  c->src_host.assign(sources, sources + (size_t)m * d);
   c->tbase = c->blk_tgt;
   c->tld = nt;
   c->tidx = nullptr;
@@ -373,6 +374,7 @@ int kid_recon_prepare(kid_ctx* c, const int64_t* skel, int64_t r, const double* 
     }
   if (ensure(c, (void**)&c->src_perm, &c->src_perm_cap, sizeof(double) * m * d)) return KID_E_OOM;
   KID_CK(c, cudaMemcpyAsync(c->src_perm, perm_h.data(), sizeof(double) * m * d, cudaMemcpyHostToDevice, c->stream));
+  c->src_perm_host = perm_h;
   // P2 = P[:, non-skel], row-major r x SP (SP = frag_stride(meff), matches k_gram)
   const int64_t SP = ((meff + 7) / 8) * 8 + 4;
   std::vector<double> p2((size_t)std::max<int64_t>(r, 1) * SP, 0.0);

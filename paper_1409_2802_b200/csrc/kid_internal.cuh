@@ -41,56 +41,86 @@ __device__ __forceinline__ double gauss_exact(double sq, double denom) {
   return exp(__ddiv_rn(-sq, denom));
 }
 
-// exp(-q), q >= 0, for the Gaussian entries of the FP64 passes: table-driven and branch-free
-// (tab[j] = 2^(j/1024), correctly rounded, staged in shared memory from c_exp2_tab):
-//   -q = (1024k + j) ln2/1024 + r,  |r| <= ln2/2048,  e^r - 1 by a degree-4 Taylor polynomial
-//   (truncation r^5/120 < 4e-20), exp(-q) = 2^k (T[j] + T[j] (e^r - 1)); the 2^k is applied as
+// exp(-q), q >= 0, for the Gaussian entries of the FP64 passes: table-driven and branch-free.
+//   -q = (64k + j) ln2/64 + r,  |r| <= ln2/128,  e^r - 1 by a degree-5 Taylor polynomial
+//   (truncation r^6/720 < 4e-17), exp(-q) = 2^k (T[j] + T[j] (e^r - 1)); the 2^k is applied as
 //   2^(k+600) on the exponent field and one multiply by 2^-600 (exact for normal results,
 //   correctly rounded into the subnormal range; k is clamped where the result rounds to 0).
-// 11 FP64-pipe ops against ~20 for libdevice exp() plus the caller's divide; max error 1 ulp
-// against glibc (tests/test_gpu_parity.py::test_fast_exp_accuracy). q >= 0 of any size: q is
-// clamped to <= 2^17 on its high word (one integer min; exp(-2^17) == 0 in double anyway), which
-// keeps the rounded multiple of ln2/1024 inside int32.
-constexpr int kExpTab = 1024;
-__device__ __forceinline__ double exp_neg_fast(double q, const double* __restrict__ tab) {
+// T[j] = 2^(j/64) (correctly rounded, c_exp2_tab) is staged in shared memory REPLICATED per lane,
+// [j][lane] (kExpTab x 32 doubles = 16 KB): a lane reads tabl[j * 32] with tabl = tab + lane, so
+// the 32 random lookups of a warp never share a bank pair (2 wavefronts, the minimum for a
+// 64-bit load; an unreplicated table costs ~5 for random indices) -- shared-memory bandwidth,
+// not the FP64 pipe, bounds the fused pass (profiles/).
+// 12 FP64-pipe ops; max error 1 ulp against glibc (tests/test_gpu_parity.py::test_fast_exp_accuracy).
+// q >= 0 of any size: q is clamped to <= 2^17 on its high word (one integer min; exp(-2^17) == 0
+// in double anyway), which keeps the rounded multiple of ln2/64 inside int32.
+constexpr int kExpTab = 64;
+constexpr int kExpRep = 32;  // replicas (one per lane)
+constexpr int kExpTabWords = kExpTab * kExpRep;
+__device__ __forceinline__ double exp_neg_fast(double q, const double* __restrict__ tabl) {
   const double shifter = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest-integer
   q = __hiloint2double(min(__double2hiint(q), 0x41000000), __double2loint(q));  // q <= ~2^17
-  double kd = fma(q, -1477.3197218702985, shifter);  // round(-q * 1024 / ln2)
+  double kd = fma(q, -92.33248261689366, shifter);  // round(-q * 64 / ln2)
   const int n = __double2loint(kd);
+  const double t = tabl[(n & (kExpTab - 1)) * kExpRep];
   kd -= shifter;
-  double r = fma(kd, -0.0006769015433292225, -q);
-  r = fma(kd, -1.8634911418658083e-13, r);
-  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
+  double r = fma(kd, -0.010830424667801708, -q);  // Cody-Waite: ln2/64 = hi (28 bits) + lo
+  r = fma(kd, -2.8447437476627285e-11, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p *= r;  // e^r - 1
-  const double t = tab[n & (kExpTab - 1)];
   const double y = fma(t, p, t);
-  const int k = max(n >> 10, -1100);  // floor(n / 1024), clamped: 2^(k+600) stays normal
+  const int k = max(n >> 6, -1100);  // floor(n / 64), clamped: 2^(k+600) stays normal
   return __hiloint2double(__double2hiint(y) + ((k + 600) << 20), __double2loint(y)) * 0x1p-600;
 }
 
-// profiling aid only (KID_GRAM_DEBUG 32): exp_neg_fast with the table entry replaced by 1
-__device__ __forceinline__ double exp_neg_notab(double q) {
+// exp_neg_fast on N independent arguments, written step-major (each step of the evaluation is
+// applied to all N before the next) so the N dependency chains stay interleaved in the SASS --
+// ptxas otherwise tends to serialise them under a tight register budget. Same arithmetic, same
+// results as N calls of exp_neg_fast.
+template <int N>
+__device__ __forceinline__ void exp_neg_fast_n(double (&q)[N], const double* __restrict__ tabl) {
   const double shifter = 6755399441055744.0;
-  double kd = fma(q, -1477.3197218702985, shifter);
-  const int n = __double2loint(kd);
-  kd -= shifter;
-  double r = fma(kd, -0.0006769015433292225, -q);
-  r = fma(kd, -1.8634911418658083e-13, r);
-  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p *= r;
-  const double t = 1.0 + (n & 1023) * 1e-300;
-  const double y = fma(t, p, t);
-  const int k = max(n >> 10, -1100);
-  return __hiloint2double(__double2hiint(y) + ((k + 600) << 20), __double2loint(y)) * 0x1p-600;
+  double kd[N], r[N], p[N], t[N];
+  int n[N];
+#pragma unroll
+  for (int u = 0; u < N; ++u) q[u] = __hiloint2double(min(__double2hiint(q[u]), 0x41000000), __double2loint(q[u]));
+#pragma unroll
+  for (int u = 0; u < N; ++u) kd[u] = fma(q[u], -92.33248261689366, shifter);
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    n[u] = __double2loint(kd[u]);
+    t[u] = tabl[(n[u] & (kExpTab - 1)) * kExpRep];
+  }
+#pragma unroll
+  for (int u = 0; u < N; ++u) kd[u] -= shifter;
+#pragma unroll
+  for (int u = 0; u < N; ++u) r[u] = fma(kd[u], -0.010830424667801708, -q[u]);
+#pragma unroll
+  for (int u = 0; u < N; ++u) r[u] = fma(kd[u], -2.8447437476627285e-11, r[u]);
+#pragma unroll
+  for (int u = 0; u < N; ++u) p[u] = fma(r[u], 1.0 / 120.0, 1.0 / 24.0);
+#pragma unroll
+  for (int u = 0; u < N; ++u) p[u] = fma(p[u], r[u], 1.0 / 6.0);
+#pragma unroll
+  for (int u = 0; u < N; ++u) p[u] = fma(p[u], r[u], 0.5);
+#pragma unroll
+  for (int u = 0; u < N; ++u) p[u] = fma(p[u], r[u], 1.0);
+#pragma unroll
+  for (int u = 0; u < N; ++u) p[u] *= r[u];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const double y = fma(t[u], p[u], t[u]);
+    const int k = max(n[u] >> 6, -1100);
+    q[u] = __hiloint2double(__double2hiint(y) + ((k + 600) << 20), __double2loint(y)) * 0x1p-600;
+  }
 }
 
 // exp(x), x <= 0 (diagnostics and callers holding the argument)
-__device__ __forceinline__ double exp_fast(double x, const double* __restrict__ tab) {
-  return exp_neg_fast(-x, tab);
+__device__ __forceinline__ double exp_fast(double x, const double* __restrict__ tabl) {
+  return exp_neg_fast(-x, tabl);
 }
 
 // FP64 tensor-core MMA (SASS DMMA.8x8x4): C[8x8] += A[8x4] * B[4x8].
@@ -149,6 +179,8 @@ struct kid_ctx {
   int64_t r = 0;
   double* src_perm = nullptr;  // m x d, columns [skel | non-skel]
   size_t src_perm_cap = 0;
+  std::vector<double> src_host;       // host copies (m x d col-major) of src / src_perm: the fused
+  std::vector<double> src_perm_host;  // pass carries them in its kernel parameters
   double* P2 = nullptr;        // r x meff row-major, stride = r-major padded
   size_t P2_cap = 0;
   std::vector<int64_t> nonskel;  // host: original column of each non-skeleton column

@@ -26,7 +26,12 @@
 
 namespace kid {
 
-__device__ double c_exp2_tab[kExpTab];  // global (L2-resident); each CTA stages it in shared memory
+__device__ double c_exp2_tab[kExpTab];  // 2^(j/64); each CTA stages it in shared memory, replicated per lane
+
+// shared table [j][lane] (kExpTabWords doubles) for exp_neg_fast(q, tab + lane)
+__device__ __forceinline__ void stage_exp_table(double* tabr, int tid, int nthr) {
+  for (int e = tid; e < kExpTabWords; e += nthr) tabr[e] = c_exp2_tab[e / kExpRep];
+}
 
 int init_device_tables() {
   static thread_local int done_dev = -1;
@@ -69,8 +74,8 @@ __global__ void __launch_bounds__(256) k_row_norms(TargetView tv, int d_rt, cons
                                                    int64_t m, double negc, double* __restrict__ w) {
   const int d = D ? D : d_rt;
   extern __shared__ double s_src[];  // d x m, s_src[j + k*m]
-  __shared__ double s_tab[kExpTab];
-  for (int e = threadIdx.x; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
+  __shared__ double s_tab[kExpTabWords];
+  stage_exp_table(s_tab, threadIdx.x, blockDim.x);
   for (int64_t e = threadIdx.x; e < m * d; e += blockDim.x) s_src[e] = src[e];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tv.nt; i += (int64_t)gridDim.x * blockDim.x) {
@@ -94,7 +99,7 @@ __global__ void __launch_bounds__(256) k_row_norms(TargetView tv, int d_rt, cons
           sq = __dadd_rn(sq, __dmul_rn(diff, diff));
         }
       }
-      const double kv = exp_fast(sq * negc, s_tab);
+      const double kv = exp_fast(sq * negc, s_tab + (threadIdx.x & 31));
       acc = __dadd_rn(acc, __dmul_rn(kv, kv));  // sequential over j (sampling.hpp:193)
     }
     w[i] = __dsqrt_rn(acc);
@@ -102,6 +107,7 @@ __global__ void __launch_bounds__(256) k_row_norms(TargetView tv, int d_rt, cons
 }
 
 // ------------------------------------------------------------------ Gram / residual Gram
+constexpr int kCSrc = 2048;  // doubles of source coordinates carried in GramArgs (16 KB)
 struct GramArgs {
   TargetView tv;
   int d;
@@ -118,8 +124,12 @@ struct GramArgs {
   int LG;              // padded Gram leading dimension = ceil8(meff)
   double* partial_sk;  // [nchunks] (written by part 0)
   int dbg;             // profiling aid (KID_GRAM_DEBUG): 1 skip eval math, 2 skip the K_S P2 FMAs, 4 skip SYRK,
-                       // 16 no coordinate copies (ring slots keep tile 0's targets), 32 exp without the table load
+                       // 16 no coordinate copies (ring slots keep tile 0's targets)
   long long* trace;    // profiling aid (KID_GRAM_TRACE): [warp][tile][4] clock64 stamps of CTA 0
+  // scaled source coordinates in the kernel-parameter (constant) bank: the eval warps read them
+  // at warp-uniform indices, so they cost constant-cache broadcasts instead of shared-memory
+  // wavefronts. [d][rS] skeleton columns, then [d][mN] non-skeleton columns (padding: far away)
+  double csrc[kCSrc];
 };
 constexpr int kTraceTiles = 64;
 
@@ -140,8 +150,8 @@ constexpr int kTraceTiles = 64;
 // DMMA and DFMA share the FP64 datapath (tools/fp64_overlap.cu): the split keeps it fed from
 // both sides -- the MMA warps never wait on a GEMM phase, the eval warps fill the DMMA gaps.
 constexpr int kMW = 8, kEW = 12, kGT = (kMW + kEW) * 32;  // 640 threads
-constexpr int kEvalW0 = 0, kMmaW0 = kEW;
-constexpr int kStages = 3;
+constexpr int kEvalW0 = kMW, kMmaW0 = 0;
+constexpr int kStages = 4;
 constexpr int kST = kTM + 4;  // column-major tile stride
 constexpr int kRing = 4;      // target-coordinate ring slots
 constexpr int kEItems = 48;   // per eval warp: 2 counts + items
@@ -204,39 +214,29 @@ __device__ __forceinline__ void syrk_stage(double (&acc)[TPW][WA][2][2], const i
 }
 
 template <int D, int TPW, int WA>
-__global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
+__global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArgs A) {
   const int d = D ? D : A.d;
   const int m = A.m, r = A.r, meff = A.meff;
   const int NBN = ceil_to(meff, 8) / 8;
   const int r4 = ceil_to(r, 4);
-  const int rS = ceil_to(r > 0 ? r : 1, 2), mN = NBN * 8;
+  const int rS = r4, mN = NBN * 8;
   const int SPn = frag_stride(meff);  // -P2 row stride (= 4 or 12 mod 16: conflict-free B fragments)
   const int TS = (r4 > 0 ? r4 : 4) * kST, TN = ceil_to(NBN + 1, 2) * 8 * kST;  // one KS slot / one KN stage
   extern __shared__ __align__(16) double smem[];
-  double* s_srcS = smem;                         // d x rS: skeleton sources, [k][j]
-  double* s_srcN = s_srcS + (size_t)d * rS;      // d x mN: non-skeleton sources, [k][j]; pad: far away
-  double* sP = s_srcN + (size_t)d * mN;          // r4 x SPn: -P2, row-major (pad rows / columns 0)
+  const double* s_srcS = A.csrc;                   // d x rS: skeleton sources, [k][j] (constant bank); pad: far away
+  const double* s_srcN = A.csrc + (size_t)d * rS;  // d x mN: non-skeleton sources, [k][j]; pad: far away
+  double* sP = smem;                             // r4 x SPn: -P2, row-major (pad rows / columns 0)
   double* KSb = sP + (size_t)r4 * SPn;           // 2 x (r4 x kST): K_S, column-major [k][t]; rows >= r are 0
   double* KNb = KSb + 2 * (size_t)TS;            // kStages x (.. x kST): D, column-major [col][t]
   double* ring = KNb + (size_t)kStages * TN;     // kRing x d x 32 target coordinates (unscaled)
   __shared__ double red[kEW];
-  __shared__ double s_tab[kExpTab];
+  __shared__ double s_tab[kExpTabWords];
   __shared__ short s_el[kEW * kEItems];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = blockIdx.x, part = blockIdx.y;
-  for (int e = tid; e < kExpTab; e += kGT) s_tab[e] = c_exp2_tab[e];
+  stage_exp_table(s_tab, tid, kGT);
   for (int e = tid; e < kEW * kEItems; e += kGT) s_el[e] = A.elist[e];
-  for (int e = tid; e < d * rS; e += kGT) {
-    const int k = e / rS, j = e % rS;
-    s_srcS[e] = A.src[(size_t)k * m + min(j, max(r - 1, 0))] * A.cscale;
-  }
-  // padding sources sit far away: their K entries are exactly 0 (exp_neg_fast clamps q), so the
-  // padding columns of D are 0 and add nothing to sum K^2
-  for (int e = tid; e < d * mN; e += kGT) {
-    const int k = e / mN, j = e % mN;
-    s_srcN[e] = j < meff ? A.src[(size_t)k * m + r + j] * A.cscale : 1.0e4;
-  }
   const int SP = frag_stride(meff);
   for (int e = tid; e < r4 * SPn; e += kGT) {
     const int k = e / SPn, n = e % SPn;
@@ -306,25 +306,27 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
       load_coords(tl);
       const bool valid = trow(tl) >= 0;
       double* KS = KSb + (size_t)(tl & 1) * TS;
-      for (int q = 0; q < nA; q += 2) {
-        const int j0 = itA[q], j1 = itA[min(q + 1, nA - 1)];
-        double q0 = 0.0, q1 = 0.0;
+      for (int q = 0; q < nA; ++q) {  // A item: skeleton columns 4g .. 4g+3 (padding columns: K == 0)
+        const int j0 = 4 * itA[q];
+        double kv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int k = 0; k < (D ? D : 1); ++k) {
           for (int kk = k; kk < (D ? k + 1 : d); ++kk) {
             const double t = coord(tl, kk);
-            const double a0 = t - s_srcS[kk * rS + j0], a1 = t - s_srcS[kk * rS + j1];
-            q0 = fma(a0, a0, q0);
-            q1 = fma(a1, a1, q1);
+            const double* ss = s_srcS + kk * rS + j0;
+            const double a0 = t - ss[0], a1 = t - ss[1], a2 = t - ss[2], a3 = t - ss[3];
+            kv[0] = fma(a0, a0, kv[0]);
+            kv[1] = fma(a1, a1, kv[1]);
+            kv[2] = fma(a2, a2, kv[2]);
+            kv[3] = fma(a3, a3, kv[3]);
           }
         }
-        double k0 = exp_neg_fast(q0, s_tab), k1 = exp_neg_fast(q1, s_tab);
-        if (!valid) k0 = k1 = 0.0;
-        KS[j0 * kST + lane] = k0;
-        sk = fma(k0, k0, sk);
-        if (q + 1 < nA) {
-          KS[j1 * kST + lane] = k1;
-          sk = fma(k1, k1, sk);
+        exp_neg_fast_n<4>(kv, s_tab + lane);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          kv[u] = valid ? kv[u] : 0.0;
+          sk = fma(kv[u], kv[u], sk);
+          KS[(j0 + u) * kST + lane] = kv[u];
         }
       }
     };
@@ -358,19 +360,18 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
             for (int k = 0; k < (D ? D : 1); ++k) {
               for (int kk = k; kk < (D ? k + 1 : d); ++kk) {
                 const double t = coord(it, kk);
-                const double2 s01 = *reinterpret_cast<const double2*>(&s_srcN[kk * mN + jh]);
-                const double2 s23 = *reinterpret_cast<const double2*>(&s_srcN[kk * mN + jh + 2]);
-                const double a0 = t - s01.x, a1 = t - s01.y, a2 = t - s23.x, a3 = t - s23.y;
+                const double* sn = s_srcN + kk * mN + jh;
+                const double a0 = t - sn[0], a1 = t - sn[1], a2 = t - sn[2], a3 = t - sn[3];
                 kv[0] = fma(a0, a0, kv[0]);
                 kv[1] = fma(a1, a1, kv[1]);
                 kv[2] = fma(a2, a2, kv[2]);
                 kv[3] = fma(a3, a3, kv[3]);
               }
             }
+            exp_neg_fast_n<4>(kv, s_tab + lane);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const double e = (A.dbg & 32) ? exp_neg_notab(kv[u]) : exp_neg_fast(kv[u], s_tab);
-              kv[u] = valid ? e : 0.0;
+              kv[u] = valid ? kv[u] : 0.0;
               sk = fma(kv[u], kv[u], sk);
               KN[(jh + u) * kST + lane] = kv[u];
             }
@@ -405,6 +406,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(GramArgs A) {
       nbar_arrive(kBarFull + s, kGT);  // stage s holds D of tile it
       if (copier) cp_async_wait<1>();  // coordinates of tile it + 2 landed (this thread's copies)
       nbar_sync(kBarEval, kEW * 32);   // ... and K_S of tile it + 1 / those coordinates are visible
+      KID_TRACE(3);
     }
     if (copier) cp_async_wait<0>();
     if (part == 0) {
@@ -553,8 +555,8 @@ __global__ void __launch_bounds__(kNT) k_leverage(LevArgs A) {
   double* rowpart = KN + (size_t)kTM * SN;  // kTM x NBR
   double* sW = rowpart + (size_t)kTM * NBR; // m4 x SW (row-major) when w_in_smem
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ double s_tab[kExpTab];
-  for (int e = tid; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
+  __shared__ double s_tab[kExpTabWords];
+  stage_exp_table(s_tab, tid, blockDim.x);
   const int t_init = tid / m, j_init = tid - (tid / m) * m;
   const int step_t = kNT / m, step_j = kNT - (kNT / m) * m;
   for (int e = tid; e < m * d; e += kNT) s_src[e] = A.src[e];
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(kNT) k_leverage(LevArgs A) {
           const double diff = __dsub_rn(s_t[t + k * kTM], s_src[j + k * m]);
           sq = __dadd_rn(sq, __dmul_rn(diff, diff));
         }
-        kv = exp_fast(sq * A.negc, s_tab);
+        kv = exp_fast(sq * A.negc, s_tab + (threadIdx.x & 31));
       }
       KN[t * SN + j] = kv;
       j += step_j;
@@ -643,11 +645,11 @@ __global__ void k_eval_rows(TargetView tv, int d, const double* __restrict__ src
 }
 
 __global__ void k_exp_check(const double* __restrict__ x, int64_t n, double* __restrict__ y) {
-  __shared__ double s_tab[kExpTab];
-  for (int e = threadIdx.x; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
+  __shared__ double s_tab[kExpTabWords];
+  stage_exp_table(s_tab, threadIdx.x, blockDim.x);
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = exp_fast(x[i], s_tab);
+    y[i] = exp_fast(x[i], s_tab + (threadIdx.x & 31));
 }
 
 TargetView view(const kid_ctx* c) { return TargetView{c->tbase, c->tld, c->tidx, c->nt}; }
@@ -723,9 +725,9 @@ int row_norms_dev(kid_ctx* c, double h, double* d_w) {
 __global__ void __launch_bounds__(256) k_eval_batch(TargetView tv, int d, const double* __restrict__ src, int m,
                                                     double cscale, int64_t t0, int B, double* __restrict__ Kb,
                                                     double* __restrict__ sk_part) {
-  __shared__ double s_tab[kExpTab];
+  __shared__ double s_tab[kExpTabWords];
   __shared__ double red[8];
-  for (int e = threadIdx.x; e < kExpTab; e += blockDim.x) s_tab[e] = c_exp2_tab[e];
+  stage_exp_table(s_tab, threadIdx.x, blockDim.x);
   __syncthreads();
   double sk = 0.0;
   const int64_t total = (int64_t)B * m;
@@ -738,7 +740,7 @@ __global__ void __launch_bounds__(256) k_eval_batch(TargetView tv, int d, const 
         const double df = tcoord(tv, t0 + i, k) * cscale - src[j + (int64_t)k * m] * cscale;
         q = fma(df, df, q);
       }
-      kv = exp_neg_fast(q, s_tab);
+      kv = exp_neg_fast(q, s_tab + (threadIdx.x & 31));
     }
     Kb[e] = kv;
     sk = fma(kv, kv, sk);
@@ -879,17 +881,17 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
       for (int q = 0; q < nw; ++q) blist[((size_t)p * kMW + w) * TPW + q] = tiles[g++];
     }
   }
-  // eval work lists: A items = the r skeleton columns, B items = the NBN 8-column blocks of the
+  // eval work lists: A items = groups of four skeleton columns (r4 / 4), B items = the NBN 8-column blocks of the
   // non-skeleton columns (exp + the K_S P2 DMMAs); longest-processing-time greedy over the eval
   // warps (FP64-pipe weights: a DMMA counts 8 warp DFMAs), ties broken by the load of the warp's
   // SMSP (warp % 4)
   std::vector<short> elist((size_t)kEW * kEItems, 0);
   {
     const int nBg = NBN;
-    const double wA = 3.0 * d + 12.0, wB = 8.0 * (3.0 * d + 12.0) + 8.0 * (double)ceil_to((int)r, 4);
-    std::vector<std::pair<double, int>> items;  // (weight, code): code >= 0 B group, < 0 A column -code-1
+    const double wA = 4.0 * (3.0 * d + 12.0), wB = 8.0 * (3.0 * d + 12.0) + 8.0 * (double)ceil_to((int)r, 4);
+    std::vector<std::pair<double, int>> items;  // (weight, code): code >= 0 B block, < 0 A group -code-1
     for (int g = 0; g < nBg; ++g) items.push_back({wB, g});
-    for (int j = 0; j < (int)r; ++j) items.push_back({wA, -j - 1});
+    for (int j = 0; j < ceil_to((int)r, 4) / 4; ++j) items.push_back({wA, -j - 1});
     std::stable_sort(items.begin(), items.end(), [](auto& x, auto& y) { return x.first > y.first; });
     std::vector<double> wl(kEW, 0.0), sl(4, 0.0);
     std::vector<std::vector<short>> la(kEW), lb(kEW);
@@ -916,10 +918,11 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     }
   }
   const int rr = (int)r, r4 = ceil_to(rr, 4);
-  const int rS = ceil_to(rr > 0 ? rr : 1, 2), mN = NBN * 8;
+  const int rS = r4, mN = NBN * 8;
   const int TS = (r4 > 0 ? r4 : 4) * kST, TN = ceil_to(NBN + 1, 2) * 8 * kST;
-  const size_t smem = sizeof(double) * ((size_t)d * rS + (size_t)d * mN + (size_t)r4 * frag_stride(meff) +
-                                        2 * (size_t)TS + (size_t)kStages * TN + (size_t)kRing * d * kTM);
+  const size_t smem = sizeof(double) * ((size_t)r4 * frag_stride(meff) + 2 * (size_t)TS + (size_t)kStages * TN +
+                                        (size_t)kRing * d * kTM);
+  if ((size_t)d * (rS + mN) > (size_t)kCSrc) return gram_dev_large(c, h, r, d_out);
   if (smem > 190 * 1024 || NBN > 16 || getenv("KID_FORCE_LARGE")) return gram_dev_large(c, h, r, d_out);
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
@@ -955,6 +958,16 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   A.tv = view(c);
   A.d = d;
   A.src = r > 0 ? c->src_perm : c->src;
+  {
+    const std::vector<double>& sh = r > 0 ? c->src_perm_host : c->src_host;
+    if (sh.size() != (size_t)m * d) return fail(c, KID_E_ERROR, "gram: host copy of the sources is stale");
+    const double cs = std::sqrt(1.0 / (2.0 * h * h));
+    for (int k = 0; k < d; ++k) {
+      for (int j = 0; j < rS; ++j) A.csrc[k * rS + j] = j < rr ? sh[(size_t)k * m + j] * cs : 1.0e4;
+      for (int j = 0; j < mN; ++j)
+        A.csrc[d * rS + k * mN + j] = j < meff ? sh[(size_t)k * m + rr + j] * cs : 1.0e4;  // far away: K == 0
+    }
+  }
   A.m = m;
   A.r = (int)r;
   A.meff = meff;
@@ -996,7 +1009,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     cudaFree(A.trace);
     // per-phase mean cycles over tiles 4..kTraceTiles-1 (steady state): MMA warp 0, eval warp 0
     auto at = [&](int w, int it, int ev) { return tr[((size_t)w * kTraceTiles + it) * 4 + ev]; };
-    double mw_full = 0, mw_syrk = 0, ew_empty = 0, ew_eval = 0, tile = 0;
+    double mw_full = 0, mw_syrk = 0, ew_empty = 0, ew_eval = 0, ew_bar = 0, tile = 0;
     int n = 0;
     for (int it = 4; it + 1 < kTraceTiles; ++it) {
       if (!at(kMmaW0, it + 1, 0)) break;
@@ -1004,6 +1017,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
       mw_syrk += at(kMmaW0, it, 3) - at(kMmaW0, it, 1);
       ew_empty += at(kEvalW0, it, 1) - at(kEvalW0, it, 0);
       ew_eval += at(kEvalW0, it, 2) - at(kEvalW0, it, 1);
+      ew_bar += at(kEvalW0, it, 3) - at(kEvalW0, it, 2);
       tile += at(kMmaW0, it + 1, 0) - at(kMmaW0, it, 0);
       ++n;
     }
@@ -1013,9 +1027,20 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     for (int w = kMmaW0; w < kMmaW0 + kMW; ++w) fprintf(stderr, " %lld", at(w, 10, 3) - at(w, 10, 1));
     fprintf(stderr, "\n");
     if (n)
+      {
+        double g3 = 0, g0 = 0;
+        int nn = 0;
+        for (int it = 4; it + 1 < kTraceTiles; ++it) {
+          if (!at(kEvalW0 + kEW - 1, it + 1, 0)) break;
+          g0 += at(kEvalW0, it + 1, 0) - at(kEvalW0, it, 3);
+          g3 += at(kEvalW0 + kEW - 1, it + 1, 0) - at(kEvalW0 + kEW - 1, it, 3);
+          ++nn;
+        }
+        if (nn) fprintf(stderr, "[kid trace] evalbar->next tile: copier warp %.0f, last eval warp %.0f\n", g0 / nn, g3 / nn);
+      }
       fprintf(stderr, "[kid trace] cycles/tile: tile %.0f | mma: wait_full %.0f syrk %.0f | "
-                      "eval: wait_empty %.0f eval %.0f (n=%d)\n",
-              tile / n, mw_full / n, mw_syrk / n, ew_empty / n, ew_eval / n, n);
+                      "eval: wait_empty %.0f eval %.0f arrive+evalbar %.0f (n=%d)\n",
+              tile / n, mw_full / n, mw_syrk / n, ew_empty / n, ew_eval / n, ew_bar / n, n);
   }
   k_gram_reduce<<<std::max(1, std::min(c->sms * 2, (meff * meff + 31) / 32)), 1024, 0, c->stream>>>(
       partial, nchunks, LG, meff, partial_sk, d_out);
@@ -1033,9 +1058,9 @@ int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_s
   const int m4 = ceil_to(m, 4), SN = frag_stride(m4), SW = frag_stride(rr), NBR = ceil_to(rr, 8) / 8;
   size_t smem = sizeof(double) * ((size_t)d * m + (size_t)d * kTM + (size_t)kTM * SN + (size_t)kTM * NBR);
   const size_t wbytes = sizeof(double) * (size_t)m4 * SW;
-  bool w_in_smem = smem + wbytes <= 200 * 1024;
+  bool w_in_smem = smem + wbytes <= 190 * 1024;
   if (w_in_smem) smem += wbytes;
-  if (smem > 220 * 1024) return fail(c, KID_E_DIM, "leverage: tile does not fit shared memory");
+  if (smem > 205 * 1024) return fail(c, KID_E_DIM, "leverage: tile does not fit shared memory");
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   LevArgs A{view(c), d, c->src, m, rr, -1.0 / (2.0 * h * h), d_W, w_in_smem, d_scores};
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;

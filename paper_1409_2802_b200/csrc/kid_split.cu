@@ -383,6 +383,9 @@ int split_finish(kid_ctx* c, const int64_t* src_idx_h, int64_t n, const double* 
   KID_LAUNCHED(c);
   int64_t nt = 0;
   KID_CK(c, cudaMemcpyAsync(&nt, c->counter + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  c->src_host.resize((size_t)n * d);
+  if (src_pts_h) std::memcpy(c->src_host.data(), src_pts_h, sizeof(double) * n * d);
+  else KID_CK(c, cudaMemcpyAsync(c->src_host.data(), c->src, sizeof(double) * n * d, cudaMemcpyDeviceToHost, c->stream));
   KID_CK(c, cudaStreamSynchronize(c->stream));
   c->n_split_targets = nt;
   c->tbase = c->pts;

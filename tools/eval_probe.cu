@@ -5,14 +5,14 @@
 #include <cmath>
 #include <cuda_runtime.h>
 #include "../paper_1409_2802_b200/csrc/kid_internal.cuh"
-__device__ double g_tab[1024];
+__device__ double g_tab[kid::kExpTab];
 constexpr int D = 3, M = 96, KST = 36;
 template <int ILP, int VAR>
 __global__ void k(double* out, int reps, double cs) {
-  __shared__ double tab[1024];
+  __shared__ double tab[kid::kExpTabWords];
   __shared__ __align__(16) double src[D * M];
   extern __shared__ double KN[];  // M x KST per warp-group (shared by warps: races are harmless here)
-  for (int e = threadIdx.x; e < 1024; e += blockDim.x) tab[e] = g_tab[e];
+  for (int e = threadIdx.x; e < kid::kExpTabWords; e += blockDim.x) tab[e] = g_tab[e / kid::kExpRep];
   for (int e = threadIdx.x; e < D * M; e += blockDim.x) src[e] = 0.01 * (e % 97) - 0.3;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -42,8 +42,8 @@ __global__ void k(double* out, int reps, double cs) {
 #pragma unroll
       for (int u = 0; u < ILP; ++u) {
         double e;
-        if (VAR == 1) e = kid::exp_neg_notab(kv[u]);
-        else e = kid::exp_neg_fast(kv[u], tab);
+        if (VAR == 1) e = kid::exp_neg_fast(kv[u], tab + lane);  // (no-table variant removed)
+        else e = kid::exp_neg_fast(kv[u], tab + lane);
         kv[u] = lane < 40 ? e : 0.0;
         sk = fma(kv[u], kv[u], sk);
         if (VAR != 2) KN[(j0 + u) * KST + lane] = kv[u];
@@ -69,8 +69,8 @@ void run(int warps, double* out) {
          exps / (ms * 1e-3) / 148 / 1.965e9);
 }
 int main() {
-  double tab[1024];
-  for (int j = 0; j < 1024; ++j) tab[j] = (double)exp2l((long double)j / 1024.0L);
+  double tab[kid::kExpTab];
+  for (int j = 0; j < kid::kExpTab; ++j) tab[j] = (double)exp2l((long double)j / (long double)kid::kExpTab);
   cudaMemcpyToSymbol(g_tab, tab, sizeof(tab));
   double* out; cudaMalloc(&out, 1 << 24);
   for (int w : {8, 12, 16, 24}) {

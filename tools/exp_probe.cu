@@ -3,11 +3,11 @@
 #include <cmath>
 #include <cuda_runtime.h>
 #include "../paper_1409_2802_b200/csrc/kid_internal.cuh"
-__device__ double g_tab[1024];
+__device__ double g_tab[kid::kExpTab];
 template <int ILP, int MODE>
 __global__ void k(double* out, int iters) {
-  __shared__ double tab[1024];
-  for (int e = threadIdx.x; e < 1024; e += blockDim.x) tab[e] = g_tab[e];
+  __shared__ double tab[kid::kExpTabWords];
+  for (int e = threadIdx.x; e < kid::kExpTabWords; e += blockDim.x) tab[e] = g_tab[e / kid::kExpRep];
   __syncthreads();
   double q[ILP], acc = 0;
 #pragma unroll
@@ -15,7 +15,7 @@ __global__ void k(double* out, int iters) {
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
     for (int u = 0; u < ILP; ++u) {
-      double v = MODE == 0 ? kid::exp_neg_fast(q[u], tab) : exp(-q[u]);
+      double v = MODE == 0 ? kid::exp_neg_fast(q[u], tab + (threadIdx.x & 31)) : exp(-q[u]);
       acc = fma(v, v, acc);
       q[u] += 0.001;
     }
@@ -38,8 +38,8 @@ void run(int warps_per_sm, double* out) {
          MODE == 0 ? "exp_neg_fast" : "libdevice", ILP, warps_per_sm, n / ms / 1e6, n / (ms * 1e-3 * 1.965e9 * 148));
 }
 int main() {
-  double tab[1024];
-  for (int j = 0; j < 1024; ++j) tab[j] = (double)exp2l((long double)j / 1024.0L);
+  double tab[kid::kExpTab];
+  for (int j = 0; j < kid::kExpTab; ++j) tab[j] = (double)exp2l((long double)j / (long double)kid::kExpTab);
   cudaMemcpyToSymbol(g_tab, tab, sizeof(tab));
   double* out; cudaMalloc(&out, 1 << 24);
   for (int w : {4, 8, 16, 32}) { run<1, 0>(w, out); run<2, 0>(w, out); run<4, 0>(w, out); run<8, 0>(w, out); }
