@@ -122,7 +122,7 @@ struct GramArgs {
   int nchunks;
   double* partial;     // [nchunks][LG][LG]
   int LG;              // padded Gram leading dimension = ceil8(meff)
-  double* partial_sk;  // [nchunks] (written by part 0)
+  double* partial_sk;  // [nchunks] sum K^2 (part 0), then [nparts][nchunks] partial traces of D^T D
   int dbg;             // profiling aid (KID_GRAM_DEBUG): 1 skip eval math, 2 skip the K_S P2 FMAs, 4 skip SYRK,
                        // 16 no coordinate copies (ring slots keep tile 0's targets)
   long long* trace;    // profiling aid (KID_GRAM_TRACE): [warp][tile][4] clock64 stamps of CTA 0
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArg
   double* KSb = sP + (size_t)r4 * SPn;           // 2 x (r4 x kST): K_S, column-major [k][t]; rows >= r are 0
   double* KNb = KSb + 2 * (size_t)TS;            // kStages x (.. x kST): D, column-major [col][t]
   double* ring = KNb + (size_t)kStages * TN;     // kRing x d x 32 target coordinates (unscaled)
-  __shared__ double red[kEW];
+  __shared__ double red[kEW], red_tr[kMW];
   __shared__ double s_tab[kExpTabWords];
   __shared__ short s_el[kEW * kEItems];
 
@@ -459,6 +459,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArg
       if (it + kStages < ntile) nbar_arrive(kBarEmpty + s, kGT);  // release stage s
     }
     double* G = A.partial + (size_t)chunk * A.LG * A.LG;
+    double trd = 0.0;  // this warp's share of trace(D^T D) = ||D||_F^2
 #pragma unroll
     for (int q = 0; q < TPW; ++q) {
       if (tl[q].x < 0) continue;
@@ -471,17 +472,24 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArg
             const int row = a * 8 + fr, colx = b * 8 + 2 * fk;
             G[row + (size_t)colx * A.LG] = acc[q][u][v][0];
             G[row + (size_t)(colx + 1) * A.LG] = acc[q][u][v][1];
+            if (row == colx) trd += acc[q][u][v][0];
+            if (row == colx + 1) trd += acc[q][u][v][1];
           }
         }
     }
+    trd = warp_sum(trd);
+    if (lane == 0) red_tr[mw] = trd;
   }
-  if (part == 0) {
-    __syncthreads();
-    if (tid == 0) {
+  __syncthreads();
+  if (tid == 0) {
+    if (part == 0) {
       double t = 0.0;
       for (int w = 0; w < kEW; ++w) t += red[w];
       A.partial_sk[chunk] = t;
     }
+    double t = 0.0;
+    for (int w = 0; w < kMW; ++w) t += red_tr[w];
+    A.partial_sk[(size_t)A.nchunks * (1 + part) + chunk] = t;
   }
 }
 
@@ -489,12 +497,25 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArg
 // Block = 32 consecutive output elements x 32 chunk groups; group g sums chunks g, g+32, ...
 // in order, then the 32 group sums are combined in a fixed order: deterministic.
 __global__ void __launch_bounds__(1024) k_gram_reduce(const double* __restrict__ partial, int nchunks, int LG,
-                                                      int meff, const double* __restrict__ partial_sk,
+                                                      int meff, const double* __restrict__ partial_sk, int nparts,
                                                       double* __restrict__ out) {
   __shared__ double part_s[32][33];
   const int64_t total = (int64_t)meff * meff;
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   double* G = out + 2;
+  if (blockIdx.x == 0 && g == 31) {
+    // out[0] = trace(G) and out[1] = ||K||_F^2 from the per-CTA partials (fixed order: lane-
+    // strided sums, then a fixed shuffle tree) -- deterministic run to run
+    double sk = 0.0, tr = 0.0;
+    for (int c = lane; c < nchunks; c += 32) sk += partial_sk[c];
+    for (int c = lane; c < nchunks * nparts; c += 32) tr += partial_sk[nchunks + c];
+    sk = warp_sum(sk);
+    tr = warp_sum(tr);
+    if (lane == 0) {
+      out[0] = tr;
+      out[1] = sk;
+    }
+  }
   for (int64_t base = (int64_t)blockIdx.x * 32; base < total; base += (int64_t)gridDim.x * 32) {
     const int64_t e = base + lane;
     double s = 0.0;
@@ -504,6 +525,7 @@ __global__ void __launch_bounds__(1024) k_gram_reduce(const double* __restrict__
       int ux = x, uy = y;
       if ((x >> 3) > (y >> 3) || (((x >> 3) == (y >> 3)) && x > y)) { ux = y; uy = x; }
       off = ux + (int64_t)uy * LG;
+#pragma unroll 8
       for (int c = g; c < nchunks; c += 32) s += partial[(size_t)c * LG * LG + off];
     }
     part_s[g][lane] = s;
@@ -514,17 +536,6 @@ __global__ void __launch_bounds__(1024) k_gram_reduce(const double* __restrict__
       G[e] = t;
     }
     __syncthreads();
-  }
-}
-
-__global__ void k_gram_finish(const double* __restrict__ partial_sk, int nchunks, int meff, double* __restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double sk = 0.0;
-    for (int c = 0; c < nchunks; ++c) sk += partial_sk[c];
-    double tr = 0.0;
-    for (int x = 0; x < meff; ++x) tr += out[2 + x + (size_t)x * meff];
-    out[0] = tr;
-    out[1] = sk;
   }
 }
 
@@ -942,7 +953,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   // scratch: blist | elist | partial | partial_sk
   const size_t bl_bytes = sizeof(int2) * blist.size() + sizeof(short) * elist.size();
   const size_t part_bytes = sizeof(double) * (size_t)nchunks * LG * LG;
-  char* base = (char*)scratch(c, bl_bytes + 256 + part_bytes + sizeof(double) * (nchunks + 8));
+  char* base = (char*)scratch(c, bl_bytes + 256 + part_bytes + sizeof(double) * ((size_t)nchunks * (1 + nparts) + 8));
   if (!base) return KID_E_OOM;
   int2* d_blist = (int2*)base;
   double* partial = (double*)(base + ((bl_bytes + 255) / 256) * 256);
@@ -1043,9 +1054,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
               tile / n, mw_full / n, mw_syrk / n, ew_empty / n, ew_eval / n, ew_bar / n, n);
   }
   k_gram_reduce<<<std::max(1, std::min(c->sms * 2, (meff * meff + 31) / 32)), 1024, 0, c->stream>>>(
-      partial, nchunks, LG, meff, partial_sk, d_out);
-  KID_LAUNCHED(c);
-  k_gram_finish<<<1, 32, 0, c->stream>>>(partial_sk, nchunks, meff, d_out);
+      partial, nchunks, LG, meff, partial_sk, nparts, d_out);
   KID_LAUNCHED(c);
   return KID_OK;
 }
