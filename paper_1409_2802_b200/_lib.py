@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-CUDA_SO = os.path.join(PKG, "libkernid_cuda.so")
+CUDA_SO = os.environ.get("KID_CUDA_SO") or os.path.join(PKG, "libkernid_cuda.so")  # override: A/B profiling only
 
 KID_OK, KID_E_RANGE, KID_E_DIM, KID_E_NO_TARGETS, KID_E_NUMERICAL = 0, 1, 2, 3, 4
 KID_E_ERROR, KID_E_CUDA, KID_E_OOM, KID_E_ILLCOND, KID_E_CONFIG = 5, 6, 7, 8, 9
