@@ -378,6 +378,53 @@ def run_split(args):
     print(json.dumps(line), flush=True)
 
 
+def run_apply(args):
+    """--pass apply: the skeleton matvec u = K(T, S_skel) (P q) over all targets (compress.hpp:
+    309-325) for the config's ID; FP64 roofline with 3d + 33 + 2 flops per
+    (target, skeleton point) entry (eval + exp by the 8(d) convention, multiply-add)."""
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    torch.cuda.set_stream(torch.cuda.Stream())
+    wl = WORKLOADS[args.config]
+    dev, prob = setup(wl, 1, 0, local, torch)
+    stream = torch.cuda.current_stream()
+    dev.set_stream(stream.cuda_stream)
+    d, m, r = wl["d"], wl["m"], prob.r
+    q = np.random.default_rng(0).standard_normal(m)
+    q_skel = prob.P @ q
+    u = torch.empty(max(prob.nt, 1), dtype=torch.float64, device="cuda")
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    for _ in range(args.warmup):
+        dev.apply_skeleton_dev(prob.h, prob.skel, q_skel, u.data_ptr())
+    torch.cuda.synchronize()
+    dev.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        dev.apply_skeleton_dev(prob.h, prob.skel, q_skel, u.data_ptr())
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    kms = dev.profile_read()
+    dev.profile(False)
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    kavg = float(np.mean(kms)) if len(kms) else float("nan")
+    entries = float(prob.nt) * r
+    fpe = 3 * d + 33 + 2
+    peaks = load_peaks()
+    ach = entries * fpe / (kavg / 1e3) / 1e12
+    line = {"metric": "apply_skeleton entries/s (targets x skeleton points, FP64)", "value": entries / (ms / 1e3),
+            "unit": "entries/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "dtype": "f64",
+            "config": {"workload": f"{args.config}: N_T={prob.nt}, m={m}, skeleton rank r={r}, d={d}",
+                       "l2": "flushed (256 MB write) between timed steps"},
+            "roofline": {"bound": "fp64", "unit": "TFLOP/s", "peak": peaks["fp64_tflops"], "achieved": ach,
+                         "frac": ach / peaks["fp64_tflops"], "kernel": "k_apply_skel", "kernel_ms": kavg,
+                         "flops_per_entry": fpe}}
+    print(json.dumps(line), flush=True)
+
+
 def run_e2e(args, dev, prob, torch, ws, rank):
     """Same metric through the C-ABI with host buffers (pinned points H2D every step)."""
     wl = prob.wl
@@ -500,7 +547,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=50000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split"])
+    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -508,6 +555,8 @@ def main():
         run_reference(args)
     elif args.pass_ == "split":
         run_split(args)
+    elif args.pass_ == "apply":
+        run_apply(args)
     else:
         run_ours(args)
 

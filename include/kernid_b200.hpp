@@ -210,6 +210,14 @@ double reconstruction_bound(int64_t m, int64_t s_count, double eps, double sigma
 std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, const RowSample& sample,
                                                           const RankRule& rule, const CompressOptions& opts = {});
 
+// compress.hpp:279-305 for the ID reconstruction (khat_row(i) = K[i, skel] P), on the device:
+// each repetition draws Bernoulli(s_mc) rows with the reference seeds, restricts the block to
+// them (kid_select_rows) and takes both spectral norms through the Gram route.
+std::vector<double> mc_error(const KernelBlock& K, const IDFactorization& id, double s_mc, int n_mc,
+                             std::uint64_t seed);
+// compress.hpp:309-325 on the device: u_i = sum_j Ker(y_i, x_skel_j) (P q)_j over the block's targets.
+std::vector<double> apply_skeleton(const KernelBlock& K, const IDFactorization& id, const std::vector<double>& q);
+
 // ------------------------------------------------------------- harness.hpp (compress sweep)
 struct ExperimentConfig {
   int d = 2;

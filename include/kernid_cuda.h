@@ -115,6 +115,21 @@ int kid_recon_error_dev(kid_ctx* ctx, double h, uint32_t flags, double* d_out);
 /* ---- gather_rows of K on the device (compress.hpp:130-137): Ks (count x m col-major) ---- */
 int kid_eval_rows(kid_ctx* ctx, double h, const int64_t* rows, int64_t count, double* Ks_out);
 
+/* ---- skeleton matvec (compress.hpp:309-325) ----
+ * u_i = sum_j Ker(y_i, x_skel_j) (P q)_j over the block's targets y_i, x_skel_j = the block's
+ * source skel[j]; P is r x m col-major (the ID projection), q the m charges; u_out n_targets.
+ * The device variant takes q_skel = P q (r entries, host) and writes d_u (n_targets, device). */
+int kid_apply_skeleton(kid_ctx* ctx, double h, const int64_t* skel, int64_t r, const double* P, const double* q,
+                       double* u_out);
+int kid_apply_skeleton_dev(kid_ctx* ctx, double h, const int64_t* skel, int64_t r, const double* q_skel,
+                           double* d_u);
+
+/* ---- row-subset view (mc_error, compress.hpp:279-305) ----
+ * Restricts the block's targets to rows[0..n) of the full target list (row numbers as in K);
+ * every pass above then runs on that subset. n < 0 (rows ignored) restores the full list;
+ * kid_split / kid_set_block also reset it. */
+int kid_select_rows(kid_ctx* ctx, const int64_t* rows, int64_t n);
+
 /* ---- diagnostics: the FP64 passes' exp(x), x <= 0 (for accuracy checks against libm) ---- */
 int kid_exp_check(kid_ctx* ctx, const double* x, int64_t n, double* y);
 

@@ -374,6 +374,13 @@ int64_t or_sample_rows(int32_t kind, int32_t replacement, int64_t m, const doubl
   if (m < 1) return -1;
   or_rng rng;
   or_rng_init(&rng, seed);
+  if (kind == 1) { /* Bernoulli (sampling.hpp:183-188): out must hold m entries */
+    if (!(s > 0.0 && s <= 1.0)) return -1;
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < m; ++i)
+      if (or_rng_uniform01(&rng) < s) out[cnt++] = i;
+    return cnt;
+  }
   const int64_t count = or_sample_count(s, m);
   if (count < 0) return -1;
   if (kind == 0) { /* :166-182 */
@@ -972,4 +979,81 @@ void or_jacobi_eigen(const double* A_in, int64_t n, double* evals, double* evecs
     if (evecs) memcpy(evecs + i * n, V + order[i] * n, sizeof(double) * (size_t)n);
   }
   free(order); free(A); free(V);
+}
+
+/* -------------------------------------------------------------- compress.hpp: next rows */
+
+/* apply_skeleton (compress.hpp:309-325): q_skel = P q (Eigen GEMV, accumulated over the m
+ * columns of P in order), u_i = sum_j eval_kernel(y_i, xskel_j) q_skel_j sequentially over j
+ * (mul then add: -ffp-contract=off). tgt nt x d, skel_pts r x d (col-major), P r x m col-major. */
+void or_apply_skeleton(const double* tgt, int64_t nt, const double* skel_pts, int64_t r, int32_t d, double h,
+                       const double* P, int64_t m, const double* q, double* u) {
+  double* qs = (double*)calloc((size_t)(r > 0 ? r : 1), sizeof(double));
+  for (int64_t k = 0; k < m; ++k)
+    for (int64_t j = 0; j < r; ++j) qs[j] += P[j + k * r] * q[k];
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  double* y = (double*)malloc(sizeof(double) * (size_t)d);
+  for (int64_t i = 0; i < nt; ++i) {
+    for (int32_t k = 0; k < d; ++k) x[k] = tgt[i + k * nt];
+    double acc = 0.0;
+    for (int64_t j = 0; j < r; ++j) {
+      for (int32_t k = 0; k < d; ++k) y[k] = skel_pts[j + k * r];
+      acc += or_eval_gaussian(x, y, d, h) * qs[j];
+    }
+    u[i] = acc;
+  }
+  free(x); free(y); free(qs);
+}
+
+/* mc_error (compress.hpp:279-305) for the ID reconstruction khat_row(i) = K[i, skel] P:
+ * per repetition a Bernoulli(s_mc) row draw with seed derive_seed(seed, rep) (retried once with
+ * derive_seed(seed, rep, 1) when empty), num = matrix_norm(khat rows - K rows), den =
+ * matrix_norm(K rows). est (n_mc). returns 0, 1 RangeError, 5 Error (empty twice). */
+int or_mc_error(const double* K, int64_t nt, int64_t m, const int64_t* skel, int64_t r, const double* P,
+                double s_mc, int32_t n_mc, uint64_t seed, double budget, double tol, int32_t cap, double* est) {
+  if (!(s_mc > 0.0 && s_mc <= 1.0) || n_mc < 1) return 1;
+  int64_t* rows = (int64_t*)malloc(sizeof(int64_t) * (size_t)nt);
+  for (int32_t rep = 0; rep < n_mc; ++rep) {
+    int64_t cnt = or_sample_rows(1, 0, nt, NULL, s_mc, or_derive_seed(seed, (uint64_t)rep, 0), rows);
+    if (cnt == 0) cnt = or_sample_rows(1, 0, nt, NULL, s_mc, or_derive_seed(seed, (uint64_t)rep, 1), rows);
+    if (cnt <= 0) { free(rows); return 5; }
+    double* ks = (double*)malloc(sizeof(double) * (size_t)(cnt * m));
+    double* diff = (double*)malloc(sizeof(double) * (size_t)(cnt * m));
+    for (int64_t i = 0; i < cnt; ++i)
+      for (int64_t j = 0; j < m; ++j) ks[i + j * cnt] = K[rows[i] + j * nt];
+    for (int64_t i = 0; i < cnt; ++i)
+      for (int64_t j = 0; j < m; ++j) {
+        double acc = 0.0;  /* khat_row(i)_j = sum_l K[i, skel_l] P[l, j] */
+        for (int64_t l = 0; l < r; ++l) acc += K[rows[i] + skel[l] * nt] * P[l + j * r];
+        diff[i + j * cnt] = acc - ks[i + j * cnt];
+      }
+    const double den = or_matrix_norm(ks, cnt, m, budget, tol, cap);
+    const double num = or_matrix_norm(diff, cnt, m, budget, tol, cap);
+    est[rep] = den > 0.0 ? num / den : (num > 0.0 ? 1.0 / 0.0 : 0.0);
+    free(ks); free(diff);
+  }
+  free(rows);
+  return 0;
+}
+
+/* compress_svd error (compress.hpp:243-262): B = K V_r, diff = B V_r^T - K, num = spectral norm
+ * (exact) of diff; returns num (the caller divides by its norm of K). Vr m x r col-major. */
+double or_svd_error_norm(const double* K, int64_t nt, int64_t m, const double* Vr, int64_t r, double budget,
+                         double tol, int32_t cap) {
+  double* B = (double*)calloc((size_t)(nt * (r > 0 ? r : 1)), sizeof(double));
+  for (int64_t k = 0; k < r; ++k)
+    for (int64_t j = 0; j < m; ++j) {
+      const double v = Vr[j + k * m];
+      for (int64_t i = 0; i < nt; ++i) B[i + k * nt] += K[i + j * nt] * v;
+    }
+  double* diff = (double*)malloc(sizeof(double) * (size_t)(nt * m));
+  for (int64_t j = 0; j < m; ++j)
+    for (int64_t i = 0; i < nt; ++i) {
+      double acc = 0.0;
+      for (int64_t k = 0; k < r; ++k) acc += B[i + k * nt] * Vr[j + k * m];
+      diff[i + j * nt] = acc - K[i + j * nt];
+    }
+  const double num = or_matrix_norm(diff, nt, m, budget, tol, cap);
+  free(B); free(diff);
+  return num;
 }

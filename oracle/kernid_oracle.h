@@ -78,7 +78,8 @@ void or_row_norms(const double* K, int64_t nt, int64_t m, double* w);
 int or_weighted_draw(const double* w, int64_t n, int64_t count, int32_t replacement, or_rng* rng,
                      int64_t* out);
 /* sample_rows for Uniform / EuclideanNorm / Leverage(with given scores) given weights;
- * kind 0 Uniform, 2 EuclideanNorm (weights = row norms), 4 Leverage (weights = scores).
+ * kind 0 Uniform, 1 Bernoulli (random count, out holds m), 2 EuclideanNorm (weights = row norms),
+ * 4 Leverage (weights = scores).
  * out must hold sample_count entries (or m for replacement). returns count or negative error. */
 int64_t or_sample_rows(int32_t kind, int32_t replacement, int64_t m, const double* weights, double s,
                        uint64_t seed, int64_t* out);
@@ -124,6 +125,16 @@ int or_compress_id(const double* K, int64_t nt, int64_t m, const int64_t* rows, 
                    double eps, int64_t fixed_r, double ref_sigma1, double k_norm, double budget,
                    double tol, int32_t cap, int64_t* rank, double* rel_error, int64_t* skel,
                    double* P, double* sigma1_sample, double* sigma_r1_sample, double* bound_id);
+
+/* apply_skeleton (compress.hpp:309-325): u (nt) */
+void or_apply_skeleton(const double* tgt, int64_t nt, const double* skel_pts, int64_t r, int32_t d, double h,
+                       const double* P, int64_t m, const double* q, double* u);
+/* mc_error (compress.hpp:279-305) for khat_row(i) = K[i, skel] P; est (n_mc); 0, 1 RangeError, 5 Error */
+int or_mc_error(const double* K, int64_t nt, int64_t m, const int64_t* skel, int64_t r, const double* P,
+                double s_mc, int32_t n_mc, uint64_t seed, double budget, double tol, int32_t cap, double* est);
+/* compress_svd numerator (compress.hpp:243-262): ||K V_r V_r^T - K|| */
+double or_svd_error_norm(const double* K, int64_t nt, int64_t m, const double* Vr, int64_t r, double budget,
+                         double tol, int32_t cap);
 
 /* sym eigen (Jacobi, tests/oracles.hpp:19-66 style), evals desc, evecs col-major */
 void or_jacobi_eigen(const double* A, int64_t n, double* evals, double* evecs);

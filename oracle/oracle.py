@@ -25,7 +25,7 @@ _lib = None
 # error codes shared with the product C-ABI (include/kernid_cuda.h)
 E_RANGE, E_DIM, E_NO_TARGETS, E_NUMERICAL, E_ERROR, E_ILLCOND = 1, 2, 3, 4, 5, 8
 
-SCHEME_UNIFORM, SCHEME_EUCLIDEAN, SCHEME_LEVERAGE = 0, 2, 4
+SCHEME_UNIFORM, SCHEME_BERNOULLI, SCHEME_EUCLIDEAN, SCHEME_LEVERAGE = 0, 1, 2, 4
 
 
 def build() -> str:
@@ -73,6 +73,10 @@ def _declare(L):
     L.or_row_norms.argtypes = [_dp, i64, i64, _dp]
     L.or_sample_rows.restype = i64
     L.or_sample_rows.argtypes = [i32, i32, i64, C.c_void_p, dbl, u64, _ip]
+    L.or_apply_skeleton.argtypes = [_dp, i64, _dp, i64, i32, dbl, _dp, i64, _dp, _dp]
+    L.or_mc_error.argtypes = [_dp, i64, i64, _ip, i64, _dp, dbl, i32, u64, dbl, dbl, i32, _dp]
+    L.or_svd_error_norm.restype = dbl
+    L.or_svd_error_norm.argtypes = [_dp, i64, i64, _dp, i64, dbl, dbl, i32]
     L.or_qr_r.argtypes = [_dp, i64, i64, _dp]
     L.or_jacobi_svd.argtypes = [_dp, i64, _dp, C.c_void_p]
     L.or_singular_values.argtypes = [_dp, i64, i64, _dp]
@@ -216,8 +220,8 @@ def row_norms(K: np.ndarray) -> np.ndarray:
 
 
 def sample_rows(kind: int, m: int, s: float, seed: int, weights=None, replacement: bool = False) -> np.ndarray:
-    """sample_rows (sampling.hpp:156-243) for Uniform / EuclideanNorm / Leverage weights."""
-    cnt = sample_count(s, m)
+    """sample_rows (sampling.hpp:156-243) for Uniform / Bernoulli / EuclideanNorm / Leverage weights."""
+    cnt = m if kind == SCHEME_BERNOULLI else sample_count(s, m)
     out = np.zeros(cnt, np.int64)
     wp = None
     if weights is not None:
@@ -226,7 +230,7 @@ def sample_rows(kind: int, m: int, s: float, seed: int, weights=None, replacemen
     rc = int(lib().or_sample_rows(kind, int(replacement), m, wp, s, seed, out))
     if rc < 0:
         raise OracleError(-rc, "sample_rows")
-    return out
+    return out[:rc].copy()
 
 
 # ------------------------------------------------------------- lowrank.hpp
@@ -372,6 +376,34 @@ def compress_id(K, rows, eps=None, fixed_r=None, ref_sigma1=None, k_norm=None,
     r = rank.value
     return CompressResult(r, rel.value, skel[:r].copy(), _from_f(P[: r * m], r, m) if r else np.zeros((0, m)),
                           s1.value, sr1.value, bid.value, r == 0)
+
+
+def apply_skeleton(targets, skel_points, h, P, q) -> np.ndarray:
+    """apply_skeleton (compress.hpp:309-325): u_i = sum_j Ker(y_i, xskel_j) (P q)_j."""
+    nt, d = targets.shape
+    r = skel_points.shape[0]
+    m = P.shape[1]
+    u = np.zeros(nt)
+    lib().or_apply_skeleton(_f(targets), nt, _f(skel_points), r, d, h, _f(P), m,
+                            np.ascontiguousarray(q, dtype=np.float64), u)
+    return u
+
+
+def mc_error(K, skel, P, s_mc, n_mc, seed, budget=BUDGET, tol=POWER_TOL, cap=POWER_CAP) -> np.ndarray:
+    """mc_error (compress.hpp:279-305) with khat_row(i) = K[i, skel] P."""
+    nt, m = K.shape
+    est = np.zeros(n_mc)
+    rc = lib().or_mc_error(_f(K), nt, m, np.ascontiguousarray(skel, dtype=np.int64), len(skel), _f(P),
+                           s_mc, n_mc, seed, budget, tol, cap, est)
+    if rc:
+        raise OracleError(rc, "mc_error")
+    return est
+
+
+def svd_error_norm(K, Vr, budget=BUDGET, tol=POWER_TOL, cap=POWER_CAP) -> float:
+    """compress_svd numerator (compress.hpp:243-262): ||K V_r V_r^T - K||."""
+    nt, m = K.shape
+    return float(lib().or_svd_error_norm(_f(K), nt, m, _f(Vr), Vr.shape[1], budget, tol, cap))
 
 
 # ------------------------------------------------------------- harness.hpp

@@ -37,7 +37,8 @@ SYMBOLS = ["kid_abi_version", "kid_host_alloc", "kid_host_free", "kid_create", "
            "kid_set_points", "kid_set_points_device", "kid_split", "kid_split_candidates", "kid_split_finish",
            "kid_get_targets", "kid_set_block", "kid_block_shape", "kid_row_norms", "kid_row_norms_dev", "kid_gram",
            "kid_gram_dev", "kid_leverage", "kid_leverage_dev", "kid_recon_error", "kid_recon_prepare",
-           "kid_recon_error_dev", "kid_eval_rows", "kid_launch_count", "kid_profile", "kid_profile_read", "kid_exp_check"]
+           "kid_recon_error_dev", "kid_eval_rows", "kid_apply_skeleton", "kid_apply_skeleton_dev", "kid_select_rows",
+           "kid_launch_count", "kid_profile", "kid_profile_read", "kid_exp_check"]
 
 
 def cuda_lib():
@@ -79,6 +80,9 @@ def cuda_lib():
         L.kid_recon_prepare.argtypes = [vp, _ip, i64, _dp]
         L.kid_recon_error_dev.argtypes = [vp, dbl, u32, vp]
         L.kid_eval_rows.argtypes = [vp, dbl, _ip, i64, _dp]
+        L.kid_apply_skeleton.argtypes = [vp, dbl, _ip, i64, _dp, _dp, _dp]
+        L.kid_apply_skeleton_dev.argtypes = [vp, dbl, _ip, i64, _dp, vp]
+        L.kid_select_rows.argtypes = [vp, vp, i64]
         L.kid_launch_count.argtypes = [vp]
         L.kid_launch_count.restype = i64
         L.kid_profile.argtypes = [vp, i32]
@@ -268,6 +272,35 @@ class Device:
                                         KtK.ctypes.data if KtK is not None else None), "kid_recon_error")
         return (sd.value, sk.value, DtD.reshape(m, m).T.copy() if DtD is not None else None,
                 KtK.reshape(m, m).T.copy() if KtK is not None else None)
+
+    def apply_skeleton(self, h: float, skel, P: np.ndarray, q) -> np.ndarray:
+        """u = K(T, S[skel]) (P q) over the block's targets (kid_apply_skeleton)."""
+        skel = np.ascontiguousarray(skel, dtype=np.int64)
+        r = skel.size
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        u = np.zeros(max(self.nt, 1))
+        Pf = _colmajor(P) if r else np.zeros(1)
+        self._ck(self.L.kid_apply_skeleton(self.h, h, skel if r else np.zeros(1, np.int64), r, Pf, q, u),
+                 "kid_apply_skeleton")
+        return u[: self.nt].copy()
+
+    def apply_skeleton_dev(self, h: float, skel, q_skel, d_u: int):
+        skel = np.ascontiguousarray(skel, dtype=np.int64)
+        self._ck(self.L.kid_apply_skeleton_dev(self.h, h, skel, skel.size,
+                                               np.ascontiguousarray(q_skel, dtype=np.float64), d_u),
+                 "kid_apply_skeleton_dev")
+
+    def select_rows(self, rows=None):
+        """Restrict the block's targets to rows of the full list (None: restore it)."""
+        if rows is None:
+            self._ck(self.L.kid_select_rows(self.h, None, -1), "kid_select_rows")
+        else:
+            rows = np.ascontiguousarray(rows, dtype=np.int64)
+            self._ck(self.L.kid_select_rows(self.h, rows.ctypes.data if rows.size else None, rows.size),
+                     "kid_select_rows")
+        nt, m, d = C.c_int64(), C.c_int64(), C.c_int32()
+        self._ck(self.L.kid_block_shape(self.h, C.byref(nt), C.byref(m), C.byref(d)), "kid_block_shape")
+        self.nt = nt.value
 
     def eval_rows(self, h: float, rows) -> np.ndarray:
         rows = np.ascontiguousarray(rows, dtype=np.int64)

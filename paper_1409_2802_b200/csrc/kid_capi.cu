@@ -135,7 +135,7 @@ void kid_destroy(kid_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   void* bufs[] = {c->pts_own, c->dist, c->tgt_idx, c->blk_tgt, c->src, c->src_perm, c->P2,
-                  c->scratch, c->partial, c->counter, c->sort_tmp};
+                  c->scratch, c->partial, c->counter, c->sort_tmp, c->sub_idx};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->hbuf) cudaFreeHost(c->hbuf);
@@ -270,6 +270,7 @@ int kid_set_block(kid_ctx* c, const double* targets, int64_t nt, const double* s
   if (nt) KID_CK(c, cudaMemcpyAsync(c->blk_tgt, targets, sizeof(double) * nt * d, cudaMemcpyHostToDevice, c->stream));
   KID_CK(c, cudaMemcpyAsync(c->src, sources, sizeof(double) * m * d, cudaMemcpyHostToDevice, c->stream));
   c->src_host.assign(sources, sources + (size_t)m * d);
+  c->sub_active = false;
   c->tbase = c->blk_tgt;
   c->tld = nt;
   c->tidx = nullptr;
@@ -447,6 +448,35 @@ int kid_eval_rows(kid_ctx* c, double h, const int64_t* rows, int64_t count, doub
   if (count) KID_CK(c, cudaMemcpyAsync(Ks_out, buf, sizeof(double) * count * m, cudaMemcpyDeviceToHost, c->stream));
   KID_CK(c, cudaStreamSynchronize(c->stream));
   return KID_OK;
+}
+
+int kid_apply_skeleton_dev(kid_ctx* c, double h, const int64_t* skel, int64_t r, const double* q_skel, double* d_u) {
+  if (!c || (r && (!skel || !q_skel)) || (!d_u && c->nt)) return KID_E_ERROR;
+  if (int rc = set_device(c)) return rc;
+  return apply_skeleton_dev(c, h, skel, r, q_skel, d_u);
+}
+
+int kid_apply_skeleton(kid_ctx* c, double h, const int64_t* skel, int64_t r, const double* P, const double* q,
+                       double* u_out) {
+  if (!c || (r && (!skel || !P || !q)) || (!u_out && c->nt)) return KID_E_ERROR;
+  if (int rc = set_device(c)) return rc;
+  const int64_t m = c->m, nt = c->nt;
+  // q_skel = P q, accumulated over the m columns of P in order (Eigen's col-major GEMV)
+  std::vector<double> qs((size_t)std::max<int64_t>(r, 1), 0.0);
+  for (int64_t k = 0; k < m; ++k)
+    for (int64_t j = 0; j < r; ++j) qs[(size_t)j] += P[j + k * r] * q[k];
+  double* buf = out_buffer(c, std::max<int64_t>(nt, 1));
+  if (!buf) return KID_E_OOM;
+  if (int rc = apply_skeleton_dev(c, h, skel, r, qs.data(), buf)) return rc;
+  if (nt) KID_CK(c, cudaMemcpyAsync(u_out, buf, sizeof(double) * nt, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  return KID_OK;
+}
+
+int kid_select_rows(kid_ctx* c, const int64_t* rows, int64_t n) {
+  if (!c || (n > 0 && !rows)) return KID_E_ERROR;
+  if (int rc = set_device(c)) return rc;
+  return select_rows(c, rows, n);
 }
 
 int kid_exp_check(kid_ctx* c, const double* x, int64_t n, double* y) {

@@ -179,6 +179,12 @@ struct kid_ctx {
   int64_t r = 0;
   double* src_perm = nullptr;  // m x d, columns [skel | non-skel]
   size_t src_perm_cap = 0;
+  // row-subset view (kid_select_rows): the block's targets restricted to rows of the full list
+  bool sub_active = false;
+  int64_t full_nt = 0;
+  const int64_t* full_tidx = nullptr;
+  int64_t* sub_idx = nullptr;  // composed indices, then the uploaded row list
+  size_t sub_cap = 0;
   std::vector<double> src_host;       // host copies (m x d col-major) of src / src_perm: the fused
   std::vector<double> src_perm_host;  // pass carries them in its kernel parameters
   double* P2 = nullptr;        // r x meff row-major, stride = r-major padded
@@ -234,6 +240,8 @@ int row_norms_dev(kid_ctx* c, double h, double* d_w);
 int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out);
 int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores);
 int eval_rows_dev(kid_ctx* c, double h, const int64_t* d_rows, int64_t count, double* d_Ks);
+int apply_skeleton_dev(kid_ctx* c, double h, const int64_t* skel, int64_t r, const double* q_skel, double* d_u);
+int select_rows(kid_ctx* c, const int64_t* rows, int64_t n);
 int init_device_tables();
 int exp_check_dev(kid_ctx* c, const double* d_x, int64_t n, double* d_y);
 // event pair bracketing the dominant kernel of a pass (no-op unless profiling)

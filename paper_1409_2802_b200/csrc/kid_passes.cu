@@ -640,6 +640,51 @@ __global__ void __launch_bounds__(kNT) k_leverage(LevArgs A) {
 }
 
 // ------------------------------------------------------------------ gather rows
+// apply_skeleton (compress.hpp:309-325): u_i = sum_j exp(-||y_i - x_j||^2 / 2h^2) q_j over the r
+// skeleton points (the far-field matvec). One thread per target, four
+// independent exp chains per step (exp_neg_fast_n), skeleton points (pre-scaled by 1/(sqrt2 h))
+// and charges staged in shared memory [k][j] / [j] (broadcast reads; r padded to a multiple of
+// four with far-away points and zero charges).
+template <int D>
+__global__ void __launch_bounds__(256) k_apply_skel(TargetView tv, int d_rt, const double* __restrict__ xs, int r4,
+                                                    const double* __restrict__ qs, double cscale,
+                                                    double* __restrict__ u) {
+  const int d = D ? D : d_rt;
+  extern __shared__ __align__(16) double sm_apply[];  // d x r4 points, then r4 charges
+  double* s_x = sm_apply;
+  double* s_q = sm_apply + (size_t)d * r4;
+  __shared__ double s_tab[kExpTabWords];
+  stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+  for (int e = threadIdx.x; e < d * r4 + r4; e += blockDim.x) s_x[e] = xs[e];
+  __syncthreads();
+  const double* tabl = s_tab + (threadIdx.x & 31);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tv.nt; i += (int64_t)gridDim.x * blockDim.x) {
+    constexpr int DR = D ? D : 1;
+    double t[DR];
+    if constexpr (D > 0) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[k] = tcoord(tv, i, k) * cscale;
+    }
+    double acc = 0.0;
+    for (int j = 0; j < r4; j += 4) {
+      double kv[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < d; ++k) {
+        const double tk = D ? t[D ? k : 0] : tcoord(tv, i, k) * cscale;
+        const double* xk = s_x + (size_t)k * r4 + j;
+        const double a0 = tk - xk[0], a1 = tk - xk[1], a2 = tk - xk[2], a3 = tk - xk[3];
+        kv[0] = fma(a0, a0, kv[0]);
+        kv[1] = fma(a1, a1, kv[1]);
+        kv[2] = fma(a2, a2, kv[2]);
+        kv[3] = fma(a3, a3, kv[3]);
+      }
+      exp_neg_fast_n<4>(kv, tabl);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc = fma(kv[v], s_q[j + v], acc);  // in skeleton order, as the reference
+    }
+    u[i] = acc;
+  }
+}
+
 __global__ void k_eval_rows(TargetView tv, int d, const double* __restrict__ src, int64_t m, double denom,
                             const int64_t* __restrict__ rows, int64_t count, double* __restrict__ out) {
   const int64_t total = count * m;
@@ -1101,6 +1146,78 @@ int eval_rows_dev(kid_ctx* c, double h, const int64_t* d_rows, int64_t count, do
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)c->sms * 16);
   k_eval_rows<<<blocks, 256, 0, c->stream>>>(view(c), c->d, c->src, c->m, 2.0 * h * h, d_rows, count, d_Ks);
   KID_LAUNCHED(c);
+  return KID_OK;
+}
+
+// u = K(T, S[skel]) q_skel over the current block; x_skel / q_skel from the host (kid_apply_skeleton)
+int apply_skeleton_dev(kid_ctx* c, double h, const int64_t* skel, int64_t r, const double* q_skel, double* d_u) {
+  if (int rc = check_block(c, h)) return rc;
+  const int d = c->d;
+  const int64_t m = c->m;
+  if (r < 0 || r > m) return fail(c, KID_E_RANGE, "apply_skeleton: rank out of range");
+  for (int64_t j = 0; j < r; ++j)
+    if (skel[j] < 0 || skel[j] >= m) return fail(c, KID_E_RANGE, "apply_skeleton: skeleton index out of range");
+  if (c->src_host.size() != (size_t)m * d) return fail(c, KID_E_ERROR, "apply_skeleton: host copy of the sources is stale");
+  if (c->nt == 0) return KID_OK;
+  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
+  const int r4 = std::max(4, ceil_to((int)r, 4));
+  const double cs = std::sqrt(1.0 / (2.0 * h * h));
+  std::vector<double> hx((size_t)d * r4 + r4);
+  for (int k = 0; k < d; ++k)
+    for (int j = 0; j < r4; ++j) hx[(size_t)k * r4 + j] = j < r ? c->src_host[(size_t)k * m + skel[j]] * cs : 1.0e4;
+  for (int j = 0; j < r4; ++j) hx[(size_t)d * r4 + j] = j < r ? q_skel[j] : 0.0;
+  const size_t bytes = sizeof(double) * hx.size();
+  if (bytes > 160 * 1024) return fail(c, KID_E_DIM, "apply_skeleton: skeleton too large for shared memory");
+  double* d_x = (double*)scratch(c, bytes);
+  if (!d_x) return KID_E_OOM;
+  KID_CK(c, cudaMemcpyAsync(d_x, hx.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+  const int blocks = (int)std::min<int64_t>((c->nt + 255) / 256, (int64_t)c->sms * 8);
+#define LAUNCH(DD)                                                                                  \
+  {                                                                                                 \
+    cudaFuncSetAttribute(k_apply_skel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); \
+    k_apply_skel<DD><<<blocks, 256, bytes, c->stream>>>(view(c), d, d_x, r4, d_x + (size_t)d * r4, cs, d_u); \
+  }
+  prof_begin(c);
+  KID_DISPATCH_D(d, LAUNCH)
+  prof_end(c);
+#undef LAUNCH
+  KID_LAUNCHED(c);
+  return KID_OK;
+}
+
+// Row-subset view for mc_error (compress.hpp:279-305): the block's targets become
+// rows[0..n) of the full target list (indices composed on the device); n < 0 restores it.
+__global__ void k_compose_rows(const int64_t* __restrict__ base_idx, const int64_t* __restrict__ rows, int64_t n,
+                               int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = base_idx ? base_idx[rows[i]] : rows[i];
+}
+
+int select_rows(kid_ctx* c, const int64_t* rows, int64_t n) {
+  if (!c->sub_active && n < 0) return KID_OK;
+  if (!c->sub_active) {  // save the full view
+    c->full_nt = c->nt;
+    c->full_tidx = c->tidx;
+  }
+  if (n < 0) {
+    c->nt = c->full_nt;
+    c->tidx = c->full_tidx;
+    c->sub_active = false;
+    return KID_OK;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (rows[i] < 0 || rows[i] >= c->full_nt) return fail(c, KID_E_RANGE, "select_rows: row index out of range");
+  if (ensure(c, (void**)&c->sub_idx, &c->sub_cap, sizeof(int64_t) * 2 * std::max<int64_t>(n, 1))) return KID_E_OOM;
+  int64_t* d_rows = c->sub_idx + std::max<int64_t>(n, 1);
+  if (n) {
+    KID_CK(c, cudaMemcpyAsync(d_rows, rows, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    k_compose_rows<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>(c->full_tidx, d_rows, n,
+                                                                                               c->sub_idx);
+    KID_LAUNCHED(c);
+  }
+  c->nt = n;
+  c->tidx = c->sub_idx;
+  c->sub_active = true;
   return KID_OK;
 }
 

@@ -394,6 +394,7 @@ int split_finish(kid_ctx* c, const int64_t* src_idx_h, int64_t n, const double* 
   c->nt = nt;
   c->m = n;
   c->r = 0;
+  c->sub_active = false;
   *n_targets_out = nt;
   return KID_OK;
 }

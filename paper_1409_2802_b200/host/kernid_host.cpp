@@ -673,6 +673,49 @@ std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, 
   return {std::move(id), rep};
 }
 
+std::vector<double> mc_error(const KernelBlock& K, const IDFactorization& id, double s_mc, int n_mc,
+                             std::uint64_t seed) {
+  if (!(s_mc > 0.0 && s_mc <= 1.0)) throw RangeError("mc_error: requires s_mc in (0, 1]");
+  if (n_mc < 1) throw RangeError("mc_error: requires n_mc >= 1");
+  kid_ctx* c = K.device().ctx();
+  const int64_t m = K.cols(), r = id.rank;
+  SamplingScheme bern;
+  bern.kind = SchemeKind::Bernoulli;
+  SampleContext ctx;
+  ctx.m = K.rows();
+  std::vector<double> estimates;
+  estimates.reserve(static_cast<size_t>(n_mc));
+  for (int rep = 0; rep < n_mc; ++rep) {
+    RowSample rows = sample_rows(bern, ctx, s_mc, derive_seed(seed, static_cast<std::uint64_t>(rep)));
+    if (rows.indices.empty()) rows = sample_rows(bern, ctx, s_mc, derive_seed(seed, static_cast<std::uint64_t>(rep), 1));
+    if (rows.indices.empty()) throw Error("mc_error: Bernoulli draw empty twice; s_mc is too small for this matrix");
+    K.device().check(kid_select_rows(c, rows.indices.data(), static_cast<int64_t>(rows.indices.size())));
+    Matrix DtD(m, m), KtK(m, m);
+    double sd = 0.0, sk = 0.0;
+    const int rc = kid_recon_error(c, K.spec().h, id.skeleton.data(), r, r ? id.projection.data() : nullptr,
+                                   KID_RECON_DTD | KID_RECON_KTK, &sd, &sk, DtD.data(), KtK.data());
+    K.device().check(kid_select_rows(c, nullptr, -1));  // the full block again
+    K.device().check(rc);
+    std::vector<double> ed, ek;
+    sym_eig(DtD, ed, nullptr);
+    sym_eig(KtK, ek, nullptr);
+    const double num = std::sqrt(std::max(ed.empty() ? 0.0 : ed[0], 0.0));
+    const double den = std::sqrt(std::max(ek.empty() ? 0.0 : ek[0], 0.0));
+    estimates.push_back(den > 0.0 ? num / den : (num > 0.0 ? std::numeric_limits<double>::infinity() : 0.0));
+  }
+  return estimates;
+}
+
+std::vector<double> apply_skeleton(const KernelBlock& K, const IDFactorization& id, const std::vector<double>& q) {
+  if (static_cast<int64_t>(q.size()) != id.projection.cols)
+    throw DimensionError("apply_skeleton: charge count disagrees with the projection width");
+  std::vector<double> u(static_cast<size_t>(std::max<int64_t>(K.rows(), 1)));
+  K.device().check(kid_apply_skeleton(K.device().ctx(), K.spec().h, id.skeleton.data(), id.rank,
+                                      id.rank ? id.projection.data() : nullptr, q.data(), u.data()));
+  u.resize(static_cast<size_t>(K.rows()));
+  return u;
+}
+
 // ------------------------------------------------------------------ harness
 std::string format_double(double v) {
   char buf[64];
@@ -1009,6 +1052,40 @@ int kidh_compress_trial(int32_t device, int32_t d, int64_t N, int64_t n, double 
     *rel_error = rep.rel_error;
     *rel_error_fro = rep.rel_error_fro;
     std::memcpy(skel_out, id.skeleton.data(), sizeof(int64_t) * id.skeleton.size());
+  });
+}
+
+// One compress trial (as kidh_compress_trial, uniform sampling) followed by the 8(f) passes on
+// its ID: mc_error (n_mc estimates) and apply_skeleton with charges q (m) -> u (n_targets).
+int kidh_trial_next_rows(int32_t device, int32_t d, int64_t N, int64_t n, double xi, double h_value,
+                         uint64_t data_seed, double s, uint64_t sample_seed, double eps, double s_mc, int32_t n_mc,
+                         uint64_t mc_seed, const double* q, int64_t* n_targets, int64_t* rank, int64_t* skel_out,
+                         double* P_out, double* mc_out, double* u_out, int64_t u_cap) {
+  return guard([&] {
+    Device dev(device);
+    const PointSet points = gen_normal(d, N, derive_seed(data_seed, 0xDA7A));
+    Rng crng(derive_seed(data_seed, 0xCE));
+    const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(N)));
+    std::vector<double> center(static_cast<size_t>(d));
+    for (int k = 0; k < d; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+    const SourceTargetSplit split = split_sources_targets(dev, points, center, n, xi);
+    const KernelBlock K(dev, KernelSpec::gaussian(h_value * silverman_bandwidth(d, N)), points, split);
+    *n_targets = K.rows();
+    SampleContext ctx;
+    ctx.m = K.rows();
+    const RowSample sample = sample_rows(SamplingScheme{}, ctx, s, sample_seed);
+    auto [id, rep] = compress_id(K, sample, RankRule::from_eps(eps));
+    *rank = rep.rank;
+    std::memcpy(skel_out, id.skeleton.data(), sizeof(int64_t) * id.skeleton.size());
+    if (rep.rank) std::memcpy(P_out, id.projection.data(), sizeof(double) * id.projection.a.size());
+    if (rep.rank == 0) {  // the zero-rank ID still reconstructs K as 0
+      id.projection = Matrix(0, K.cols());
+    }
+    const std::vector<double> est = mc_error(K, id, s_mc, n_mc, mc_seed);
+    std::memcpy(mc_out, est.data(), sizeof(double) * est.size());
+    const std::vector<double> u = apply_skeleton(K, id, std::vector<double>(q, q + K.cols()));
+    if (static_cast<int64_t>(u.size()) > u_cap) throw RangeError("kidh_trial_next_rows: u buffer too small");
+    std::memcpy(u_out, u.data(), sizeof(double) * u.size());
   });
 }
 

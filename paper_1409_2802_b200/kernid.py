@@ -43,6 +43,8 @@ def host_lib():
         L.kidh_sym_eig.argtypes = [_dp, i64, _dp, C.c_void_p]
         L.kidh_draw.argtypes = [i32, i32, i64, C.c_void_p, dbl, u64, _ip, P(i64)]
         L.kidh_kernel_rows.argtypes = [_dp, i64, i32, _ip, _ip, i64, _ip, i64, dbl, _dp]
+        L.kidh_trial_next_rows.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, dbl, i32, u64, _dp,
+                                           P(i64), P(i64), _ip, _dp, _dp, _dp, i64]
         L.kidh_compress_trial.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, i32, i64, dbl, u64, dbl, P(i64), P(i64),
                                           P(dbl), P(dbl), _ip, _ip, P(i64)]
         L.kidh_run_experiment.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, i64, _dp, i32, dbl, i32, u64, C.c_char_p]
@@ -153,6 +155,23 @@ def compress_trial(d, N, n, xi, data_seed, scheme, s, sample_seed, eps, h_value=
                                        C.byref(nt), C.byref(rank), C.byref(rel), C.byref(relf), skel, sample,
                                        C.byref(cnt)), "compress_trial")
     return TrialResult(nt.value, rank.value, rel.value, relf.value, skel[: rank.value].copy(), sample[: cnt.value].copy())
+
+
+def trial_next_rows(d, N, n, xi, data_seed, s, sample_seed, eps, s_mc, n_mc, mc_seed, q, h_value=1.0, device=0):
+    """A uniform-sampling compress trial through the C++ mirror, then mc_error (compress.hpp:279-305)
+    and apply_skeleton (compress.hpp:309-325) on its ID. Returns (n_targets, rank, skeleton, P
+    (rank x n), mc estimates, u)."""
+    nt, rank = C.c_int64(), C.c_int64()
+    skel = np.zeros(n, np.int64)
+    P = np.zeros(n * n)
+    mc = np.zeros(n_mc)
+    u = np.zeros(N)
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    _ck(host_lib().kidh_trial_next_rows(device, d, N, n, xi, h_value, data_seed, s, sample_seed, eps, s_mc, n_mc,
+                                        mc_seed, q, C.byref(nt), C.byref(rank), skel, P, mc, u, N), "trial_next_rows")
+    r = rank.value
+    return (nt.value, r, skel[:r].copy(), P[: r * n].reshape(n, r).T.copy() if r else np.zeros((0, n)), mc,
+            u[: nt.value].copy())
 
 
 def run_experiment(path: str, d, N, n, xi, scheme, s_grid, eps, trials=1, seed=1, h_value=1.0, lev_rank=0, device=0):

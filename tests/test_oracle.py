@@ -381,3 +381,35 @@ def test_gaussian_instance_error_and_norm_paths(oracle):  # :119-141 fixture (d=
     assert math.sqrt(lam_d / lam_k) == pytest.approx(res.rel_error, rel=1e-8)
     assert sd == pytest.approx(np.sum(D * D), rel=1e-12)
     assert sk == pytest.approx(np.sum(K * K), rel=1e-12)
+
+
+# ---------------------------------------------------------------- SURVEY.md 8(f) rows
+def test_oracle_bernoulli_draw(oracle):
+    """Bernoulli (sampling.hpp:183-188): i kept iff uniform01 < s, in row order; s outside (0, 1]
+    is a RangeError."""
+    seed = oracle.derive_seed(4, 2, 0)
+    got = oracle.sample_rows(oracle.SCHEME_BERNOULLI, 500, 0.3, seed)
+    _, unif, _, _ = oracle.rng_dump(seed, 500)
+    assert np.array_equal(got, np.nonzero(unif < 0.3)[0])
+    assert oracle.sample_rows(oracle.SCHEME_BERNOULLI, 50, 1.0, seed).size == 50
+    with pytest.raises(oracle.OracleError):
+        oracle.sample_rows(oracle.SCHEME_BERNOULLI, 50, 0.0, seed)
+
+
+def test_oracle_apply_skeleton_and_errors(oracle):
+    """apply_skeleton equals K[:, skel] (P q); mc_error with s_mc = 1 equals the full relative
+    error; the SVD-path numerator equals ||K V V^T - K|| (compress.hpp:243-325)."""
+    t = oracle.prepare_trial(2, 3000, 30, 2.0, oracle.derive_seed(1, 0, 0))
+    K = oracle.kernel_matrix(t.targets, t.sources, t.h)
+    rows = oracle.sample_rows(oracle.SCHEME_UNIFORM, K.shape[0], 0.1, 3)
+    res = oracle.compress_id(K, rows, eps=1e-4)
+    q = np.linspace(-1.0, 1.0, K.shape[1])
+    u = oracle.apply_skeleton(t.targets, t.sources[res.skeleton], t.h, res.P, q)
+    assert np.allclose(u, K[:, res.skeleton] @ (res.P @ q), rtol=1e-13, atol=1e-15)
+    est = oracle.mc_error(K, res.skeleton, res.P, 1.0, 2, 7)
+    assert np.allclose(est, res.rel_error, rtol=1e-12)
+    _, _, Vt = np.linalg.svd(K[rows], full_matrices=True)
+    Vr = np.ascontiguousarray(Vt.T[:, : res.rank])
+    assert oracle.svd_error_norm(K, Vr) == pytest.approx(np.linalg.norm(K @ Vr @ Vr.T - K, 2), rel=1e-12)
+    with pytest.raises(oracle.OracleError):
+        oracle.mc_error(K, res.skeleton, res.P, 1.5, 2, 7)
