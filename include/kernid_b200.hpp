@@ -106,6 +106,10 @@ struct SourceTargetSplit {
 SourceTargetSplit split_sources_targets(Device& dev, const PointSet& ps, const std::vector<double>& x_c,
                                         int64_t n, double xi);
 
+struct RightFactor {  // lowrank.hpp:43-46
+  std::vector<double> singular_values;  // min(rows, cols), nonincreasing
+  Matrix V;                             // cols x cols: the reference's thin V, completed to a basis
+};
 // The device-resident K(T, S) of the last split (replaces the dense MatrixXd K).
 class KernelBlock {
  public:
@@ -119,6 +123,11 @@ class KernelBlock {
   std::vector<double> row_norms() const;        // sampling.hpp:193 (device)
   Matrix gram(double* sumsq = nullptr) const;   // K^T K (device)
   double spectral_norm() const;                 // ||K||_2 = sqrt(lambda_max(K^T K))
+  // right_factor(K) / singular_values(K) of the full block (lowrank.hpp:70-90): Householder TSQR
+  // on the device (kid_tsqr_r) + a Jacobi SVD of the m x m factor for m <= 128 -- every sigma
+  // to ~u sigma_1; the Gram route (sqrt(eig(K^T K)), ~sqrt(u) sigma_1 floor) above that.
+  RightFactor right_factor() const;
+  std::vector<double> singular_values() const { return right_factor().singular_values; }
 
  private:
   Device* dev_;
@@ -137,6 +146,7 @@ struct LeverageScores {
   std::vector<double> scores;
   bool degenerate_gap = false;
 };
+RightFactor right_factor(const Matrix& A);                                  // lowrank.hpp:81-90
 std::vector<double> singular_values(const Matrix& A);                       // lowrank.hpp:70-77
 int64_t epsilon_rank(const std::vector<double>& sv, double eps,
                      std::optional<double> reference_sigma1 = std::nullopt);  // :117-126
@@ -210,6 +220,10 @@ double reconstruction_bound(int64_t m, int64_t s_count, double eps, double sigma
 std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, const RowSample& sample,
                                                           const RankRule& rule, const CompressOptions& opts = {});
 
+// compress.hpp:219-273: right singular basis V_r of the sample; rel_error = ||K - K V_r V_r^T||_2 / ||K||_2
+// with the error pass on the device (kid_proj_gram over V_perp; the difference is never formed).
+std::pair<Matrix, CompressionReport> compress_svd(const KernelBlock& K, const RowSample& sample, const RankRule& rule,
+                                                  const CompressOptions& opts = {});
 // compress.hpp:279-305 for the ID reconstruction (khat_row(i) = K[i, skel] P), on the device:
 // each repetition draws Bernoulli(s_mc) rows with the reference seeds, restricts the block to
 // them (kid_select_rows) and takes both spectral norms through the Gram route.

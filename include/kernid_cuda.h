@@ -112,6 +112,26 @@ int kid_recon_error(kid_ctx* ctx, double h, const int64_t* skel, int64_t r, cons
 int kid_recon_prepare(kid_ctx* ctx, const int64_t* skel, int64_t r, const double* P);
 int kid_recon_error_dev(kid_ctx* ctx, double h, uint32_t flags, double* d_out);
 
+/* ---- TSQR: the stable spectrum of the full K (lowrank.hpp:56-90 right_factor / singular_values
+ * of K; harness.hpp:176-184 full_sv) ----
+ * R (m x m col-major, upper triangular, m <= 128) with R^T R = K^T K by Householder TSQR over all
+ * targets: the singular values / right singular vectors of R are those of K, including the ones
+ * below sqrt(u) sigma_1 that the Gram route (kid_gram) cannot resolve. R is unique up to row
+ * signs. kid_tsqr_combine folds `count` stacked factors (m x m each, host) into one (the
+ * per-rank factors of a sharded block). */
+int kid_tsqr_r(kid_ctx* ctx, double h, double* R);
+int kid_tsqr_r_dev(kid_ctx* ctx, double h, double* d_R);
+int kid_tsqr_combine(kid_ctx* ctx, const double* Rs, int64_t count, int64_t m, double* R);
+
+/* ---- projected Gram: the compress_svd error pass (compress.hpp:243-262) ----
+ * D = K C for an m x n coefficient matrix C (col-major, 1 <= n <= m), never materialised.
+ * Outputs ||D||_F^2, ||K||_F^2 and D^T D (n x n col-major, nullable). With C = V_perp, an
+ * orthonormal basis of the complement of V_r, ||K - K V_r V_r^T||_2 = sqrt(lambda_max(D^T D)).
+ * The device variant takes d_C (device) and writes d_out = [||D||_F^2, ||K||_F^2, D^T D]. */
+int kid_proj_gram(kid_ctx* ctx, double h, const double* C, int64_t n, double* sumsq_D, double* sumsq_K,
+                  double* DtD);
+int kid_proj_gram_dev(kid_ctx* ctx, double h, const double* d_C, int64_t n, double* d_out);
+
 /* ---- gather_rows of K on the device (compress.hpp:130-137): Ks (count x m col-major) ---- */
 int kid_eval_rows(kid_ctx* ctx, double h, const int64_t* rows, int64_t count, double* Ks_out);
 

@@ -80,6 +80,11 @@ def cuda_lib():
         L.kid_recon_prepare.argtypes = [vp, _ip, i64, _dp]
         L.kid_recon_error_dev.argtypes = [vp, dbl, u32, vp]
         L.kid_eval_rows.argtypes = [vp, dbl, _ip, i64, _dp]
+        L.kid_tsqr_r.argtypes = [vp, dbl, _dp]
+        L.kid_tsqr_r_dev.argtypes = [vp, dbl, vp]
+        L.kid_tsqr_combine.argtypes = [vp, _dp, i64, i64, _dp]
+        L.kid_proj_gram.argtypes = [vp, dbl, _dp, i64, P(dbl), P(dbl), vp]
+        L.kid_proj_gram_dev.argtypes = [vp, dbl, vp, i64, vp]
         L.kid_apply_skeleton.argtypes = [vp, dbl, _ip, i64, _dp, _dp, _dp]
         L.kid_apply_skeleton_dev.argtypes = [vp, dbl, _ip, i64, _dp, vp]
         L.kid_select_rows.argtypes = [vp, vp, i64]
@@ -272,6 +277,34 @@ class Device:
                                         KtK.ctypes.data if KtK is not None else None), "kid_recon_error")
         return (sd.value, sk.value, DtD.reshape(m, m).T.copy() if DtD is not None else None,
                 KtK.reshape(m, m).T.copy() if KtK is not None else None)
+
+    def tsqr_r(self, h: float) -> np.ndarray:
+        """Upper-triangular R with R^T R = K^T K (kid_tsqr_r, Householder TSQR over all targets)."""
+        R = np.zeros(max(self.m * self.m, 1))
+        self._ck(self.L.kid_tsqr_r(self.h, h, R), "kid_tsqr_r")
+        return R[: self.m * self.m].reshape(self.m, self.m).T.copy()
+
+    def tsqr_combine(self, Rs) -> np.ndarray:
+        """Fold stacked m x m factors into one (kid_tsqr_combine)."""
+        Rs = [np.asarray(R, dtype=np.float64) for R in Rs]
+        m = Rs[0].shape[0]
+        flat = np.concatenate([_colmajor(R) for R in Rs])
+        out = np.zeros(m * m)
+        self._ck(self.L.kid_tsqr_combine(self.h, flat, len(Rs), m, out), "kid_tsqr_combine")
+        return out.reshape(m, m).T.copy()
+
+    def proj_gram(self, h: float, Cm: np.ndarray):
+        """(||K C||_F^2, ||K||_F^2, (K C)^T (K C)) for an m x n coefficient matrix C
+        (kid_proj_gram: the compress_svd error pass with C = V_perp)."""
+        n = Cm.shape[1]
+        sd, sk = C.c_double(), C.c_double()
+        G = np.zeros(n * n)
+        self._ck(self.L.kid_proj_gram(self.h, h, _colmajor(Cm), n, C.byref(sd), C.byref(sk), G.ctypes.data),
+                 "kid_proj_gram")
+        return sd.value, sk.value, G.reshape(n, n).T.copy()
+
+    def proj_gram_dev(self, h: float, d_C: int, n: int, d_out: int):
+        self._ck(self.L.kid_proj_gram_dev(self.h, h, d_C, n, d_out), "kid_proj_gram_dev")
 
     def apply_skeleton(self, h: float, skel, P: np.ndarray, q) -> np.ndarray:
         """u = K(T, S[skel]) (P q) over the block's targets (kid_apply_skeleton)."""

@@ -327,6 +327,64 @@ int kid_gram(kid_ctx* c, double h, double* G_out, double* sumsq_K_out) {
   return KID_OK;
 }
 
+int kid_tsqr_r(kid_ctx* c, double h, double* R) {
+  if (!c || !R) return KID_E_ERROR;
+  if (int rc = set_device(c)) return rc;
+  const int64_t m = c->m;
+  double* d_R = out_buffer(c, std::max<int64_t>(m * m, 1));
+  if (!d_R) return KID_E_OOM;
+  if (int rc = tsqr_dev(c, h, nullptr, 0, m, d_R)) return rc;
+  KID_CK(c, cudaMemcpyAsync(R, d_R, sizeof(double) * m * m, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  return KID_OK;
+}
+
+int kid_tsqr_r_dev(kid_ctx* c, double h, double* d_R) {
+  if (!c || !d_R) return KID_E_ERROR;
+  if (int rc = set_device(c)) return rc;
+  return tsqr_dev(c, h, nullptr, 0, c->m, d_R);
+}
+
+int kid_tsqr_combine(kid_ctx* c, const double* Rs, int64_t count, int64_t m, double* R) {
+  if (!c || !Rs || !R) return KID_E_ERROR;
+  if (count < 1 || m < 1) return fail(c, KID_E_RANGE, "tsqr_combine: requires count >= 1 and m >= 1");
+  if (int rc = set_device(c)) return rc;
+  double* buf = out_buffer(c, (size_t)(count + 1) * m * m);
+  if (!buf) return KID_E_OOM;
+  KID_CK(c, cudaMemcpyAsync(buf, Rs, sizeof(double) * count * m * m, cudaMemcpyHostToDevice, c->stream));
+  double* d_R = buf + (size_t)count * m * m;
+  if (int rc = tsqr_dev(c, 0.0, buf, count, m, d_R)) return rc;
+  KID_CK(c, cudaMemcpyAsync(R, d_R, sizeof(double) * m * m, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  return KID_OK;
+}
+
+int kid_proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n, double* d_out) {
+  if (!c || !d_C || !d_out) return KID_E_ERROR;
+  if (int rc = set_device(c)) return rc;
+  return proj_gram_dev(c, h, d_C, n, d_out);
+}
+
+int kid_proj_gram(kid_ctx* c, double h, const double* C, int64_t n, double* sumsq_D, double* sumsq_K, double* DtD) {
+  if (!c || !C || !sumsq_D || !sumsq_K) return KID_E_ERROR;
+  if (int rc = set_device(c)) return rc;
+  const int64_t m = c->m;
+  if (n < 1 || n > m) return fail(c, KID_E_RANGE, "proj_gram: requires 1 <= n <= m");
+  double* buf = out_buffer(c, m * n + 2 + n * n);
+  if (!buf) return KID_E_OOM;
+  double* d_C = buf;
+  double* d_out = buf + m * n;
+  KID_CK(c, cudaMemcpyAsync(d_C, C, sizeof(double) * m * n, cudaMemcpyHostToDevice, c->stream));
+  if (int rc = proj_gram_dev(c, h, d_C, n, d_out)) return rc;
+  double head[2];
+  KID_CK(c, cudaMemcpyAsync(head, d_out, sizeof(head), cudaMemcpyDeviceToHost, c->stream));
+  if (DtD) KID_CK(c, cudaMemcpyAsync(DtD, d_out + 2, sizeof(double) * n * n, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  *sumsq_D = head[0];
+  *sumsq_K = head[1];
+  return KID_OK;
+}
+
 int kid_leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores) {
   if (!c || !d_W || !d_scores) return KID_E_ERROR;
   return leverage_dev(c, h, d_W, r, d_scores);

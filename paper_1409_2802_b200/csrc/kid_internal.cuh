@@ -239,6 +239,8 @@ int split_finish(kid_ctx* c, const int64_t* src_idx_h, int64_t n, const double* 
 int row_norms_dev(kid_ctx* c, double h, double* d_w);
 int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out);
 int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores);
+int tsqr_dev(kid_ctx* c, double h, const double* d_Rin, int64_t nR, int64_t m, double* d_R);
+int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n, double* d_out);
 int eval_rows_dev(kid_ctx* c, double h, const int64_t* d_rows, int64_t count, double* d_Ks);
 int apply_skeleton_dev(kid_ctx* c, double h, const int64_t* skel, int64_t r, const double* q_skel, double* d_u);
 int select_rows(kid_ctx* c, const int64_t* rows, int64_t n);

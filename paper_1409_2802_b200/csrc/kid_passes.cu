@@ -639,6 +639,334 @@ __global__ void __launch_bounds__(kNT) k_leverage(LevArgs A) {
   }
 }
 
+// ------------------------------------------------------------------ projected Gram
+// G += (K C)^T (K C) for an arbitrary m x n coefficient matrix C, ||K C||_F^2 and ||K||_F^2.
+// The compress_svd error pass (compress.hpp:243-262): with C = V_perp, an
+// orthonormal basis of the complement of the sample's right singular vectors V_r,
+// ||K - K V_r V_r^T||_2 = ||K V_perp||_2 = sqrt(lambda_max(G)), so the N_T x m difference the
+// reference materialises and QR-factors is never formed. Per 32-target tile: K(tile, S) by exp into
+// shared memory ([j][t]), D = K C on DMMA ([col][t]), G += D^T D on DMMA with the upper-triangular
+// 8x8 blocks of G register-resident across the worker's contiguous chunk of tiles.
+// Two warp groups ping-pong on separate K / D buffers (C shared), so one group's exps (DFMA)
+// overlap the other's DMMAs; group-local named barriers, no CTA-wide sync in the loop.
+struct ProjArgs {
+  TargetView tv;
+  int d, m, n;
+  double cscale;
+  const double* src;  // m x d col-major (device, unscaled)
+  const double* C;    // m x n col-major (device)
+  int64_t ntiles;
+  int nworkers;       // gridDim.x * kPG
+  double* partial;    // [nworkers][LG][LG]
+  int LG;             // ceil8(n)
+  double* partial_sk; // [nworkers] sum K^2, then [nworkers] tr(D^T D)
+};
+constexpr int kPG = 2, kPW = 8, kPT = kPG * kPW * 32;
+constexpr int kPMaxBlk = 17;  // SYRK blocks per warp: n <= 128 -> 136 upper blocks over 8 warps
+
+size_t proj_smem_bytes(int m, int n, int d) {
+  const int m4 = ceil_to(m, 4), n8 = ceil_to(n, 8);
+  return sizeof(double) * ((size_t)m4 * frag_stride(n) + (size_t)d * m4 + (size_t)kPG * (m4 + n8) * kST);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kPT, 1) k_proj_gram(const ProjArgs A) {
+  const int d = D ? D : A.d;
+  const int m = A.m, n = A.n;
+  const int m4 = ceil_to(m, 4), NB = ceil_to(n, 8) / 8, n8 = NB * 8, SC = frag_stride(n);
+  const int nblk = NB * (NB + 1) / 2;
+  extern __shared__ __align__(16) double sm_pg[];
+  double* sC = sm_pg;                         // m4 x SC row-major
+  double* s_src = sC + (size_t)m4 * SC;       // d x m4 scaled sources (pad: far away)
+  __shared__ double s_tab[kExpTabWords];
+  __shared__ short2 s_blk[kPW * kPMaxBlk];
+  __shared__ double red_sk[kPG][kPW], red_tr[kPG][kPW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp / kPW, gw = warp % kPW;
+  double* sK = s_src + (size_t)d * m4 + (size_t)grp * (m4 + n8) * kST;  // [j][t], m4 x kST
+  double* sD = sK + (size_t)m4 * kST;                                     // [col][t], n8 x kST
+  stage_exp_table(s_tab, tid, kPT);
+  for (int e = tid; e < m4 * SC; e += kPT) {
+    const int j = e / SC, col = e - j * SC;
+    sC[e] = (j < m && col < n) ? A.C[j + (size_t)col * m] : 0.0;
+  }
+  for (int e = tid; e < d * m4; e += kPT) {
+    const int k = e / m4, j = e - k * m4;
+    s_src[e] = j < m ? A.src[j + (size_t)k * m] * A.cscale : 1.0e4;
+  }
+  for (int b = tid; b < nblk; b += kPT) {  // upper-triangular block list, row-major
+    int a = 0, rem = b;
+    while (rem >= NB - a) { rem -= NB - a; ++a; }
+    s_blk[b] = make_short2((short)a, (short)(a + rem));
+  }
+  __syncthreads();
+  const int worker = blockIdx.x * kPG + grp;
+  const int64_t tile_lo = A.ntiles * worker / A.nworkers, tile_hi = A.ntiles * (worker + 1) / A.nworkers;
+  const double* tabl = s_tab + lane;
+  const int bar = 1 + grp, nthr = kPW * 32;
+  double acc[kPMaxBlk][2];
+#pragma unroll
+  for (int q = 0; q < kPMaxBlk; ++q) acc[q][0] = acc[q][1] = 0.0;
+  double sk = 0.0;
+  for (int64_t tile = tile_lo; tile < tile_hi; ++tile) {
+    const int64_t row = tile * kTM + lane;
+    const bool live = row < A.tv.nt;
+    constexpr int DR = D ? D : 1;
+    double t[DR];
+    if constexpr (D > 0) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[k] = live ? tcoord(A.tv, row, k) * A.cscale : 0.0;
+    }
+    // eval: lane = target, four-column groups strided over the group's warps
+    for (int g = gw; g < m4 / 4; g += kPW) {
+      const int j = 4 * g;
+      double kv[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < d; ++k) {
+        const double tk = D ? t[D ? k : 0] : (live ? tcoord(A.tv, row, k) * A.cscale : 0.0);
+        const double* xk = s_src + (size_t)k * m4 + j;
+        const double a0 = tk - xk[0], a1 = tk - xk[1], a2 = tk - xk[2], a3 = tk - xk[3];
+        kv[0] = fma(a0, a0, kv[0]);
+        kv[1] = fma(a1, a1, kv[1]);
+        kv[2] = fma(a2, a2, kv[2]);
+        kv[3] = fma(a3, a3, kv[3]);
+      }
+      exp_neg_fast_n<4>(kv, tabl);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double v = live ? kv[u] : 0.0;  // padding columns are exactly 0 (far-away sources)
+        sK[(j + u) * kST + lane] = v;
+        sk = fma(v, v, sk);
+      }
+    }
+    nbar_sync(bar, nthr);
+    // D = K C: units (column block nb, row half rh), two 8-row blocks per unit share the B fragment
+    for (int u = gw; u < 2 * NB; u += kPW) {
+      const int nb = u >> 1, rh = u & 1;
+      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      const double* pa = sK + (lane & 3) * kST + rh * 16 + (lane >> 2);
+      const double* pb = sC + (lane & 3) * SC + nb * 8 + (lane >> 2);
+      for (int k0 = 0; k0 < m4; k0 += 4) {
+        const double b = pb[k0 * SC];
+        dmma884(c[0][0], c[0][1], pa[k0 * kST], b);
+        dmma884(c[1][0], c[1][1], pa[k0 * kST + 8], b);
+      }
+#pragma unroll
+      for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) sD[(nb * 8 + 2 * (lane & 3) + e) * kST + rh * 16 + rb * 8 + (lane >> 2)] = c[rb][e];
+    }
+    nbar_sync(bar, nthr);
+    // G += D^T D over the tile's 32 targets (8 k-steps)
+#pragma unroll
+    for (int kk = 0; kk < kTM / 4; ++kk) {
+      const int k0 = kk * 4 + (lane & 3);
+#pragma unroll
+      for (int q = 0; q < kPMaxBlk; ++q) {
+        const int bi = gw + kPW * q;
+        if (bi < nblk) {
+          const short2 ab = s_blk[bi];
+          const double fa = sD[(ab.x * 8 + (lane >> 2)) * kST + k0];
+          const double fb = sD[(ab.y * 8 + (lane >> 2)) * kST + k0];
+          dmma884(acc[q][0], acc[q][1], fa, fb);
+        }
+      }
+    }
+  }
+  // per-worker partial: upper blocks at (a8 + row) + (b8 + col) * LG; trace from the diagonal blocks
+  double tr = 0.0;
+  double* P = A.partial + (size_t)worker * A.LG * A.LG;
+#pragma unroll
+  for (int q = 0; q < kPMaxBlk; ++q) {
+    const int bi = gw + kPW * q;
+    if (bi < nblk) {
+      const short2 ab = s_blk[bi];
+      const int x = ab.x * 8 + (lane >> 2);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int y = ab.y * 8 + 2 * (lane & 3) + e;
+        P[x + (size_t)y * A.LG] = acc[q][e];
+        if (x == y) tr += acc[q][e];
+      }
+    }
+  }
+  sk = warp_sum(sk);
+  tr = warp_sum(tr);
+  if (lane == 0) {
+    red_sk[grp][gw] = sk;
+    red_tr[grp][gw] = tr;
+  }
+  nbar_sync(bar, nthr);
+  if (gw == 0 && lane == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int w = 0; w < kPW; ++w) {
+      s0 += red_sk[grp][w];
+      s1 += red_tr[grp][w];
+    }
+    A.partial_sk[worker] = s0;
+    A.partial_sk[A.nworkers + worker] = s1;
+  }
+}
+
+// ------------------------------------------------------------------ TSQR
+// Stable spectrum of the full K (lowrank.hpp:56-90 right_factor / singular_values of K, the
+// `full_sv` of harness.hpp:176-184): the Gram route loses every sigma below
+// ~sqrt(u) sigma_1, Householder QR does not. Each CTA folds its contiguous chunk of 64-row tiles
+// of K into an m x m triangular factor kept in shared memory: per tile, Householder QR of the
+// stacked [R; A] (A = the tile, evaluated in shared memory), whose reflector for column j touches
+// only R[j, :] and A[:, j..] -- one barrier per column, column k of the update owned by warp
+// k mod 16 (its dot product with the reflector is a warp-shuffle reduction over the tile rows).
+// The per-CTA factors are then folded the same way (mode REDUCE: the tile rows come from a stack
+// of upper-triangular factors) until one R remains. R is unique up to row signs; its singular
+// values and right singular vectors are those of K.
+constexpr int kQT = 64;                 // tile rows (two per lane)
+constexpr int kQW = 16, kQThreads = kQW * 32;
+
+struct TsqrArgs {
+  TargetView tv;       // EVAL mode: rows of K(T, S)
+  int d, m;
+  double cscale;
+  const double* src;   // m x d col-major (device, unscaled)
+  const double* Rin;   // REDUCE mode: nR stacked m x m col-major upper factors
+  int64_t nrows;       // rows to fold: nt (EVAL) or nR * m (REDUCE)
+  int64_t ntiles;
+  double* Rout;        // [gridDim.x][m][m] col-major
+};
+
+size_t tsqr_smem_bytes(int m, int d) {
+  const int m4 = ceil_to(m, 4);
+  return sizeof(double) * ((size_t)m * m + (size_t)m4 * kQT + (size_t)d * m4);
+}
+
+template <int D, bool EVAL>
+__global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
+  const int d = D ? D : A.d;
+  const int m = A.m, m4 = ceil_to(m, 4);
+  extern __shared__ __align__(16) double sm_q[];
+  double* sR = sm_q;                         // m x m col-major (upper triangle used)
+  double* sA = sR + (size_t)m * m;           // tile, column-major [k][i], m4 x kQT
+  double* s_src = sA + (size_t)m4 * kQT;     // d x m4 scaled sources (EVAL)
+  __shared__ double s_tab[kExpTabWords];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (EVAL) stage_exp_table(s_tab, tid, kQThreads);
+  for (int e = tid; e < m * m; e += kQThreads) sR[e] = 0.0;
+  if (EVAL)
+    for (int e = tid; e < d * m4; e += kQThreads) {
+      const int k = e / m4, j = e - k * m4;
+      s_src[e] = j < m ? A.src[j + (size_t)k * m] * A.cscale : 1.0e4;
+    }
+  const int64_t t_lo = A.ntiles * blockIdx.x / gridDim.x, t_hi = A.ntiles * (blockIdx.x + 1) / gridDim.x;
+  const double* tabl = s_tab + lane;
+  for (int64_t tile = t_lo; tile < t_hi; ++tile) {
+    __syncthreads();  // previous tile's last column step done (and the staging above)
+    const int64_t row0 = tile * kQT;
+    if (EVAL) {
+      // lane = rows lane and lane + 32; four-column groups strided over the warps
+      constexpr int DR = D ? D : 1;
+      double t[2][DR];
+      bool live[2];
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int64_t row = row0 + lane + 32 * h2;
+        live[h2] = row < A.nrows;
+        if constexpr (D > 0) {
+#pragma unroll
+          for (int k = 0; k < D; ++k) t[h2][k] = live[h2] ? tcoord(A.tv, row, k) * A.cscale : 0.0;
+        }
+      }
+      for (int g = warp; g < m4 / 4; g += kQW) {
+        const int j = 4 * g;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int64_t row = row0 + lane + 32 * h2;
+          double kv[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int k = 0; k < d; ++k) {
+            const double tk = D ? t[h2][D ? k : 0] : (live[h2] ? tcoord(A.tv, row, k) * A.cscale : 0.0);
+            const double* xk = s_src + (size_t)k * m4 + j;
+            const double a0 = tk - xk[0], a1 = tk - xk[1], a2 = tk - xk[2], a3 = tk - xk[3];
+            kv[0] = fma(a0, a0, kv[0]);
+            kv[1] = fma(a1, a1, kv[1]);
+            kv[2] = fma(a2, a2, kv[2]);
+            kv[3] = fma(a3, a3, kv[3]);
+          }
+          exp_neg_fast_n<4>(kv, tabl);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) sA[(j + u) * kQT + lane + 32 * h2] = live[h2] ? kv[u] : 0.0;
+        }
+      }
+    } else {
+      for (int e = tid; e < m * kQT; e += kQThreads) {
+        const int k = e / kQT, i = e - k * kQT;
+        const int64_t gr = row0 + i;
+        double v = 0.0;
+        if (gr < A.nrows) {
+          const int64_t b = gr / m;
+          const int j = (int)(gr - b * m);
+          v = k >= j ? A.Rin[(size_t)b * m * m + j + (size_t)k * m] : 0.0;
+        }
+        sA[e] = v;
+      }
+    }
+    __syncthreads();
+    int pend = -1;      // deferred diagonal write (R[j][j] is read by every warp during step j)
+    double pend_beta = 0.0;
+    for (int j = 0; j < m; ++j) {
+      const double a0 = sA[j * kQT + lane], a1 = sA[j * kQT + lane + 32];
+      const double sig = warp_sum(fma(a0, a0, a1 * a1));
+      const double x0 = sR[j + (size_t)j * m];
+      if (pend >= 0 && warp == (pend % kQW) && lane == 0) sR[pend + (size_t)pend * m] = pend_beta;
+      pend = -1;
+      if (sig == 0.0) continue;  // H_j = I (uniform over the CTA: every warp sees the same column)
+      const double nrm = sqrt(fma(x0, x0, sig));
+      const double beta = x0 >= 0.0 ? -nrm : nrm;
+      const double v0 = x0 - beta;
+      const double tau = -v0 / beta;
+      const double v_lo = a0 / v0, v_hi = a1 / v0;
+      // columns k > j owned by this warp (k mod kQW == warp), two at a time for ILP
+      int k = j + 1 + ((warp - (j + 1)) % kQW + kQW) % kQW;
+      for (; k + kQW < m; k += 2 * kQW) {
+        const int k2 = k + kQW;
+        const double b0 = sA[k * kQT + lane], b1 = sA[k * kQT + lane + 32];
+        const double c0 = sA[k2 * kQT + lane], c1 = sA[k2 * kQT + lane + 32];
+        double dot = fma(v_lo, b0, v_hi * b1), dot2 = fma(v_lo, c0, v_hi * c1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          dot += __shfl_xor_sync(0xffffffffu, dot, o);
+          dot2 += __shfl_xor_sync(0xffffffffu, dot2, o);
+        }
+        const double w = tau * (sR[j + (size_t)k * m] + dot), w2 = tau * (sR[j + (size_t)k2 * m] + dot2);
+        sA[k * kQT + lane] = fma(-w, v_lo, b0);
+        sA[k * kQT + lane + 32] = fma(-w, v_hi, b1);
+        sA[k2 * kQT + lane] = fma(-w2, v_lo, c0);
+        sA[k2 * kQT + lane + 32] = fma(-w2, v_hi, c1);
+        __syncwarp();
+        if (lane == 0) {
+          sR[j + (size_t)k * m] -= w;
+          sR[j + (size_t)k2 * m] -= w2;
+        }
+      }
+      if (k < m) {
+        const double b0 = sA[k * kQT + lane], b1 = sA[k * kQT + lane + 32];
+        const double dot = warp_sum(fma(v_lo, b0, v_hi * b1));
+        const double w = tau * (sR[j + (size_t)k * m] + dot);
+        sA[k * kQT + lane] = fma(-w, v_lo, b0);
+        sA[k * kQT + lane + 32] = fma(-w, v_hi, b1);
+        __syncwarp();
+        if (lane == 0) sR[j + (size_t)k * m] -= w;
+      }
+      pend = j;
+      pend_beta = beta;
+      __syncthreads();
+    }
+    if (pend >= 0 && warp == (pend % kQW) && lane == 0) sR[pend + (size_t)pend * m] = pend_beta;
+  }
+  __syncthreads();
+  double* out = A.Rout + (size_t)blockIdx.x * m * m;
+  for (int e = tid; e < m * m; e += kQThreads) {
+    const int k = e / m, j = e - k * m;
+    out[e] = j <= k ? sR[e] : 0.0;
+  }
+}
+
 // ------------------------------------------------------------------ gather rows
 // apply_skeleton (compress.hpp:309-325): u_i = sum_j exp(-||y_i - x_j||^2 / 2h^2) q_j over the r
 // skeleton points (the far-field matvec). One thread per target, four
@@ -778,36 +1106,68 @@ int row_norms_dev(kid_ctx* c, double h, double* d_w) {
 // transient column-major HBM buffer with the same arithmetic, then D = K_N - K_S P2 is one DGEMM
 // and G += D^T D one DSYRK (cuBLAS, DMMA). ROUND-1 FALLBACK: it materialises K batch-wise,
 // which the fused kernel avoids; DESIGN.md section 8 plans its replacement.
-__global__ void __launch_bounds__(256) k_eval_batch(TargetView tv, int d, const double* __restrict__ src, int m,
+// One thread per target row (coordinates in registers, pre-scaled by 1/(sqrt2 h)), a block of
+// 256 rows x a contiguous range of the m4/4 four-column groups (blockIdx.y); sources staged in
+// shared memory [k][j] (scaled, padding far away -> exactly 0), four exp chains per step; the
+// column-major stores Kb[i + j*B] are coalesced across the warp. ||K||_F^2 partial per block.
+template <int D>
+__global__ void __launch_bounds__(256) k_eval_batch(TargetView tv, int d_rt, const double* __restrict__ src, int m,
                                                     double cscale, int64_t t0, int B, double* __restrict__ Kb,
                                                     double* __restrict__ sk_part) {
+  const int d = D ? D : d_rt;
+  const int m4 = ceil_to(m, 4);
+  extern __shared__ __align__(16) double sm_eb[];  // d x m4 scaled sources
   __shared__ double s_tab[kExpTabWords];
   __shared__ double red[8];
   stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+  for (int e = threadIdx.x; e < d * m4; e += blockDim.x) {
+    const int k = e / m4, j = e - k * m4;
+    sm_eb[e] = j < m ? src[j + (int64_t)k * m] * cscale : 1.0e4;
+  }
   __syncthreads();
+  const double* tabl = s_tab + (threadIdx.x & 31);
+  const int ng = m4 / 4;
+  const int g_lo = (int)((int64_t)ng * blockIdx.y / gridDim.y), g_hi = (int)((int64_t)ng * (blockIdx.y + 1) / gridDim.y);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double sk = 0.0;
-  const int64_t total = (int64_t)B * m;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e % B), j = (int)(e / B);
-    double kv = 0.0;
-    if (t0 + i < tv.nt) {
-      double q = 0.0;
-      for (int k = 0; k < d; ++k) {
-        const double df = tcoord(tv, t0 + i, k) * cscale - src[j + (int64_t)k * m] * cscale;
-        q = fma(df, df, q);
-      }
-      kv = exp_neg_fast(q, s_tab + (threadIdx.x & 31));
+  if (i < B) {
+    const bool live = t0 + i < tv.nt;
+    constexpr int DR = D ? D : 1;
+    double t[DR];
+    if constexpr (D > 0) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[k] = live ? tcoord(tv, t0 + i, k) * cscale : 0.0;
     }
-    Kb[e] = kv;
-    sk = fma(kv, kv, sk);
+    for (int g = g_lo; g < g_hi; ++g) {
+      const int j = 4 * g;
+      double kv[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < d; ++k) {
+        const double tk = D ? t[D ? k : 0] : (live ? tcoord(tv, t0 + i, k) * cscale : 0.0);
+        const double* xk = sm_eb + (size_t)k * m4 + j;
+        const double a0 = tk - xk[0], a1 = tk - xk[1], a2 = tk - xk[2], a3 = tk - xk[3];
+        kv[0] = fma(a0, a0, kv[0]);
+        kv[1] = fma(a1, a1, kv[1]);
+        kv[2] = fma(a2, a2, kv[2]);
+        kv[3] = fma(a3, a3, kv[3]);
+      }
+      exp_neg_fast_n<4>(kv, tabl);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double v = live ? kv[u] : 0.0;
+        if (j + u < m) {
+          Kb[i + (int64_t)(j + u) * B] = v;
+          sk = fma(v, v, sk);
+        }
+      }
+    }
   }
   sk = warp_sum(sk);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sk;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    sk_part[blockIdx.x] = t;
+    double tt = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tt += red[w];
+    sk_part[blockIdx.y * gridDim.x + blockIdx.x] = tt;
   }
 }
 
@@ -836,9 +1196,15 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   cublasSetStream(c->blas, c->stream);
   cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
   const int64_t nt = c->nt;
-  const int B = (int)std::max<int64_t>(1024, std::min<int64_t>(nt, (int64_t)(256ll << 20) / (8ll * m)));
+  // batch of B target rows: a 1 GB transient K buffer (HBM holds 180 GB)
+  const int B = (int)std::max<int64_t>(1024, std::min<int64_t>(nt, (int64_t)(1ll << 30) / (8ll * m)));
   const int64_t nbatch = (nt + B - 1) / B;
-  const int ev_blocks = c->sms * 8;
+  const int ev_rows = (B + 255) / 256;
+  const int ev_cols = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_to(m, 4) / 4, (4ll * c->sms + ev_rows - 1) / ev_rows));
+  const int ev_blocks = ev_rows * ev_cols;
+  const size_t ev_smem = sizeof(double) * (size_t)d * ceil_to(m, 4);
+  if (ev_smem > 160 * 1024) return fail(c, KID_E_DIM, "large-m Gram: m*d too large for shared memory");
+  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   // scratch: K batch (B x m) | G (meff x meff) | P2 col-major (r x meff) | sk partials
   const size_t kb = (size_t)B * m, gb = (size_t)meff * meff, pb = (size_t)std::max<int64_t>(r, 1) * meff;
   char* base = (char*)scratch(c, sizeof(double) * (kb + gb + pb + (size_t)nbatch * ev_blocks + 64));
@@ -863,7 +1229,14 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   for (int64_t b = 0; b < nbatch; ++b) {
     const int64_t t0 = b * (int64_t)B;
     const int rows = (int)std::min<int64_t>(B, nt - t0);
-    k_eval_batch<<<ev_blocks, 256, 0, c->stream>>>(view(c), d, src, m, cscale, t0, rows, Kb, skp + b * ev_blocks);
+#define LAUNCH(DD)                                                                                        \
+  {                                                                                                       \
+    cudaFuncSetAttribute(k_eval_batch<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ev_smem);     \
+    k_eval_batch<DD><<<dim3(ev_rows, ev_cols), 256, ev_smem, c->stream>>>(view(c), d, src, m, cscale, t0, rows, \
+                                                                         Kb, skp + b * ev_blocks);        \
+  }
+    KID_DISPATCH_D(d, LAUNCH)
+#undef LAUNCH
     KID_LAUNCHED(c);
     double* KN = Kb + (size_t)r * rows;  // non-skeleton columns follow the r skeleton columns
     if (r > 0) {
@@ -1101,6 +1474,174 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   k_gram_reduce<<<std::max(1, std::min(c->sms * 2, (meff * meff + 31) / 32)), 1024, 0, c->stream>>>(
       partial, nchunks, LG, meff, partial_sk, nparts, d_out);
   KID_LAUNCHED(c);
+  return KID_OK;
+}
+
+// G = (K C)^T (K C) for a device m x n coefficient matrix C (col-major); d_out = [||K C||_F^2,
+// ||K||_F^2, G (n x n col-major)]. Fused k_proj_gram when its shared-memory footprint fits, else
+// the batched path (K batch in HBM, D = K C by DGEMM, G += D^T D by DSYRK).
+int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n64, double* d_out) {
+  if (int rc = check_block(c, h)) return rc;
+  const int m = (int)c->m, d = c->d, n = (int)n64;
+  if (n < 1 || n > m) return fail(c, KID_E_RANGE, "proj_gram: requires 1 <= n <= m");
+  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
+  const double cscale = std::sqrt(1.0 / (2.0 * h * h));
+  const int LG = ceil_to(n, 8);
+  const size_t smem = proj_smem_bytes(m, n, d);
+  if (LG <= 128 && smem <= 200 * 1024 && !getenv("KID_FORCE_LARGE")) {
+    const int64_t ntiles = (c->nt + kTM - 1) / kTM;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms, (ntiles + kPG - 1) / kPG));
+    const int nworkers = blocks * kPG;
+    char* base = (char*)scratch(c, sizeof(double) * ((size_t)nworkers * LG * LG + 2 * (size_t)nworkers + 8));
+    if (!base) return KID_E_OOM;
+    ProjArgs A;
+    A.tv = view(c);
+    A.d = d;
+    A.m = m;
+    A.n = n;
+    A.cscale = cscale;
+    A.src = c->src;
+    A.C = d_C;
+    A.ntiles = ntiles;
+    A.nworkers = nworkers;
+    A.partial = (double*)base;
+    A.LG = LG;
+    A.partial_sk = A.partial + (size_t)nworkers * LG * LG;
+#define LAUNCH(DD)                                                                                   \
+  {                                                                                                  \
+    cudaFuncSetAttribute(k_proj_gram<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+    k_proj_gram<DD><<<blocks, kPT, smem, c->stream>>>(A);                                            \
+  }
+    prof_begin(c);
+    KID_DISPATCH_D(d, LAUNCH)
+    prof_end(c);
+#undef LAUNCH
+    KID_LAUNCHED(c);
+    k_gram_reduce<<<std::max(1, std::min(c->sms * 2, (n * n + 31) / 32)), 1024, 0, c->stream>>>(
+        A.partial, nworkers, LG, n, A.partial_sk, 1, d_out);
+    KID_LAUNCHED(c);
+    return KID_OK;
+  }
+  // batched path
+  if (!c->blas) {
+    if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return fail(c, KID_E_CUDA, "cublasCreate failed");
+  }
+  cublasSetStream(c->blas, c->stream);
+  cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
+  const int64_t nt = c->nt;
+  const int B = (int)std::max<int64_t>(1024, std::min<int64_t>(nt, (int64_t)(1ll << 30) / (8ll * (m + n))));
+  const int64_t nbatch = std::max<int64_t>(1, (nt + B - 1) / B);
+  const int ev_rows = (B + 255) / 256;
+  const int ev_cols = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_to(m, 4) / 4, (4ll * c->sms + ev_rows - 1) / ev_rows));
+  const int ev_blocks = ev_rows * ev_cols;
+  const size_t ev_smem = sizeof(double) * (size_t)d * ceil_to(m, 4);
+  if (ev_smem > 160 * 1024) return fail(c, KID_E_DIM, "proj_gram: m*d too large for shared memory");
+  char* base = (char*)scratch(c, sizeof(double) * ((size_t)B * (m + n) + (size_t)n * n + (size_t)nbatch * ev_blocks + 64));
+  if (!base) return KID_E_OOM;
+  double* Kb = (double*)base;
+  double* Db = Kb + (size_t)B * m;
+  double* G = Db + (size_t)B * n;
+  double* skp = G + (size_t)n * n;
+  const double one = 1.0, zero = 0.0;
+  if (nt == 0) {
+    KID_CK(c, cudaMemsetAsync(G, 0, sizeof(double) * n * n, c->stream));
+    KID_CK(c, cudaMemsetAsync(skp, 0, sizeof(double) * ev_blocks, c->stream));
+  }
+  prof_begin(c);
+  for (int64_t b = 0; b < nbatch && nt > 0; ++b) {
+    const int64_t t0 = b * (int64_t)B;
+    const int rows = (int)std::min<int64_t>(B, nt - t0);
+#define LAUNCH(DD)                                                                                         \
+  {                                                                                                        \
+    cudaFuncSetAttribute(k_eval_batch<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ev_smem);      \
+    k_eval_batch<DD><<<dim3(ev_rows, ev_cols), 256, ev_smem, c->stream>>>(view(c), d, c->src, m, cscale, t0, \
+                                                                         rows, Kb, skp + b * ev_blocks);   \
+  }
+    KID_DISPATCH_D(d, LAUNCH)
+#undef LAUNCH
+    KID_LAUNCHED(c);
+    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, n, m, &one, Kb, rows, d_C, m, &zero, Db, rows) !=
+        CUBLAS_STATUS_SUCCESS)
+      return fail(c, KID_E_CUDA, "cublasDgemm failed");
+    c->launches++;
+    if (cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, n, rows, &one, Db, rows, b == 0 ? &zero : &one, G, n) !=
+        CUBLAS_STATUS_SUCCESS)
+      return fail(c, KID_E_CUDA, "cublasDsyrk failed");
+    c->launches++;
+  }
+  prof_end(c);
+  const int nsk = nt == 0 ? ev_blocks : (int)(nbatch * ev_blocks);
+  k_large_finish<<<std::max(1, std::min(c->sms * 4, (n * n + 255) / 256)), 256, 0, c->stream>>>(G, n, skp, nsk, d_out);
+  KID_LAUNCHED(c);
+  return KID_OK;
+}
+
+// Upper-triangular R (m x m col-major, device) with R^T R = K^T K, by TSQR over all targets
+// (EVAL level: one CTA per SM over contiguous 64-row tiles; REDUCE levels: groups of up to 8
+// factors folded per CTA until one remains). Rin/nR: optional extra factors to fold in first
+// (kid_tsqr_combine: the factors of other ranks).
+int tsqr_dev(kid_ctx* c, double h, const double* d_Rin, int64_t nR, int64_t m64, double* d_R) {
+  const bool eval = d_Rin == nullptr;
+  if (eval) {
+    if (int rc = check_block(c, h)) return rc;
+  }
+  const int m = eval ? (int)c->m : (int)m64, d = eval ? c->d : 1;
+  if (m < 1) return fail(c, KID_E_RANGE, "tsqr: requires m >= 1");
+  if (m > 128) return fail(c, KID_E_DIM, "tsqr: m > 128 does not fit the shared-memory factor (use the Gram route)");
+  const size_t smem = tsqr_smem_bytes(m, d);
+  if (smem > 200 * 1024) return fail(c, KID_E_DIM, "tsqr: m*d too large for shared memory");
+  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
+  const size_t mm = (size_t)m * m;
+  const int64_t nrows0 = eval ? c->nt : nR * m;
+  const int64_t ntiles0 = (nrows0 + kQT - 1) / kQT;
+  const int blocks0 = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms, ntiles0));
+  // ping-pong factor stacks
+  double* base = (double*)scratch(c, sizeof(double) * mm * (size_t)(2 * blocks0 + 2));
+  if (!base) return KID_E_OOM;
+  double* bufA = base;
+  double* bufB = base + mm * (size_t)(blocks0 + 1);
+  TsqrArgs A;
+  A.tv = eval ? view(c) : TargetView{nullptr, 0, nullptr, 0};
+  A.d = d;
+  A.m = m;
+  A.cscale = std::sqrt(1.0 / (2.0 * h * h));
+  A.src = eval ? c->src : nullptr;
+  A.Rin = d_Rin;
+  A.nrows = nrows0;
+  A.ntiles = ntiles0;
+  A.Rout = bufA;
+  prof_begin(c);
+  if (eval) {
+#define LAUNCH(DD)                                                                                   \
+  {                                                                                                  \
+    cudaFuncSetAttribute(k_tsqr<DD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    k_tsqr<DD, true><<<blocks0, kQThreads, smem, c->stream>>>(A);                                    \
+  }
+    KID_DISPATCH_D(d, LAUNCH)
+#undef LAUNCH
+  } else {
+    cudaFuncSetAttribute(k_tsqr<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_tsqr<1, false><<<blocks0, kQThreads, smem, c->stream>>>(A);
+  }
+  prof_end(c);
+  KID_LAUNCHED(c);
+  int64_t nf = blocks0;
+  double* cur = bufA;
+  double* nxt = bufB;
+  while (nf > 1) {
+    const int64_t groups = (nf + 7) / 8;
+    TsqrArgs Rd = A;
+    Rd.Rin = cur;
+    Rd.nrows = nf * m;
+    Rd.ntiles = (Rd.nrows + kQT - 1) / kQT;
+    Rd.Rout = nxt;
+    cudaFuncSetAttribute(k_tsqr<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_tsqr<1, false><<<(unsigned)groups, kQThreads, smem, c->stream>>>(Rd);
+    KID_LAUNCHED(c);
+    nf = groups;
+    std::swap(cur, nxt);
+  }
+  KID_CK(c, cudaMemcpyAsync(d_R, cur, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
   return KID_OK;
 }
 

@@ -239,6 +239,60 @@ std::vector<double> jacobi_sv(Matrix U) {
   return sv;
 }
 
+// One-sided Jacobi with the accumulated rotations: U V = [u_1 s_1 ...]; singular values
+// (descending, all cols of them) and V (cols x cols, columns in the same order).
+void jacobi_svd_v(Matrix U, std::vector<double>& sv, Matrix& V) {
+  const int64_t n = U.cols, rows = U.rows;
+  V = Matrix(n, n);
+  for (int64_t i = 0; i < n; ++i) V(i, i) = 1.0;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    int64_t rotated = 0;
+    for (int64_t p = 0; p + 1 < n; ++p)
+      for (int64_t q = p + 1; q < n; ++q) {
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int64_t i = 0; i < rows; ++i) {
+          a += U(i, p) * U(i, p);
+          b += U(i, q) * U(i, q);
+          g += U(i, p) * U(i, q);
+        }
+        if (g == 0.0 || std::fabs(g) <= 1e-15 * std::sqrt(a) * std::sqrt(b)) continue;
+        ++rotated;
+        const double zeta = (b - a) / (2.0 * g);
+        const double t = std::fabs(zeta) > 1e150 ? 0.5 / zeta
+                                                   : (zeta >= 0.0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), s = c * t;
+        for (int64_t i = 0; i < rows; ++i) {
+          const double x = U(i, p), y = U(i, q);
+          U(i, p) = c * x - s * y;
+          U(i, q) = s * x + c * y;
+        }
+        for (int64_t i = 0; i < n; ++i) {
+          const double x = V(i, p), y = V(i, q);
+          V(i, p) = c * x - s * y;
+          V(i, q) = s * x + c * y;
+        }
+      }
+    if (!rotated) break;
+  }
+  std::vector<double> nrm(static_cast<size_t>(n));
+  for (int64_t j = 0; j < n; ++j) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < rows; ++i) acc += U(i, j) * U(i, j);
+    nrm[static_cast<size_t>(j)] = std::sqrt(acc);
+  }
+  std::vector<int64_t> order(static_cast<size_t>(n));
+  std::iota(order.begin(), order.end(), int64_t{0});
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t x, int64_t y) { return nrm[static_cast<size_t>(x)] > nrm[static_cast<size_t>(y)]; });
+  Matrix Vs(n, n);
+  sv.resize(static_cast<size_t>(n));
+  for (int64_t j = 0; j < n; ++j) {
+    sv[static_cast<size_t>(j)] = nrm[static_cast<size_t>(order[static_cast<size_t>(j)])];
+    for (int64_t i = 0; i < n; ++i) Vs(i, j) = V(i, order[static_cast<size_t>(j)]);
+  }
+  V = std::move(Vs);
+}
+
 Matrix transpose(const Matrix& A) {
   Matrix T(A.cols, A.rows);
   for (int64_t j = 0; j < A.cols; ++j)
@@ -252,6 +306,33 @@ std::vector<double> singular_values(const Matrix& A) {
   if (A.rows == 0 || A.cols == 0) throw RangeError("singular_values: empty matrix");
   if (A.rows >= A.cols) return jacobi_sv(qr_r(A));
   return jacobi_sv(qr_r(transpose(A)));
+}
+
+RightFactor right_factor(const Matrix& A) {
+  if (A.rows == 0 || A.cols == 0) throw RangeError("right_factor: empty matrix");
+  RightFactor rf;
+  // tall: V from the SVD of the triangular factor (lowrank.hpp:81-86); wide: the full V of A,
+  // whose trailing columns complete the thin V of the reference to an orthonormal basis
+  jacobi_svd_v(A.rows >= A.cols ? qr_r(A) : A, rf.singular_values, rf.V);
+  rf.singular_values.resize(static_cast<size_t>(std::min(A.rows, A.cols)));
+  return rf;
+}
+
+RightFactor KernelBlock::right_factor() const {
+  const int64_t m = cols();
+  RightFactor rf;
+  if (m <= 128) {
+    Matrix R(m, m);
+    dev_->check(kid_tsqr_r(dev_->ctx(), spec_.h, R.data()));
+    jacobi_svd_v(R, rf.singular_values, rf.V);
+  } else {
+    std::vector<double> ev;
+    sym_eig(gram(), ev, &rf.V);
+    rf.singular_values.resize(ev.size());
+    for (size_t i = 0; i < ev.size(); ++i) rf.singular_values[i] = std::sqrt(std::max(ev[i], 0.0));
+  }
+  rf.singular_values.resize(static_cast<size_t>(std::min(rows(), m)));
+  return rf;
 }
 
 int64_t epsilon_rank(const std::vector<double>& sv, double eps, std::optional<double> reference_sigma1) {
@@ -402,12 +483,11 @@ void sym_eig(const Matrix& A_in, std::vector<double>& evals, Matrix* evecs) {
 LeverageScores row_leverage_scores(const KernelBlock& K, int64_t r) {
   const int64_t mn = std::min(K.rows(), K.cols());
   if (r < 1 || r > mn) throw RangeError("row_leverage_scores: requires 1 <= r <= min(m, n)");
-  std::vector<double> ev;
-  Matrix V;
-  sym_eig(K.gram(), ev, &V);
+  const RightFactor rf = K.right_factor();  // lowrank.hpp:299 (TSQR on the device for m <= 128)
+  const Matrix& V = rf.V;
   const int64_t m = K.cols();
-  std::vector<double> sv(static_cast<size_t>(m));
-  for (int64_t i = 0; i < m; ++i) sv[static_cast<size_t>(i)] = std::sqrt(std::max(ev[static_cast<size_t>(i)], 0.0));
+  std::vector<double> sv = rf.singular_values;
+  sv.resize(static_cast<size_t>(m), 0.0);
   if (!(sv[static_cast<size_t>(r - 1)] > 0.0))
     throw NumericalError("row_leverage_scores: sigma_r vanishes; scores undefined");
   Matrix W(m, r);  // lowrank.hpp:304
@@ -673,6 +753,62 @@ std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, 
   return {std::move(id), rep};
 }
 
+// compress.hpp:219-273 with the error pass on the device: ||K - K V_r V_r^T||_2 = ||K V_perp||_2,
+// V_perp = the trailing m - r columns of the full right factor, by kid_proj_gram (the N_T x m
+// difference is never formed).
+std::pair<Matrix, CompressionReport> compress_svd(const KernelBlock& K, const RowSample& sample, const RankRule& rule,
+                                                  const CompressOptions& opts) {
+  if (sample.indices.empty()) throw RangeError("compress_svd: empty row sample");
+  CompressionReport rep;
+  rep.fraction = sample.fraction;
+  rep.seed = sample.seed;
+  double t0 = now_ms();
+  const Matrix sub = K.rows_exact(sample.indices);
+  rep.timings.sample_ms = now_ms() - t0;
+  t0 = now_ms();
+  const RightFactor rf = right_factor(sub);
+  const int64_t r = rule.resolve(rf.singular_values);
+  rep.rank = r;
+  rep.sigma1_sample = rf.singular_values[0];
+  rep.sigma_r1_sample = (r < static_cast<int64_t>(rf.singular_values.size())) ? rf.singular_values[static_cast<size_t>(r)] : 0.0;
+  rep.timings.factor_ms = now_ms() - t0;
+  const int64_t m = K.cols();
+  Matrix Vr(m, r);
+  t0 = now_ms();
+  if (r == 0) {
+    rep.rank_zero = true;
+    rep.rel_error = 1.0;
+    rep.rel_error_fro = 1.0;
+  } else {
+    for (int64_t j = 0; j < r; ++j)
+      for (int64_t i = 0; i < m; ++i) Vr(i, j) = rf.V(i, j);
+    double num = 0.0, sd = 0.0, sk = 0.0;
+    if (r < m) {
+      const int64_t n = m - r;
+      Matrix Vp(m, n);
+      for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) Vp(i, j) = rf.V(i, r + j);
+      Matrix DtD(n, n);
+      K.device().check(kid_proj_gram(K.device().ctx(), K.spec().h, Vp.data(), n, &sd, &sk, DtD.data()));
+      std::vector<double> ev;
+      sym_eig(DtD, ev, nullptr);
+      num = std::sqrt(std::max(ev.empty() ? 0.0 : ev[0], 0.0));
+    } else {
+      K.gram(&sk);  // V_r spans R^m: the difference is rounding only
+    }
+    const double den = opts.k_norm ? *opts.k_norm : K.spectral_norm();
+    rep.rel_error = (den > 0.0) ? num / den : 0.0;
+    rep.rel_error_fro = (sk > 0.0) ? std::sqrt(sd / sk) : 0.0;
+  }
+  rep.timings.error_ms = now_ms() - t0;
+  if (opts.full_spectrum) {
+    const auto& fs = *opts.full_spectrum;
+    const double sig = (r < static_cast<int64_t>(fs.size())) ? fs[static_cast<size_t>(r)] : 0.0;
+    rep.bound_sampling = reconstruction_bound(K.rows(), static_cast<int64_t>(sample.indices.size()), opts.theorem_eps, sig);
+  }
+  return {std::move(Vr), rep};
+}
+
 std::vector<double> mc_error(const KernelBlock& K, const IDFactorization& id, double s_mc, int n_mc,
                              std::uint64_t seed) {
   if (!(s_mc > 0.0 && s_mc <= 1.0)) throw RangeError("mc_error: requires s_mc in (0, 1]");
@@ -795,13 +931,7 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
         K.emplace(dev, KernelSpec::gaussian(h_abs), points, split);
         const bool auto_rank = scheme.kind == SchemeKind::Leverage && cfg.scheme_rank_auto[scheme_idx];
         const bool need_full = cfg.rank_reference_full || cfg.emit_bound_sampling || auto_rank;
-        if (need_full) {  // Gram route for the full spectrum (harness.hpp:176-184)
-          std::vector<double> ev;
-          sym_eig(K->gram(), ev, nullptr);
-          std::vector<double> sv(ev.size());
-          for (size_t i = 0; i < ev.size(); ++i) sv[i] = std::sqrt(std::max(ev[i], 0.0));
-          full_sv = sv;
-        }
+        if (need_full) full_sv = K->singular_values();  // harness.hpp:176-184 (device TSQR)
         if (cfg.rank_reference_full) rule.reference_sigma1 = (*full_sv)[0];
         if (auto_rank) scheme.rank_for_leverage = std::max<int64_t>(1, rule.resolve(*full_sv));
       }
@@ -1086,6 +1216,30 @@ int kidh_trial_next_rows(int32_t device, int32_t d, int64_t N, int64_t n, double
     const std::vector<double> u = apply_skeleton(K, id, std::vector<double>(q, q + K.cols()));
     if (static_cast<int64_t>(u.size()) > u_cap) throw RangeError("kidh_trial_next_rows: u buffer too small");
     std::memcpy(u_out, u.data(), sizeof(double) * u.size());
+  });
+}
+
+// One compress_svd trial (uniform sampling): rank, rel_error, rel_error_fro and V_r (m x rank).
+int kidh_trial_svd(int32_t device, int32_t d, int64_t N, int64_t n, double xi, double h_value, uint64_t data_seed,
+                   double s, uint64_t sample_seed, double eps, int64_t* rank, double* rel, double* rel_fro,
+                   double* Vr_out) {
+  return guard([&] {
+    Device dev(device);
+    const PointSet points = gen_normal(d, N, derive_seed(data_seed, 0xDA7A));
+    Rng crng(derive_seed(data_seed, 0xCE));
+    const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(N)));
+    std::vector<double> center(static_cast<size_t>(d));
+    for (int k = 0; k < d; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+    const SourceTargetSplit split = split_sources_targets(dev, points, center, n, xi);
+    const KernelBlock K(dev, KernelSpec::gaussian(h_value * silverman_bandwidth(d, N)), points, split);
+    SampleContext ctx;
+    ctx.m = K.rows();
+    const RowSample sample = sample_rows(SamplingScheme{}, ctx, s, sample_seed);
+    auto [Vr, rep] = compress_svd(K, sample, RankRule::from_eps(eps));
+    *rank = rep.rank;
+    *rel = rep.rel_error;
+    *rel_fro = rep.rel_error_fro;
+    if (rep.rank) std::memcpy(Vr_out, Vr.data(), sizeof(double) * Vr.a.size());
   });
 }
 

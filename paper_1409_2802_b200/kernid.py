@@ -47,6 +47,7 @@ def host_lib():
                                            P(i64), P(i64), _ip, _dp, _dp, _dp, i64]
         L.kidh_compress_trial.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, i32, i64, dbl, u64, dbl, P(i64), P(i64),
                                           P(dbl), P(dbl), _ip, _ip, P(i64)]
+        L.kidh_trial_svd.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, P(i64), P(dbl), P(dbl), _dp]
         L.kidh_run_experiment.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, i64, _dp, i32, dbl, i32, u64, C.c_char_p]
         _host = L
     return _host
@@ -172,6 +173,17 @@ def trial_next_rows(d, N, n, xi, data_seed, s, sample_seed, eps, s_mc, n_mc, mc_
     r = rank.value
     return (nt.value, r, skel[:r].copy(), P[: r * n].reshape(n, r).T.copy() if r else np.zeros((0, n)), mc,
             u[: nt.value].copy())
+
+
+def trial_svd(d, N, n, xi, data_seed, s, sample_seed, eps, h_value=1.0, device=0):
+    """A uniform-sampling compress_svd trial (compress.hpp:219-273) through the C++ mirror.
+    Returns (rank, rel_error, rel_error_fro, V_r (n x rank))."""
+    rank, rel, fro = C.c_int64(), C.c_double(), C.c_double()
+    V = np.zeros(n * n)
+    _ck(host_lib().kidh_trial_svd(device, d, N, n, xi, h_value, data_seed, s, sample_seed, eps, C.byref(rank),
+                                  C.byref(rel), C.byref(fro), V), "trial_svd")
+    r = rank.value
+    return r, rel.value, fro.value, _uncm(V[: n * r], n, r)
 
 
 def run_experiment(path: str, d, N, n, xi, scheme, s_grid, eps, trials=1, seed=1, h_value=1.0, lev_rank=0, device=0):
