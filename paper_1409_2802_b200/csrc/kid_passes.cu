@@ -1188,6 +1188,45 @@ __global__ void k_large_finish(double* __restrict__ G, int n, const double* __re
   }
 }
 
+// G (n x n, full) = D^T D (+ G when accumulate) for a tall D (rows x n, col-major, ld): cuBLAS'
+// SYRK parallelises over output tiles only, which for n << rows leaves most SMs idle (one 3.5 ms
+// call per 262k x 47 batch at c5); here the rows are split into nch chunks, one strided-batched
+// DGEMM computes the per-chunk D_c^T D_c, and a fixed-order sum folds them (bitwise reproducible).
+__global__ void k_sum_partials(const double* __restrict__ part, int nparts, int64_t len, double* __restrict__ G,
+                               bool accumulate) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = accumulate ? G[e] : 0.0;
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += part[(size_t)p * len + e];
+    G[e] = acc + s;
+  }
+}
+
+int tall_syrk(kid_ctx* c, const double* D, int rows, int ld, int n, double* G, bool accumulate, double* part,
+              int max_parts) {
+  const double one = 1.0, zero = 0.0;
+  const int nch = std::max(1, std::min(max_parts - 1, rows / 2048));
+  const int chunk = rows / nch, rem = rows - nch * chunk;
+  const int64_t nn = (int64_t)n * n;
+  if (chunk > 0 &&
+      cublasDgemmStridedBatched(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, n, n, chunk, &one, D, ld, chunk, D, ld, chunk, &zero,
+                                part, n, nn, nch) != CUBLAS_STATUS_SUCCESS)
+    return fail(c, KID_E_CUDA, "cublasDgemmStridedBatched failed");
+  c->launches++;
+  if (rem > 0) {
+    const double* Dr = D + (size_t)nch * chunk;
+    if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, n, n, rem, &one, Dr, ld, Dr, ld, &zero, part + nch * nn, n) !=
+        CUBLAS_STATUS_SUCCESS)
+      return fail(c, KID_E_CUDA, "cublasDgemm failed");
+    c->launches++;
+  }
+  k_sum_partials<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nn + 255) / 256, c->sms * 4)), 256, 0, c->stream>>>(
+      part, nch + (rem > 0 ? 1 : 0), nn, G, accumulate);
+  KID_LAUNCHED(c);
+  return KID_OK;
+}
+constexpr int kSyrkParts = 297;
+
 int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   const int m = (int)c->m, d = c->d, meff = (int)(m - r);
   if (!c->blas) {
@@ -1207,12 +1246,13 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   // scratch: K batch (B x m) | G (meff x meff) | P2 col-major (r x meff) | sk partials
   const size_t kb = (size_t)B * m, gb = (size_t)meff * meff, pb = (size_t)std::max<int64_t>(r, 1) * meff;
-  char* base = (char*)scratch(c, sizeof(double) * (kb + gb + pb + (size_t)nbatch * ev_blocks + 64));
+  char* base = (char*)scratch(c, sizeof(double) * (kb + gb + pb + (size_t)nbatch * ev_blocks + (size_t)kSyrkParts * gb + 64));
   if (!base) return KID_E_OOM;
   double* Kb = (double*)base;
   double* G = Kb + kb;
   double* P2c = G + gb;
   double* skp = P2c + pb;
+  double* gpart = skp + (size_t)nbatch * ev_blocks;
   if (r > 0) {  // P2 (row-major r x SP on the device) -> column-major r x meff
     const int SP = frag_stride(meff);
     std::vector<double> h_row((size_t)r * SP), h_col((size_t)r * meff);
@@ -1224,7 +1264,7 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   }
   const double* src = r > 0 ? c->src_perm : c->src;
   const double cscale = std::sqrt(1.0 / (2.0 * h * h));
-  const double one = 1.0, mone = -1.0, zero = 0.0;
+  const double one = 1.0, mone = -1.0;
   prof_begin(c);
   for (int64_t b = 0; b < nbatch; ++b) {
     const int64_t t0 = b * (int64_t)B;
@@ -1245,10 +1285,7 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
         return fail(c, KID_E_CUDA, "cublasDgemm failed");
       c->launches++;
     }
-    if (cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, meff, rows, &one, KN, rows, b == 0 ? &zero : &one, G,
-                    meff) != CUBLAS_STATUS_SUCCESS)
-      return fail(c, KID_E_CUDA, "cublasDsyrk failed");
-    c->launches++;
+    if (int rc = tall_syrk(c, KN, rows, rows, meff, G, b > 0, gpart, kSyrkParts)) return rc;
   }
   prof_end(c);
   k_large_finish<<<std::max(1, std::min(c->sms * 4, (meff * meff + 255) / 256)), 256, 0, c->stream>>>(
@@ -1536,12 +1573,14 @@ int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n64, double* 
   const int ev_blocks = ev_rows * ev_cols;
   const size_t ev_smem = sizeof(double) * (size_t)d * ceil_to(m, 4);
   if (ev_smem > 160 * 1024) return fail(c, KID_E_DIM, "proj_gram: m*d too large for shared memory");
-  char* base = (char*)scratch(c, sizeof(double) * ((size_t)B * (m + n) + (size_t)n * n + (size_t)nbatch * ev_blocks + 64));
+  char* base = (char*)scratch(c, sizeof(double) * ((size_t)B * (m + n) + (size_t)n * n + (size_t)nbatch * ev_blocks +
+                                                  (size_t)kSyrkParts * n * n + 64));
   if (!base) return KID_E_OOM;
   double* Kb = (double*)base;
   double* Db = Kb + (size_t)B * m;
   double* G = Db + (size_t)B * n;
   double* skp = G + (size_t)n * n;
+  double* gpart = skp + (size_t)nbatch * ev_blocks;
   const double one = 1.0, zero = 0.0;
   if (nt == 0) {
     KID_CK(c, cudaMemsetAsync(G, 0, sizeof(double) * n * n, c->stream));
@@ -1564,10 +1603,7 @@ int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n64, double* 
         CUBLAS_STATUS_SUCCESS)
       return fail(c, KID_E_CUDA, "cublasDgemm failed");
     c->launches++;
-    if (cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, n, rows, &one, Db, rows, b == 0 ? &zero : &one, G, n) !=
-        CUBLAS_STATUS_SUCCESS)
-      return fail(c, KID_E_CUDA, "cublasDsyrk failed");
-    c->launches++;
+    if (int rc = tall_syrk(c, Db, rows, rows, n, G, b > 0, gpart, kSyrkParts)) return rc;
   }
   prof_end(c);
   const int nsk = nt == 0 ? ev_blocks : (int)(nbatch * ev_blocks);
