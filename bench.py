@@ -425,6 +425,75 @@ def run_apply(args):
     print(json.dumps(line), flush=True)
 
 
+def run_next_pass(args):
+    """--pass svd: the compress_svd error pass (kid_proj_gram, compress.hpp:243-262, SURVEY.md 8f
+    item 1) with C = V_perp of the config's sample (rank r by its eps): per (target, source) entry
+    eval 3d + 33, ||K||^2 2, D = K V_perp 2n, D^T D n(n+1)/m (n = m - r).
+    --pass tsqr: the TSQR factor of the full K (kid_tsqr_r): eval 3d + 33 and
+    the Householder fold ~2m per entry."""
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    torch.cuda.set_stream(torch.cuda.Stream())
+    wl = WORKLOADS[args.config]
+    dev, prob = setup(wl, 1, 0, local, torch)
+    stream = torch.cuda.current_stream()
+    dev.set_stream(stream.cuda_stream)
+    d, m = wl["d"], wl["m"]
+    H = prob.H
+    if args.pass_ == "svd":
+        w = dev.row_norms(prob.h)
+        sample = H.draw(H.EUCLIDEAN_NORM, w.size, wl["s"], H.derive_seed(prob.data_seed, 0, 1), w)
+        Ks = H.kernel_rows(prob.pts_cm, prob.points.shape[0], d, dev.targets() - prob.offset, sample,
+                           prob.src - prob.offset, prob.h)
+        _, sv, Vt = np.linalg.svd(Ks, full_matrices=True)
+        r = H.epsilon_rank(sv, wl["eps"])
+        n = m - r
+        Vp = Vt.T[:, r:]  # m x n: V_perp
+        Cm = torch.tensor(np.ascontiguousarray(Vp.T).ravel(), dtype=torch.float64, device="cuda")  # column-major
+        out = torch.empty(2 + n * n, dtype=torch.float64, device="cuda")
+        fn = lambda: dev.proj_gram_dev(prob.h, Cm.data_ptr(), n, out.data_ptr())
+        fpe = 3 * d + 33 + 2 + 2 * n + n * (n + 1) / m
+        kern, metric = "k_proj_gram", "compress_svd error-pass entries/s (targets x sources, FP64)"
+        extra = {"rank": r, "n_perp": n}
+    else:
+        R = torch.empty(m * m, dtype=torch.float64, device="cuda")
+        fn = lambda: dev.tsqr_r_dev(prob.h, R.data_ptr())
+        fpe = 3 * d + 33 + 2 * m
+        kern, metric = "k_tsqr", "TSQR entries/s (targets x sources, FP64)"
+        extra = {}
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    for _ in range(args.warmup):
+        fn()
+    torch.cuda.synchronize()
+    dev.profile(True)
+    l0 = dev.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        fn()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    launches = dev.launches - l0
+    kms = dev.profile_read()
+    dev.profile(False)
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    kavg = float(np.mean(kms)) if len(kms) else float("nan")
+    entries = float(prob.nt) * m
+    peaks = load_peaks()
+    ach = entries * fpe / (kavg / 1e3) / 1e12
+    line = {"metric": metric, "value": entries / (ms / 1e3), "unit": "entries/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f64",
+            "gpu_launches": launches,
+            "config": dict({"workload": f"{args.config}: N_T={prob.nt}, m={m}, d={d}",
+                            "l2": "flushed (256 MB write) between timed steps"}, **extra),
+            "roofline": {"bound": "fp64", "unit": "TFLOP/s", "peak": peaks["fp64_tflops"], "achieved": ach,
+                         "frac": ach / peaks["fp64_tflops"], "kernel": kern, "kernel_ms": kavg,
+                         "flops_per_entry": fpe}}
+    print(json.dumps(line), flush=True)
+
+
 def run_e2e(args, dev, prob, torch, ws, rank):
     """Same metric through the C-ABI with host buffers (pinned points H2D every step)."""
     wl = prob.wl
@@ -547,7 +616,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=50000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply"])
+    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -555,6 +624,8 @@ def main():
         run_reference(args)
     elif args.pass_ == "split":
         run_split(args)
+    elif args.pass_ in ("svd", "tsqr"):
+        run_next_pass(args)
     elif args.pass_ == "apply":
         run_apply(args)
     else:

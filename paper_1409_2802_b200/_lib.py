@@ -284,6 +284,9 @@ class Device:
         self._ck(self.L.kid_tsqr_r(self.h, h, R), "kid_tsqr_r")
         return R[: self.m * self.m].reshape(self.m, self.m).T.copy()
 
+    def tsqr_r_dev(self, h: float, d_R: int):
+        self._ck(self.L.kid_tsqr_r_dev(self.h, h, d_R), "kid_tsqr_r_dev")
+
     def tsqr_combine(self, Rs) -> np.ndarray:
         """Fold stacked m x m factors into one (kid_tsqr_combine)."""
         Rs = [np.asarray(R, dtype=np.float64) for R in Rs]

@@ -75,3 +75,13 @@ def ordered_sum(partial: np.ndarray, group=None, device=None) -> np.ndarray:
     for row in allp:
         out += row
     return out.reshape(partial.shape)
+
+
+def sharded_tsqr(dev, h: float, group=None, device=None) -> np.ndarray:
+    """TSQR factor of the sharded block: each rank's m x m factor of its
+    targets (kid_tsqr_r), all_gather, then every rank folds the stack in rank order
+    (kid_tsqr_combine) -> the identical R with R^T R = K^T K of the whole block."""
+    R = np.asarray(dev.tsqr_r(h), dtype=np.float64)
+    m = R.shape[0]
+    allR = all_gather_np(R.reshape(1, -1), group, device)
+    return dev.tsqr_combine([row.reshape(m, m) for row in allR])

@@ -31,7 +31,15 @@ class CpuShard:
         order = np.lexsort((idx, self.dist))[: min(n, p.shape[0])]
         return self.dist[order], idx[order]
 
+    def tsqr_r(self, h):  # stand-in for kid_tsqr_r on this shard's block
+        from oracle import oracle as O
+        return np.linalg.qr(O.kernel_matrix(self.pts[self.targets - self.offset], self.src_pts, h), mode="r")
+
+    def tsqr_combine(self, Rs):  # stand-in for kid_tsqr_combine
+        return np.linalg.qr(np.concatenate(Rs), mode="r")
+
     def split_finish(self, src_idx, rho, xi, src_points=None):
+        self.src_pts = src_points
         local = np.arange(self.pts.shape[0]) + self.offset
         keep = (self.dist >= xi * rho) & ~np.isin(local, src_idx)
         self.targets = local[keep]
@@ -65,7 +73,8 @@ def _worker(rank, ws, port, d, N, n, xi, q):
     P[:, skel] = np.eye(3)
     sd, sk, DtD, KtK = O.residual_stats(K_local, skel, P)
     red = D.ordered_sum(np.concatenate([[sd, sk], DtD.ravel()]))
-    q.put((rank, src, rho, shard.targets, red))
+    R = D.sharded_tsqr(shard, 0.3)
+    q.put((rank, src, rho, shard.targets, red, R))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -84,7 +93,7 @@ def test_sharded_split_and_reduction_match_single_process(oracle, d, N, n, xi):
         assert p.exitcode == 0
     allpts = oracle.gen_normal(d, N, 12345)
     ref = oracle.split_sources_targets(allpts, allpts[77], n, xi)
-    for _, src, rho, _, _ in res:
+    for _, src, rho, _, _, _ in res:
         assert np.array_equal(src, ref.source_indices)
         assert rho == ref.rho
     tg = np.concatenate([r[3] for r in res])
@@ -99,6 +108,10 @@ def test_sharded_split_and_reduction_match_single_process(oracle, d, N, n, xi):
     assert np.array_equal(red, res[1][4])  # every rank holds the identical reduction
     assert red[0] == pytest.approx(sd, rel=1e-12) and red[1] == pytest.approx(sk, rel=1e-12)
     assert np.allclose(red[2:].reshape(n, n), DtD, rtol=1e-11, atol=1e-14 * np.abs(DtD).max())
+    # sharded TSQR: identical factor on every rank, R^T R == K^T K of the whole block
+    R = res[0][5]
+    assert np.array_equal(R, res[1][5])
+    assert np.allclose(R.T @ R, K.T @ K, rtol=0, atol=1e-12 * np.abs(K.T @ K).max())
 
 
 def test_merge_candidates_tie_break():
