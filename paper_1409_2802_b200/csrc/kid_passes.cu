@@ -818,8 +818,8 @@ __global__ void __launch_bounds__(kPT, 1) k_proj_gram(const ProjArgs A) {
 // The per-CTA factors are then folded the same way (mode REDUCE: the tile rows come from a stack
 // of upper-triangular factors) until one R remains. R is unique up to row signs; its singular
 // values and right singular vectors are those of K.
-constexpr int kQT = 64;                 // tile rows (two per lane)
 constexpr int kQW = 16, kQThreads = kQW * 32;
+constexpr int kQCols = 4;  // owned columns updated together (independent shuffle reductions)
 
 struct TsqrArgs {
   TargetView tv;       // EVAL mode: rows of K(T, S)
@@ -832,20 +832,26 @@ struct TsqrArgs {
   double* Rout;        // [gridDim.x][m][m] col-major
 };
 
-size_t tsqr_smem_bytes(int m, int d) {
+size_t tsqr_smem_bytes(int m, int d, int rows) {
   const int m4 = ceil_to(m, 4);
-  return sizeof(double) * ((size_t)m * m + (size_t)m4 * kQT + (size_t)d * m4);
+  return sizeof(double) * ((size_t)m * m + (size_t)m4 * rows + (size_t)d * m4);
 }
 
-template <int D, bool EVAL>
+// ROWS-row tiles (ROWS / 32 rows per lane). Per column step j the reflector parameters
+// (beta, tau, 1/v0) come from shared memory, computed one step ahead by the warp that owns
+// column j: it updates column j first in step j - 1 and derives them from the updated column
+// (lookahead), so a step is one barrier plus each warp's batch of column updates.
+template <int D, bool EVAL, int ROWS>
 __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
+  constexpr int RL = ROWS / 32;  // rows per lane
   const int d = D ? D : A.d;
   const int m = A.m, m4 = ceil_to(m, 4);
   extern __shared__ __align__(16) double sm_q[];
   double* sR = sm_q;                         // m x m col-major (upper triangle used)
-  double* sA = sR + (size_t)m * m;           // tile, column-major [k][i], m4 x kQT
-  double* s_src = sA + (size_t)m4 * kQT;     // d x m4 scaled sources (EVAL)
+  double* sA = sR + (size_t)m * m;           // tile, column-major [k][i], m4 x ROWS
+  double* s_src = sA + (size_t)m4 * ROWS;    // d x m4 scaled sources (EVAL)
   __shared__ double s_tab[kExpTabWords];
+  __shared__ double s_par[2][4];             // per step parity: beta, tau, 1/v0, live
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (EVAL) stage_exp_table(s_tab, tid, kQThreads);
   for (int e = tid; e < m * m; e += kQThreads) sR[e] = 0.0;
@@ -856,31 +862,48 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
     }
   const int64_t t_lo = A.ntiles * blockIdx.x / gridDim.x, t_hi = A.ntiles * (blockIdx.x + 1) / gridDim.x;
   const double* tabl = s_tab + lane;
+  // reflector parameters of column j from its current entries (x0 = R[j][j], a = A[:, j])
+  auto params = [&](int j, int slot) {
+    double sq = 0.0;
+#pragma unroll
+    for (int q = 0; q < RL; ++q) {
+      const double a = sA[j * ROWS + lane + 32 * q];
+      sq = fma(a, a, sq);
+    }
+    const double sig = warp_sum(sq);
+    if (lane == 0) {
+      const double x0 = sR[j + (size_t)j * m];
+      if (sig == 0.0) {
+        s_par[slot][3] = 0.0;  // H_j = I
+      } else {
+        const double nrm = sqrt(fma(x0, x0, sig));
+        const double beta = x0 >= 0.0 ? -nrm : nrm;
+        const double v0 = x0 - beta;
+        s_par[slot][0] = beta;
+        s_par[slot][1] = -v0 / beta;
+        s_par[slot][2] = 1.0 / v0;
+        s_par[slot][3] = 1.0;
+      }
+    }
+  };
   for (int64_t tile = t_lo; tile < t_hi; ++tile) {
     __syncthreads();  // previous tile's last column step done (and the staging above)
-    const int64_t row0 = tile * kQT;
+    const int64_t row0 = tile * ROWS;
     if (EVAL) {
-      // lane = rows lane and lane + 32; four-column groups strided over the warps
       constexpr int DR = D ? D : 1;
-      double t[2][DR];
-      bool live[2];
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int64_t row = row0 + lane + 32 * h2;
-        live[h2] = row < A.nrows;
+      for (int q = 0; q < RL; ++q) {
+        const int64_t row = row0 + lane + 32 * q;
+        const bool live = row < A.nrows;
+        double t[DR];
         if constexpr (D > 0) {
 #pragma unroll
-          for (int k = 0; k < D; ++k) t[h2][k] = live[h2] ? tcoord(A.tv, row, k) * A.cscale : 0.0;
+          for (int k = 0; k < D; ++k) t[k] = live ? tcoord(A.tv, row, k) * A.cscale : 0.0;
         }
-      }
-      for (int g = warp; g < m4 / 4; g += kQW) {
-        const int j = 4 * g;
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int64_t row = row0 + lane + 32 * h2;
+        for (int g = warp; g < m4 / 4; g += kQW) {
+          const int j = 4 * g;
           double kv[4] = {0.0, 0.0, 0.0, 0.0};
           for (int k = 0; k < d; ++k) {
-            const double tk = D ? t[h2][D ? k : 0] : (live[h2] ? tcoord(A.tv, row, k) * A.cscale : 0.0);
+            const double tk = D ? t[D ? k : 0] : (live ? tcoord(A.tv, row, k) * A.cscale : 0.0);
             const double* xk = s_src + (size_t)k * m4 + j;
             const double a0 = tk - xk[0], a1 = tk - xk[1], a2 = tk - xk[2], a3 = tk - xk[3];
             kv[0] = fma(a0, a0, kv[0]);
@@ -890,12 +913,12 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
           }
           exp_neg_fast_n<4>(kv, tabl);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sA[(j + u) * kQT + lane + 32 * h2] = live[h2] ? kv[u] : 0.0;
+          for (int u = 0; u < 4; ++u) sA[(j + u) * ROWS + lane + 32 * q] = live ? kv[u] : 0.0;
         }
       }
     } else {
-      for (int e = tid; e < m * kQT; e += kQThreads) {
-        const int k = e / kQT, i = e - k * kQT;
+      for (int e = tid; e < m * ROWS; e += kQThreads) {
+        const int k = e / ROWS, i = e - k * ROWS;
         const int64_t gr = row0 + i;
         double v = 0.0;
         if (gr < A.nrows) {
@@ -907,57 +930,62 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
       }
     }
     __syncthreads();
-    int pend = -1;      // deferred diagonal write (R[j][j] is read by every warp during step j)
-    double pend_beta = 0.0;
+    if (warp == 0) params(0, 0);
+    __syncthreads();
     for (int j = 0; j < m; ++j) {
-      const double a0 = sA[j * kQT + lane], a1 = sA[j * kQT + lane + 32];
-      const double sig = warp_sum(fma(a0, a0, a1 * a1));
-      const double x0 = sR[j + (size_t)j * m];
-      if (pend >= 0 && warp == (pend % kQW) && lane == 0) sR[pend + (size_t)pend * m] = pend_beta;
-      pend = -1;
-      if (sig == 0.0) continue;  // H_j = I (uniform over the CTA: every warp sees the same column)
-      const double nrm = sqrt(fma(x0, x0, sig));
-      const double beta = x0 >= 0.0 ? -nrm : nrm;
-      const double v0 = x0 - beta;
-      const double tau = -v0 / beta;
-      const double v_lo = a0 / v0, v_hi = a1 / v0;
-      // columns k > j owned by this warp (k mod kQW == warp), two at a time for ILP
-      int k = j + 1 + ((warp - (j + 1)) % kQW + kQW) % kQW;
-      for (; k + kQW < m; k += 2 * kQW) {
-        const int k2 = k + kQW;
-        const double b0 = sA[k * kQT + lane], b1 = sA[k * kQT + lane + 32];
-        const double c0 = sA[k2 * kQT + lane], c1 = sA[k2 * kQT + lane + 32];
-        double dot = fma(v_lo, b0, v_hi * b1), dot2 = fma(v_lo, c0, v_hi * c1);
+      const double* par = s_par[j & 1];
+      if (par[3] != 0.0) {  // uniform over the CTA
+        const double beta = par[0], tau = par[1], iv0 = par[2];
+        double v[RL];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          dot += __shfl_xor_sync(0xffffffffu, dot, o);
-          dot2 += __shfl_xor_sync(0xffffffffu, dot2, o);
+        for (int q = 0; q < RL; ++q) v[q] = sA[j * ROWS + lane + 32 * q] * iv0;
+        if (warp == j % kQW && lane == 0) sR[j + (size_t)j * m] = beta;  // nobody reads R[j][j] again
+        // owned columns k > j, k = warp (mod kQW); the owner of column j + 1 takes it first
+        int k = j + 1 + ((warp - (j + 1)) % kQW + kQW) % kQW;
+        for (; k < m; k += kQCols * kQW) {
+          double b[kQCols][RL], dot[kQCols];
+#pragma unroll
+          for (int c = 0; c < kQCols; ++c) {
+            const int kc = k + c * kQW;
+            dot[c] = 0.0;
+#pragma unroll
+            for (int q = 0; q < RL; ++q) {
+              b[c][q] = kc < m ? sA[kc * ROWS + lane + 32 * q] : 0.0;
+              dot[c] = fma(v[q], b[c][q], dot[c]);
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int c = 0; c < kQCols; ++c) dot[c] += __shfl_xor_sync(0xffffffffu, dot[c], o);
+          double w[kQCols];
+#pragma unroll
+          for (int c = 0; c < kQCols; ++c) {
+            const int kc = k + c * kQW;
+            w[c] = kc < m ? tau * (sR[j + (size_t)kc * m] + dot[c]) : 0.0;
+            if (kc < m) {
+#pragma unroll
+              for (int q = 0; q < RL; ++q) sA[kc * ROWS + lane + 32 * q] = fma(-w[c], v[q], b[c][q]);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int c = 0; c < kQCols; ++c) {
+              const int kc = k + c * kQW;
+              if (kc < m) sR[j + (size_t)kc * m] -= w[c];
+            }
+          }
+          if (k == j + 1) {  // lookahead: the next step's reflector from the updated column j + 1
+            __syncwarp();
+            params(j + 1, (j + 1) & 1);
+          }
         }
-        const double w = tau * (sR[j + (size_t)k * m] + dot), w2 = tau * (sR[j + (size_t)k2 * m] + dot2);
-        sA[k * kQT + lane] = fma(-w, v_lo, b0);
-        sA[k * kQT + lane + 32] = fma(-w, v_hi, b1);
-        sA[k2 * kQT + lane] = fma(-w2, v_lo, c0);
-        sA[k2 * kQT + lane + 32] = fma(-w2, v_hi, c1);
-        __syncwarp();
-        if (lane == 0) {
-          sR[j + (size_t)k * m] -= w;
-          sR[j + (size_t)k2 * m] -= w2;
-        }
+      } else if (j + 1 < m && warp == (j + 1) % kQW) {
+        params(j + 1, (j + 1) & 1);
       }
-      if (k < m) {
-        const double b0 = sA[k * kQT + lane], b1 = sA[k * kQT + lane + 32];
-        const double dot = warp_sum(fma(v_lo, b0, v_hi * b1));
-        const double w = tau * (sR[j + (size_t)k * m] + dot);
-        sA[k * kQT + lane] = fma(-w, v_lo, b0);
-        sA[k * kQT + lane + 32] = fma(-w, v_hi, b1);
-        __syncwarp();
-        if (lane == 0) sR[j + (size_t)k * m] -= w;
-      }
-      pend = j;
-      pend_beta = beta;
       __syncthreads();
     }
-    if (pend >= 0 && warp == (pend % kQW) && lane == 0) sR[pend + (size_t)pend * m] = pend_beta;
   }
   __syncthreads();
   double* out = A.Rout + (size_t)blockIdx.x * m * m;
@@ -1624,14 +1652,16 @@ int tsqr_dev(kid_ctx* c, double h, const double* d_Rin, int64_t nR, int64_t m64,
   const int m = eval ? (int)c->m : (int)m64, d = eval ? c->d : 1;
   if (m < 1) return fail(c, KID_E_RANGE, "tsqr: requires m >= 1");
   if (m > 128) return fail(c, KID_E_DIM, "tsqr: m > 128 does not fit the shared-memory factor (use the Gram route)");
-  const size_t smem = tsqr_smem_bytes(m, d);
+  // 128-row tiles where the factor and the tile fit shared memory, else 64
+  const int rows = tsqr_smem_bytes(m, d, 128) <= 200 * 1024 ? 128 : 64;
+  const size_t smem = tsqr_smem_bytes(m, d, rows);
+  const size_t smem_red = tsqr_smem_bytes(m, 1, rows);
   if (smem > 200 * 1024) return fail(c, KID_E_DIM, "tsqr: m*d too large for shared memory");
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   const size_t mm = (size_t)m * m;
   const int64_t nrows0 = eval ? c->nt : nR * m;
-  const int64_t ntiles0 = (nrows0 + kQT - 1) / kQT;
+  const int64_t ntiles0 = (nrows0 + rows - 1) / rows;
   const int blocks0 = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms, ntiles0));
-  // ping-pong factor stacks
   double* base = (double*)scratch(c, sizeof(double) * mm * (size_t)(2 * blocks0 + 2));
   if (!base) return KID_E_OOM;
   double* bufA = base;
@@ -1646,37 +1676,42 @@ int tsqr_dev(kid_ctx* c, double h, const double* d_Rin, int64_t nR, int64_t m64,
   A.nrows = nrows0;
   A.ntiles = ntiles0;
   A.Rout = bufA;
+#define KID_TSQR_LAUNCH(DD, EV, RR, GRID, ARGS, SM)                                                     \
+  {                                                                                                     \
+    cudaFuncSetAttribute(k_tsqr<DD, EV, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SM));   \
+    k_tsqr<DD, EV, RR><<<(GRID), kQThreads, (SM), c->stream>>>(ARGS);                                   \
+  }
   prof_begin(c);
   if (eval) {
-#define LAUNCH(DD)                                                                                   \
-  {                                                                                                  \
-    cudaFuncSetAttribute(k_tsqr<DD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    k_tsqr<DD, true><<<blocks0, kQThreads, smem, c->stream>>>(A);                                    \
-  }
+#define LAUNCH(DD)                                                     \
+  if (rows == 128) KID_TSQR_LAUNCH(DD, true, 128, blocks0, A, smem)    \
+  else KID_TSQR_LAUNCH(DD, true, 64, blocks0, A, smem)
     KID_DISPATCH_D(d, LAUNCH)
 #undef LAUNCH
   } else {
-    cudaFuncSetAttribute(k_tsqr<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_tsqr<1, false><<<blocks0, kQThreads, smem, c->stream>>>(A);
+    if (rows == 128) KID_TSQR_LAUNCH(1, false, 128, blocks0, A, smem_red)
+    else KID_TSQR_LAUNCH(1, false, 64, blocks0, A, smem_red)
   }
   prof_end(c);
   KID_LAUNCHED(c);
+  // fold the per-CTA factors, four per CTA per level
   int64_t nf = blocks0;
   double* cur = bufA;
   double* nxt = bufB;
   while (nf > 1) {
-    const int64_t groups = (nf + 7) / 8;
+    const int64_t groups = (nf + 3) / 4;
     TsqrArgs Rd = A;
     Rd.Rin = cur;
     Rd.nrows = nf * m;
-    Rd.ntiles = (Rd.nrows + kQT - 1) / kQT;
+    Rd.ntiles = (Rd.nrows + rows - 1) / rows;
     Rd.Rout = nxt;
-    cudaFuncSetAttribute(k_tsqr<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_tsqr<1, false><<<(unsigned)groups, kQThreads, smem, c->stream>>>(Rd);
+    if (rows == 128) KID_TSQR_LAUNCH(1, false, 128, (unsigned)groups, Rd, smem_red)
+    else KID_TSQR_LAUNCH(1, false, 64, (unsigned)groups, Rd, smem_red)
     KID_LAUNCHED(c);
     nf = groups;
     std::swap(cur, nxt);
   }
+#undef KID_TSQR_LAUNCH
   KID_CK(c, cudaMemcpyAsync(d_R, cur, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
   return KID_OK;
 }
