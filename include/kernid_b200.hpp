@@ -232,7 +232,14 @@ std::vector<double> mc_error(const KernelBlock& K, const IDFactorization& id, do
 // compress.hpp:309-325 on the device: u_i = sum_j Ker(y_i, x_skel_j) (P q)_j over the block's targets.
 std::vector<double> apply_skeleton(const KernelBlock& K, const IDFactorization& id, const std::vector<double>& q);
 
+// compress.hpp:279-305 for the SVD reconstruction (khat_row(i) = V_r V_r^T K_i): num from the
+// projected Gram of the row subset onto V_perp (the complement of V_r), den from its K^T K.
+std::vector<double> mc_error_svd(const KernelBlock& K, const Matrix& Vr, double s_mc, int n_mc, std::uint64_t seed);
+// An orthonormal basis (m x (m - r)) of the complement of the orthonormal columns of Vr (Householder).
+Matrix complement_basis(const Matrix& Vr);
+
 // ------------------------------------------------------------- harness.hpp (compress sweep)
+enum class CompressionMethod { ID, SVD };  // compress.hpp:57-60
 struct ExperimentConfig {
   int d = 2;
   int64_t N = 100000;
@@ -250,6 +257,9 @@ struct ExperimentConfig {
   double theorem_eps = 0.5;
   int trials = 1;
   std::uint64_t seed = 1;
+  std::vector<CompressionMethod> methods{CompressionMethod::ID};  // config.hpp:79
+  std::optional<double> s_mc;                                     // config.hpp:85-86 (mc_error)
+  int n_mc = 1;
 };
 // harness.hpp:143-328 for the Normal dataset / RandomPoint center / ID method.
 void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out, std::ostream* log = nullptr);

@@ -842,6 +842,81 @@ std::vector<double> mc_error(const KernelBlock& K, const IDFactorization& id, do
   return estimates;
 }
 
+Matrix complement_basis(const Matrix& Vr) {
+  const int64_t m = Vr.rows, r = Vr.cols;
+  if (r > m) throw DimensionError("complement_basis: more columns than rows");
+  Matrix A = Vr;
+  std::vector<std::vector<double>> vs;  // Householder vectors (v[0] = 1, from row j), tau
+  std::vector<double> taus;
+  for (int64_t j = 0; j < r; ++j) {
+    double nrm = 0.0;
+    for (int64_t i = j; i < m; ++i) nrm += A(i, j) * A(i, j);
+    nrm = std::sqrt(nrm);
+    std::vector<double> v(static_cast<size_t>(m - j), 0.0);
+    double tau = 0.0;
+    if (nrm > 0.0) {
+      const double alpha = A(j, j), beta = alpha >= 0.0 ? -nrm : nrm, v0 = alpha - beta;
+      tau = -v0 / beta;
+      v[0] = 1.0;
+      for (int64_t i = 1; i < m - j; ++i) v[static_cast<size_t>(i)] = A(j + i, j) / v0;
+      for (int64_t k = j; k < r; ++k) {
+        double w = 0.0;
+        for (int64_t i = 0; i < m - j; ++i) w += v[static_cast<size_t>(i)] * A(j + i, k);
+        w *= tau;
+        for (int64_t i = 0; i < m - j; ++i) A(j + i, k) -= w * v[static_cast<size_t>(i)];
+      }
+    }
+    vs.push_back(std::move(v));
+    taus.push_back(tau);
+  }
+  Matrix Q(m, m - r);  // Q e_k = H_0 H_1 ... H_{r-1} e_k, k = r..m-1
+  for (int64_t c = 0; c < m - r; ++c) {
+    std::vector<double> x(static_cast<size_t>(m), 0.0);
+    x[static_cast<size_t>(r + c)] = 1.0;
+    for (int64_t j = r - 1; j >= 0; --j) {
+      const auto& v = vs[static_cast<size_t>(j)];
+      double w = 0.0;
+      for (int64_t i = 0; i < m - j; ++i) w += v[static_cast<size_t>(i)] * x[static_cast<size_t>(j + i)];
+      w *= taus[static_cast<size_t>(j)];
+      for (int64_t i = 0; i < m - j; ++i) x[static_cast<size_t>(j + i)] -= w * v[static_cast<size_t>(i)];
+    }
+    for (int64_t i = 0; i < m; ++i) Q(i, c) = x[static_cast<size_t>(i)];
+  }
+  return Q;
+}
+
+std::vector<double> mc_error_svd(const KernelBlock& K, const Matrix& Vr, double s_mc, int n_mc, std::uint64_t seed) {
+  if (!(s_mc > 0.0 && s_mc <= 1.0)) throw RangeError("mc_error: requires s_mc in (0, 1]");
+  if (n_mc < 1) throw RangeError("mc_error: requires n_mc >= 1");
+  kid_ctx* c = K.device().ctx();
+  const int64_t m = K.cols(), n = m - Vr.cols;
+  const Matrix Vp = n > 0 ? complement_basis(Vr) : Matrix();
+  SamplingScheme bern;
+  bern.kind = SchemeKind::Bernoulli;
+  SampleContext ctx;
+  ctx.m = K.rows();
+  std::vector<double> estimates;
+  for (int rep = 0; rep < n_mc; ++rep) {
+    RowSample rows = sample_rows(bern, ctx, s_mc, derive_seed(seed, static_cast<std::uint64_t>(rep)));
+    if (rows.indices.empty()) rows = sample_rows(bern, ctx, s_mc, derive_seed(seed, static_cast<std::uint64_t>(rep), 1));
+    if (rows.indices.empty()) throw Error("mc_error: Bernoulli draw empty twice; s_mc is too small for this matrix");
+    K.device().check(kid_select_rows(c, rows.indices.data(), static_cast<int64_t>(rows.indices.size())));
+    Matrix KtK(m, m), DtD(std::max<int64_t>(n, 1), std::max<int64_t>(n, 1));
+    double sd = 0.0, sk = 0.0;
+    int rc = kid_gram(c, K.spec().h, KtK.data(), &sk);
+    if (!rc && n > 0) rc = kid_proj_gram(c, K.spec().h, Vp.data(), n, &sd, &sk, DtD.data());
+    K.device().check(kid_select_rows(c, nullptr, -1));
+    K.device().check(rc);
+    std::vector<double> ed, ek;
+    if (n > 0) sym_eig(DtD, ed, nullptr);
+    sym_eig(KtK, ek, nullptr);
+    const double num = std::sqrt(std::max(ed.empty() ? 0.0 : ed[0], 0.0));
+    const double den = std::sqrt(std::max(ek.empty() ? 0.0 : ek[0], 0.0));
+    estimates.push_back(den > 0.0 ? num / den : (num > 0.0 ? std::numeric_limits<double>::infinity() : 0.0));
+  }
+  return estimates;
+}
+
 std::vector<double> apply_skeleton(const KernelBlock& K, const IDFactorization& id, const std::vector<double>& q) {
   if (static_cast<int64_t>(q.size()) != id.projection.cols)
     throw DimensionError("apply_skeleton: charge count disagrees with the projection width");
@@ -897,11 +972,11 @@ const std::vector<std::string>& compress_csv_header() {
 // harness.hpp:143-328 (Normal dataset, RandomPoint center, method "id").
 void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out, std::ostream* log) {
   struct Accum {
-    std::vector<double> errors, ranks;
+    std::vector<double> errors, ranks, mc;
   };
-  std::map<std::tuple<size_t, size_t>, Accum> accum;
+  std::map<std::tuple<size_t, size_t, size_t>, Accum> accum;
   struct Row {
-    std::tuple<size_t, size_t, int> key;
+    std::tuple<size_t, size_t, int, size_t> key;
     std::vector<std::string> cells;
   };
   std::vector<Row> rows;
@@ -955,37 +1030,53 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
           }
           if (!sample_error.empty() && log) *log << "trial " << trial << " s=" << s << ": " << sample_error << "\n";
         }
-        std::vector<std::string> cells(compress_csv_header().size());
-        cells[0] = "normal";
-        cells[1] = format_int(cfg.d);
-        cells[2] = format_int(static_cast<long long>(cfg.N));
-        cells[3] = format_int(static_cast<long long>(cfg.n_sources));
-        cells[4] = format_double(cfg.xi);
-        cells[5] = "gaussian";
-        cells[6] = trial_failed ? "" : format_double(h_abs);
-        cells[7] = "id";
-        cells[8] = cfg.schemes[scheme_idx].name();
-        cells[9] = format_double(s);
-        cells[10] = format_int(trial);
-        cells[11] = format_int(static_cast<long long>(sample_seed));
-        if (!trial_failed && sample) {
-          CompressOptions opts;
-          opts.theorem_eps = cfg.theorem_eps;
-          if (full_sv && cfg.emit_bound_sampling) opts.full_spectrum = *full_sv;
-          if (full_sv) opts.k_norm = (*full_sv)[0];
-          const double t0 = now_ms();
-          auto [id, rep] = compress_id(*K, *sample, rule, opts);
-          const double elapsed = now_ms() - t0;
-          cells[12] = format_int(static_cast<long long>(rep.rank));
-          cells[13] = format_double(rep.rel_error);
-          cells[15] = rep.bound_id ? format_double(*rep.bound_id) : "";
-          cells[16] = rep.bound_sampling ? format_double(*rep.bound_sampling) : "";
-          cells[17] = cfg.emit_timings ? format_double(elapsed) : "";
-          auto& acc = accum[{scheme_idx, s_idx}];
-          acc.errors.push_back(rep.rel_error);
-          acc.ranks.push_back(static_cast<double>(rep.rank));
+        for (size_t method_idx = 0; method_idx < cfg.methods.size(); ++method_idx) {  // harness.hpp:211-289
+          const CompressionMethod method = cfg.methods[method_idx];
+          std::vector<std::string> cells(compress_csv_header().size());
+          cells[0] = "normal";
+          cells[1] = format_int(cfg.d);
+          cells[2] = format_int(static_cast<long long>(cfg.N));
+          cells[3] = format_int(static_cast<long long>(cfg.n_sources));
+          cells[4] = format_double(cfg.xi);
+          cells[5] = "gaussian";
+          cells[6] = trial_failed ? "" : format_double(h_abs);
+          cells[7] = method == CompressionMethod::ID ? "id" : "svd";
+          cells[8] = cfg.schemes[scheme_idx].name();
+          cells[9] = format_double(s);
+          cells[10] = format_int(trial);
+          cells[11] = format_int(static_cast<long long>(sample_seed));
+          if (!trial_failed && sample) {
+            CompressOptions opts;
+            opts.theorem_eps = cfg.theorem_eps;
+            if (full_sv && cfg.emit_bound_sampling) opts.full_spectrum = *full_sv;
+            if (full_sv) opts.k_norm = (*full_sv)[0];
+            const double t0 = now_ms();
+            CompressionReport rep;
+            std::optional<double> mc_mean;
+            const std::uint64_t mc_seed = derive_seed(data_seed, s_idx, 2);
+            if (method == CompressionMethod::ID) {
+              auto [id, r] = compress_id(*K, *sample, rule, opts);
+              rep = r;
+              if (cfg.s_mc && !rep.rank_zero) mc_mean = mean_of(mc_error(*K, id, *cfg.s_mc, cfg.n_mc, mc_seed));
+            } else {
+              auto [Vr, r] = compress_svd(*K, *sample, rule, opts);
+              rep = r;
+              if (cfg.s_mc && !rep.rank_zero) mc_mean = mean_of(mc_error_svd(*K, Vr, *cfg.s_mc, cfg.n_mc, mc_seed));
+            }
+            const double elapsed = now_ms() - t0;
+            cells[12] = format_int(static_cast<long long>(rep.rank));
+            cells[13] = format_double(rep.rel_error);
+            cells[14] = mc_mean ? format_double(*mc_mean) : "";
+            cells[15] = rep.bound_id ? format_double(*rep.bound_id) : "";
+            cells[16] = rep.bound_sampling ? format_double(*rep.bound_sampling) : "";
+            cells[17] = cfg.emit_timings ? format_double(elapsed) : "";
+            auto& acc = accum[{scheme_idx, s_idx, method_idx}];
+            acc.errors.push_back(rep.rel_error);
+            acc.ranks.push_back(static_cast<double>(rep.rank));
+            if (mc_mean) acc.mc.push_back(*mc_mean);
+          }
+          rows.push_back({{scheme_idx, s_idx, trial, method_idx}, std::move(cells)});
         }
-        rows.push_back({{scheme_idx, s_idx, trial}, std::move(cells)});
       }
     }
   }
@@ -993,8 +1084,9 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
   out << csv_join(compress_csv_header()) << "\n";
   for (const Row& row : rows) out << csv_join(row.cells) << "\n";
   for (size_t scheme_idx = 0; scheme_idx < cfg.schemes.size(); ++scheme_idx)
-    for (size_t s_idx = 0; s_idx < cfg.s_grid.size(); ++s_idx) {
-      const auto it = accum.find({scheme_idx, s_idx});
+    for (size_t s_idx = 0; s_idx < cfg.s_grid.size(); ++s_idx)
+      for (size_t method_idx = 0; method_idx < cfg.methods.size(); ++method_idx) {
+      const auto it = accum.find({scheme_idx, s_idx, method_idx});
       if (it == accum.end() || it->second.errors.empty()) continue;
       const Accum& acc = it->second;
       for (const char* stat : {"mean", "std"}) {
@@ -1007,12 +1099,13 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
         cells[3] = format_int(static_cast<long long>(cfg.n_sources));
         cells[4] = format_double(cfg.xi);
         cells[5] = "gaussian";
-        cells[7] = "id";
+        cells[7] = cfg.methods[method_idx] == CompressionMethod::ID ? "id" : "svd";
         cells[8] = cfg.schemes[scheme_idx].name();
         cells[9] = format_double(cfg.s_grid[s_idx]);
         cells[10] = stat;
         cells[12] = is_mean ? format_int(static_cast<long long>(std::llround(mean_of(acc.ranks)))) : "";
         cells[13] = is_mean ? format_double(mean_of(acc.errors)) : format_double(stddev_of(acc.errors));
+        cells[14] = acc.mc.empty() ? "" : (is_mean ? format_double(mean_of(acc.mc)) : format_double(stddev_of(acc.mc)));
         out << csv_join(cells) << "\n";
       }
     }
@@ -1246,7 +1339,7 @@ int kidh_trial_svd(int32_t device, int32_t d, int64_t N, int64_t n, double xi, d
 // run_experiment through the mirror; CSV written to `path`.
 int kidh_run_experiment(int32_t device, int32_t d, int64_t N, int64_t n, double xi, double h_value, int32_t scheme,
                         int64_t lev_rank, const double* s_grid, int32_t n_s, double eps, int32_t trials,
-                        uint64_t seed, const char* path) {
+                        uint64_t seed, const char* path, int32_t methods_mask, double s_mc, int32_t n_mc) {
   return guard([&] {
     Device dev(device);
     ExperimentConfig cfg;
@@ -1264,6 +1357,16 @@ int kidh_run_experiment(int32_t device, int32_t d, int64_t N, int64_t n, double 
     cfg.rank_rule = RankRule::from_eps(eps);
     cfg.trials = trials;
     cfg.seed = seed;
+    cfg.methods.clear();  // bit 0: id, bit 1: svd (config "methods", in that order)
+    if (methods_mask & 1) cfg.methods.push_back(CompressionMethod::ID);
+    if (methods_mask & 2) cfg.methods.push_back(CompressionMethod::SVD);
+    if (cfg.methods.empty()) throw ConfigError("config: methods must be nonempty");
+    if (s_mc > 0.0) {
+      if (!(s_mc <= 1.0)) throw ConfigError("mc_error.s_mc must lie in (0, 1]");
+      if (n_mc < 1) throw ConfigError("mc_error.n_mc must be >= 1");
+      cfg.s_mc = s_mc;
+      cfg.n_mc = n_mc;
+    }
     std::ostringstream os;
     run_experiment(dev, cfg, os, nullptr);
     FILE* f = std::fopen(path, "w");

@@ -48,7 +48,8 @@ def host_lib():
         L.kidh_compress_trial.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, i32, i64, dbl, u64, dbl, P(i64), P(i64),
                                           P(dbl), P(dbl), _ip, _ip, P(i64)]
         L.kidh_trial_svd.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, P(i64), P(dbl), P(dbl), _dp]
-        L.kidh_run_experiment.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, i64, _dp, i32, dbl, i32, u64, C.c_char_p]
+        L.kidh_run_experiment.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, i64, _dp, i32, dbl, i32, u64, C.c_char_p,
+                                          i32, dbl, i32]
         _host = L
     return _host
 
@@ -186,9 +187,13 @@ def trial_svd(d, N, n, xi, data_seed, s, sample_seed, eps, h_value=1.0, device=0
     return r, rel.value, fro.value, _uncm(V[: n * r], n, r)
 
 
-def run_experiment(path: str, d, N, n, xi, scheme, s_grid, eps, trials=1, seed=1, h_value=1.0, lev_rank=0, device=0):
+def run_experiment(path: str, d, N, n, xi, scheme, s_grid, eps, trials=1, seed=1, h_value=1.0, lev_rank=0, device=0,
+                   methods=("id",), s_mc=None, n_mc=1):
+    """kernid_b200::run_experiment (harness.hpp:143-328): the compress sweep CSV. `methods` in
+    {"id", "svd"} (config "methods"); `s_mc` / `n_mc` the config's mc_error block."""
     s_grid = np.ascontiguousarray(s_grid, dtype=np.float64)
+    mask = (1 if "id" in methods else 0) | (2 if "svd" in methods else 0)
     _ck(host_lib().kidh_run_experiment(device, d, N, n, xi, h_value, scheme, lev_rank, s_grid, s_grid.size, eps, trials,
-                                       seed, path.encode()), "run_experiment")
+                                       seed, path.encode(), mask, s_mc if s_mc else 0.0, n_mc), "run_experiment")
     with open(path) as f:
         return f.read()

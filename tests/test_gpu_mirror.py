@@ -78,3 +78,46 @@ def test_run_experiment_csv_matches_oracle(oracle, tmp_path):
         assert float(r[6]) == t.h
     stats = [r for r in rows if r[10] in ("mean", "std")]
     assert len(stats) == 2 * len(s_grid)
+
+
+def test_run_experiment_methods_and_mc(oracle, tmp_path):
+    """methods ["id", "svd"] with an mc_error block (harness.hpp:211-289): per row the ID / SVD
+    rel_error and the mean Monte Carlo estimate (seed derive_seed(data_seed, s_idx, 2)) against
+    the oracle pipeline; summary rows per (scheme, s, method)."""
+    from paper_1409_2802_b200 import kernid as H
+    d, N, n, xi, eps, trials, s_mc, n_mc = 2, 20000, 100, 2.0, 1e-4, 2, 0.1, 2
+    s_grid = [0.02]
+    csv = H.run_experiment(str(tmp_path / "m.csv"), d, N, n, xi, H.EUCLIDEAN_NORM, s_grid, eps, trials=trials, seed=1,
+                           methods=("id", "svd"), s_mc=s_mc, n_mc=n_mc)
+    rows = [l.split(",") for l in csv.strip().splitlines()[1:]]
+    body = [r for r in rows if r[10] not in ("mean", "std")]
+    assert [(r[10], r[7]) for r in body] == [("0", "id"), ("0", "svd"), ("1", "id"), ("1", "svd")]
+    U = 2.220446049250313e-16
+    for r in body:
+        trial, seed = int(r[10]), int(r[11]) % (1 << 64)
+        data_seed = oracle.derive_seed(1, trial, 0)
+        t, K, rws, res = _oracle_trial(oracle, d, N, n, xi, data_seed, oracle.SCHEME_EUCLIDEAN, 0.02, seed, eps)
+        normK = oracle.spectral_norm_exact(K)
+        floor = 10 * n * U * math.sqrt(np.sum(K * K)) / normK
+        mc_seed = oracle.derive_seed(data_seed, 0, 2)
+        if r[7] == "id":
+            assert int(r[12]) == res.rank
+            assert float(r[13]) == pytest.approx(res.rel_error, rel=1e-8)
+            ref_mc = float(np.mean(oracle.mc_error(K, res.skeleton, res.P, s_mc, n_mc, mc_seed)))
+        else:
+            sv, V = oracle.right_factor(K[rws])
+            rank = oracle.epsilon_rank(sv, eps)
+            Vr = V[:, :rank]
+            assert int(r[12]) == rank
+            ref = oracle.svd_error_norm(K, Vr) / normK
+            assert abs(float(r[13]) - ref) <= max(1e-8 * ref, floor)
+            ests = []
+            for rep in range(n_mc):
+                sel = oracle.sample_rows(oracle.SCHEME_BERNOULLI, K.shape[0], s_mc, oracle.derive_seed(mc_seed, rep, 0))
+                Ks = K[sel]
+                ests.append(np.linalg.norm(Ks @ Vr @ Vr.T - Ks, 2) / np.linalg.norm(Ks, 2))
+            ref_mc = float(np.mean(ests))
+        assert abs(float(r[14]) - ref_mc) <= max(1e-8 * ref_mc, 10 * floor)
+    stats = [r for r in rows if r[10] in ("mean", "std")]
+    assert [(r[7], r[10]) for r in stats] == [("id", "mean"), ("id", "std"), ("svd", "mean"), ("svd", "std")]
+    assert all(r[14] != "" for r in stats)
