@@ -37,6 +37,11 @@ class RangeError : public Error { public: using Error::Error; };
 class IllConditionedSkeletonError : public Error { public: using Error::Error; };
 class ConfigError : public Error { public: using Error::Error; };
 class NumericalError : public Error { public: using Error::Error; };
+class SearchFailureError : public Error {  // errors.hpp:71-77
+ public:
+  SearchFailureError(const std::string& msg, std::vector<std::pair<double, long>> p) : Error(msg), profile(std::move(p)) {}
+  std::vector<std::pair<double, long>> profile;
+};
 [[noreturn]] void throw_status(int code, const std::string& msg);
 
 // ------------------------------------------------------------- rng.hpp:19-78
@@ -263,6 +268,36 @@ struct ExperimentConfig {
 };
 // harness.hpp:143-328 for the Normal dataset / RandomPoint center / ID method.
 void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out, std::ostream* log = nullptr);
+
+// compress.hpp:327-378: spectral-norm fractions of the source-source, neighbour-source and
+// far-field blocks of the N x n matrix of all points against the n points closest to x_c.
+// The blocks are evaluated on the device (kid_set_block + kid_gram); ||.||_2 = sqrt(lambda_max)
+// of the block Grams, ||K||_2 of the stack from their sum.
+struct InteractionFractions {
+  double self_frac = 0.0, nn_frac = 0.0, far_frac = 0.0;
+};
+InteractionFractions interaction_fractions(Device& dev, const PointSet& ps, const KernelSpec& spec,
+                                           const std::vector<double>& x_c, int64_t n);
+
+// harness.hpp:330-438: bisection over the Gaussian bandwidth for the h at which the eps-rank of
+// K meets kappa * n; each evaluation is the device TSQR spectrum (KernelBlock::singular_values).
+struct BandwidthSearchSpec {  // config.hpp:56-63
+  double kappa = 0.2;
+  bool large_h_branch = false;
+  double eps = 1e-2;
+  int max_iters = 40;
+  int rank_tolerance_rows = 2;
+  int seeds = 5;
+};
+struct BandwidthResult {
+  double h_abs = 0.0, h_over_hs = 0.0;
+  long rank = 0;
+  int evaluations = 0;
+  bool converged = false;
+  std::vector<std::pair<double, long>> profile;
+};
+BandwidthResult bandwidth_search(Device& dev, const ExperimentConfig& cfg, const BandwidthSearchSpec& spec,
+                                 std::uint64_t data_seed);
 std::string format_double(double v);
 
 }  // namespace kernid_b200

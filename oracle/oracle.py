@@ -12,6 +12,7 @@ known-answer tests, ported in ``tests/test_oracle.py``).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from dataclasses import dataclass
@@ -428,3 +429,98 @@ def prepare_trial(d: int, N: int, n_sources: int, xi: float, data_seed: int, h_v
     targets = gather_points(points, split.target_indices)
     h = h_value * silverman_bandwidth(d, N) if silverman_units else h_value
     return Trial(points, center, split, sources, targets, h, d)
+
+
+# ------------------------------------------------------------- compress.hpp:327-378, harness.hpp:330-438
+def interaction_fractions(points: np.ndarray, h: float, x_c, n: int):
+    """interaction_fractions (compress.hpp:336-378): order all points by (||p - x_c||, index),
+    sources = first n, neighbours = next n, far = the rest; fractions of ||K||_2 of the stack
+    carried by each block (exact norms: matrix_norm at these sizes, compress.hpp:156-159)."""
+    N = points.shape[0]
+    if N < 2 * n:
+        raise OracleError(E_RANGE, "interaction_fractions: requires N >= 2n")
+    diff = points - np.asarray(x_c)[None, :]
+    acc = diff[:, 0] * diff[:, 0]
+    for k in range(1, points.shape[1]):
+        acc = acc + diff[:, k] * diff[:, k]
+    dist = np.sqrt(acc)
+    order = np.lexsort((np.arange(N), dist))
+    src, nb, far = points[order[:n]], points[order[n:2 * n]], points[order[2 * n:]]
+    KS, KN = kernel_matrix(src, src, h), kernel_matrix(nb, src, h)
+    KF = kernel_matrix(far, src, h) if far.shape[0] else np.zeros((0, n))
+    total = spectral_norm_exact(np.concatenate([KS, KN, KF]))
+    if not total > 0.0:
+        return 0.0, 0.0, 0.0
+    return (spectral_norm_exact(KS) / total, spectral_norm_exact(KN) / total,
+            spectral_norm_exact(KF) / total if far.shape[0] else 0.0)
+
+
+def bandwidth_search(d, N, n, xi, data_seed, kappa=0.2, large_h=False, eps=1e-2, max_iters=40, tol_rows=2):
+    """bandwidth_search (harness.hpp:345-438) on the oracle's K and singular_values; returns
+    (h_abs, h_over_hs, rank, evaluations, converged, profile) or raises OracleError with the
+    profile in .profile when the budget cannot be bracketed."""
+    t = prepare_trial(d, N, n, xi, data_seed)
+    h_S = silverman_bandwidth(d, N)
+    target = kappa * n
+    profile = []
+
+    def rank_at(h):
+        r = epsilon_rank(singular_values(kernel_matrix(t.targets, t.sources, h)), eps)
+        profile.append((h, r))
+        return r
+
+    def fail(msg):
+        e = OracleError(E_RANGE, msg)
+        e.profile = profile
+        raise e
+
+    scan = [1e-3, 1e-2, 0.03, 0.1, 0.3, 1.0, 3.0, 10.0, 1e2]
+    coarse, peak = [], 0
+    for i, sc in enumerate(scan):
+        coarse.append((sc * h_S, rank_at(sc * h_S)))
+        if coarse[i][1] > coarse[peak][1]:
+            peak = i
+    if coarse[peak][1] < target:
+        fail("rank budget exceeds the peak epsilon-rank")
+    if not large_h:
+        hi, r_hi = coarse[peak]
+        below = peak
+        while below > 0 and coarse[below][1] >= target:
+            below -= 1
+        lo, r_lo = coarse[below]
+        for _ in range(5):
+            if r_lo < target:
+                break
+            lo /= 2.0
+            r_lo = rank_at(lo)
+        ok = r_lo < target <= r_hi
+    else:
+        lo, r_lo = coarse[peak]
+        above = peak
+        while above + 1 < len(coarse) and coarse[above][1] >= target:
+            above += 1
+        hi, r_hi = coarse[above]
+        for _ in range(5):
+            if r_hi < target:
+                break
+            hi *= 2.0
+            r_hi = rank_at(hi)
+        ok = r_lo >= target > r_hi
+    if not ok:
+        fail("could not bracket the rank budget")
+    h_best, r_best = (hi, r_hi) if not large_h else (lo, r_lo)
+    converged = False
+    while len(profile) < max_iters:
+        mid = math.sqrt(lo * hi)
+        r_mid = rank_at(mid)
+        if abs(r_mid - target) <= abs(r_best - target):
+            h_best, r_best = mid, r_mid
+        if abs(r_mid - target) <= tol_rows:
+            converged = True
+            break
+        go_right = (r_mid < target) if not large_h else (r_mid >= target)
+        if go_right:
+            lo = mid
+        else:
+            hi = mid
+    return h_best, h_best / h_S, r_best, len(profile), converged, profile

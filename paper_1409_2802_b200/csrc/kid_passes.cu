@@ -1141,17 +1141,18 @@ int row_norms_dev(kid_ctx* c, double h, double* d_w) {
 template <int D>
 __global__ void __launch_bounds__(256) k_eval_batch(TargetView tv, int d_rt, const double* __restrict__ src, int m,
                                                     double cscale, int64_t t0, int B, double* __restrict__ Kb,
-                                                    double* __restrict__ sk_part) {
+                                                    double* __restrict__ sk_part, bool staged) {
   const int d = D ? D : d_rt;
   const int m4 = ceil_to(m, 4);
-  extern __shared__ __align__(16) double sm_eb[];  // d x m4 scaled sources
+  extern __shared__ __align__(16) double sm_eb[];  // d x m4 scaled sources (when staged)
   __shared__ double s_tab[kExpTabWords];
   __shared__ double red[8];
   stage_exp_table(s_tab, threadIdx.x, blockDim.x);
-  for (int e = threadIdx.x; e < d * m4; e += blockDim.x) {
-    const int k = e / m4, j = e - k * m4;
-    sm_eb[e] = j < m ? src[j + (int64_t)k * m] * cscale : 1.0e4;
-  }
+  if (staged)
+    for (int e = threadIdx.x; e < d * m4; e += blockDim.x) {
+      const int k = e / m4, j = e - k * m4;
+      sm_eb[e] = j < m ? src[j + (int64_t)k * m] * cscale : 1.0e4;
+    }
   __syncthreads();
   const double* tabl = s_tab + (threadIdx.x & 31);
   const int ng = m4 / 4;
@@ -1171,8 +1172,16 @@ __global__ void __launch_bounds__(256) k_eval_batch(TargetView tv, int d_rt, con
       double kv[4] = {0.0, 0.0, 0.0, 0.0};
       for (int k = 0; k < d; ++k) {
         const double tk = D ? t[D ? k : 0] : (live ? tcoord(tv, t0 + i, k) * cscale : 0.0);
-        const double* xk = sm_eb + (size_t)k * m4 + j;
-        const double a0 = tk - xk[0], a1 = tk - xk[1], a2 = tk - xk[2], a3 = tk - xk[3];
+        double x[4];
+        if (staged) {
+          const double* xk = sm_eb + (size_t)k * m4 + j;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = xk[u];
+        } else {  // m * d too large for shared memory: warp-uniform L1 broadcasts
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = j + u < m ? __ldg(src + j + u + (int64_t)k * m) * cscale : 1.0e4;
+        }
+        const double a0 = tk - x[0], a1 = tk - x[1], a2 = tk - x[2], a3 = tk - x[3];
         kv[0] = fma(a0, a0, kv[0]);
         kv[1] = fma(a1, a1, kv[1]);
         kv[2] = fma(a2, a2, kv[2]);
@@ -1269,8 +1278,8 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   const int ev_rows = (B + 255) / 256;
   const int ev_cols = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_to(m, 4) / 4, (4ll * c->sms + ev_rows - 1) / ev_rows));
   const int ev_blocks = ev_rows * ev_cols;
-  const size_t ev_smem = sizeof(double) * (size_t)d * ceil_to(m, 4);
-  if (ev_smem > 160 * 1024) return fail(c, KID_E_DIM, "large-m Gram: m*d too large for shared memory");
+  const bool ev_staged = sizeof(double) * (size_t)d * ceil_to(m, 4) <= 160 * 1024;
+  const size_t ev_smem = ev_staged ? sizeof(double) * (size_t)d * ceil_to(m, 4) : 0;
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   // scratch: K batch (B x m) | G (meff x meff) | P2 col-major (r x meff) | sk partials
   const size_t kb = (size_t)B * m, gb = (size_t)meff * meff, pb = (size_t)std::max<int64_t>(r, 1) * meff;
@@ -1301,7 +1310,7 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   {                                                                                                       \
     cudaFuncSetAttribute(k_eval_batch<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ev_smem);     \
     k_eval_batch<DD><<<dim3(ev_rows, ev_cols), 256, ev_smem, c->stream>>>(view(c), d, src, m, cscale, t0, rows, \
-                                                                         Kb, skp + b * ev_blocks);        \
+                                                                         Kb, skp + b * ev_blocks, ev_staged); \
   }
     KID_DISPATCH_D(d, LAUNCH)
 #undef LAUNCH
@@ -1599,8 +1608,8 @@ int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n64, double* 
   const int ev_rows = (B + 255) / 256;
   const int ev_cols = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_to(m, 4) / 4, (4ll * c->sms + ev_rows - 1) / ev_rows));
   const int ev_blocks = ev_rows * ev_cols;
-  const size_t ev_smem = sizeof(double) * (size_t)d * ceil_to(m, 4);
-  if (ev_smem > 160 * 1024) return fail(c, KID_E_DIM, "proj_gram: m*d too large for shared memory");
+  const bool ev_staged = sizeof(double) * (size_t)d * ceil_to(m, 4) <= 160 * 1024;
+  const size_t ev_smem = ev_staged ? sizeof(double) * (size_t)d * ceil_to(m, 4) : 0;
   char* base = (char*)scratch(c, sizeof(double) * ((size_t)B * (m + n) + (size_t)n * n + (size_t)nbatch * ev_blocks +
                                                   (size_t)kSyrkParts * n * n + 64));
   if (!base) return KID_E_OOM;
@@ -1622,7 +1631,7 @@ int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n64, double* 
   {                                                                                                        \
     cudaFuncSetAttribute(k_eval_batch<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ev_smem);      \
     k_eval_batch<DD><<<dim3(ev_rows, ev_cols), 256, ev_smem, c->stream>>>(view(c), d, c->src, m, cscale, t0, \
-                                                                         rows, Kb, skp + b * ev_blocks);   \
+                                                                         rows, Kb, skp + b * ev_blocks, ev_staged); \
   }
     KID_DISPATCH_D(d, LAUNCH)
 #undef LAUNCH

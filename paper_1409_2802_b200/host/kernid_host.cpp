@@ -1111,6 +1111,168 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
     }
 }
 
+// ------------------------------------------------------------------ interaction fractions
+namespace {
+// largest eigenvalue of a symmetric PSD matrix: Jacobi for small n, else power iteration
+// (Rayleigh quotient to 1e-15 relative change)
+double lambda_max(const Matrix& G) {
+  const int64_t n = G.rows;
+  if (n <= 128) {
+    std::vector<double> ev;
+    sym_eig(G, ev, nullptr);
+    return ev.empty() ? 0.0 : std::max(ev[0], 0.0);
+  }
+  std::vector<double> x(static_cast<size_t>(n), 1.0 / std::sqrt(static_cast<double>(n))), y(static_cast<size_t>(n));
+  double lam = 0.0;
+  for (int it = 0; it < 100000; ++it) {
+    for (int64_t i = 0; i < n; ++i) {
+      double acc = 0.0;
+      for (int64_t j = 0; j < n; ++j) acc += G(i, j) * x[static_cast<size_t>(j)];
+      y[static_cast<size_t>(i)] = acc;
+    }
+    double nrm = 0.0, rq = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      nrm += y[static_cast<size_t>(i)] * y[static_cast<size_t>(i)];
+      rq += x[static_cast<size_t>(i)] * y[static_cast<size_t>(i)];
+    }
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) return 0.0;
+    for (int64_t i = 0; i < n; ++i) x[static_cast<size_t>(i)] = y[static_cast<size_t>(i)] / nrm;
+    if (it > 3 && std::fabs(rq - lam) <= 1e-15 * rq) return rq;
+    lam = rq;
+  }
+  return lam;
+}
+}  // namespace
+
+InteractionFractions interaction_fractions(Device& dev, const PointSet& ps, const KernelSpec& spec,
+                                           const std::vector<double>& x_c, int64_t n) {
+  spec.validate();
+  const int64_t N = ps.rows;
+  const int d = static_cast<int>(ps.cols);
+  if (N < 2 * n) throw RangeError("interaction_fractions: requires N >= 2n");
+  if (static_cast<int64_t>(x_c.size()) != d) throw DimensionError("interaction_fractions: center dimension mismatch");
+  std::vector<double> dist(static_cast<size_t>(N));
+  for (int64_t i = 0; i < N; ++i) dist[static_cast<size_t>(i)] = center_distance(ps, i, x_c);
+  std::vector<int64_t> order(static_cast<size_t>(N));
+  std::iota(order.begin(), order.end(), int64_t{0});
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {  // compress.hpp:344-347
+    if (dist[static_cast<size_t>(a)] != dist[static_cast<size_t>(b)]) return dist[static_cast<size_t>(a)] < dist[static_cast<size_t>(b)];
+    return a < b;
+  });
+  auto take = [&](int64_t from, int64_t count) {  // col-major count x d
+    Matrix blk(count, d);
+    for (int64_t i = 0; i < count; ++i)
+      for (int k = 0; k < d; ++k) blk(i, k) = ps(order[static_cast<size_t>(from + i)], k);
+    return blk;
+  };
+  const Matrix sources = take(0, n), neighbors = take(n, n), far = take(2 * n, N - 2 * n);
+  auto block_gram = [&](const Matrix& tg) {
+    Matrix G(n, n);
+    dev.check(kid_set_block(dev.ctx(), tg.data(), tg.rows, sources.data(), n, d));
+    dev.check(kid_gram(dev.ctx(), spec.h, G.data(), nullptr));
+    return G;
+  };
+  const Matrix GS = block_gram(sources), GN = block_gram(neighbors);
+  const Matrix GF = far.rows > 0 ? block_gram(far) : Matrix(n, n);
+  Matrix GT(n, n);
+  for (size_t e = 0; e < GT.a.size(); ++e) GT.a[e] = GS.a[e] + GN.a[e] + GF.a[e];
+  const double total = std::sqrt(lambda_max(GT));
+  InteractionFractions f;
+  if (total > 0.0) {
+    f.self_frac = std::sqrt(lambda_max(GS)) / total;
+    f.nn_frac = std::sqrt(lambda_max(GN)) / total;
+    f.far_frac = far.rows > 0 ? std::sqrt(lambda_max(GF)) / total : 0.0;
+  }
+  return f;
+}
+
+// ------------------------------------------------------------------ bandwidth search
+BandwidthResult bandwidth_search(Device& dev, const ExperimentConfig& cfg, const BandwidthSearchSpec& spec,
+                                 std::uint64_t data_seed) {
+  // prepare_trial(cfg, data_seed, /*assemble_matrix=*/false) (harness.hpp:107-129)
+  const PointSet points = gen_normal(cfg.d, cfg.N, derive_seed(data_seed, 0xDA7A));
+  Rng crng(derive_seed(data_seed, 0xCE));
+  const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(points.rows)));
+  std::vector<double> center(static_cast<size_t>(cfg.d));
+  for (int k = 0; k < cfg.d; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+  const SourceTargetSplit split = split_sources_targets(dev, points, center, cfg.n_sources, cfg.xi);
+  const double h_S = silverman_bandwidth(cfg.d, points.rows);
+  const double target = spec.kappa * static_cast<double>(cfg.n_sources);
+  BandwidthResult res;
+  auto rank_at = [&](double h) -> long {
+    const KernelBlock K(dev, KernelSpec::gaussian(h), points, split);
+    const long r = static_cast<long>(epsilon_rank(K.singular_values(), spec.eps));
+    ++res.evaluations;
+    res.profile.emplace_back(h, r);
+    return r;
+  };
+  const bool increasing = !spec.large_h_branch;
+  const std::vector<double> scan = {1e-3, 1e-2, 0.03, 0.1, 0.3, 1.0, 3.0, 10.0, 1e2};
+  std::vector<std::pair<double, long>> coarse;
+  size_t peak_idx = 0;
+  for (size_t i = 0; i < scan.size(); ++i) {
+    coarse.emplace_back(scan[i] * h_S, rank_at(scan[i] * h_S));
+    if (coarse[i].second > coarse[peak_idx].second) peak_idx = i;
+  }
+  if (static_cast<double>(coarse[peak_idx].second) < target)
+    throw SearchFailureError("bandwidth_search: rank budget " + std::to_string(target) +
+                                 " exceeds the peak epsilon-rank " + std::to_string(coarse[peak_idx].second),
+                             res.profile);
+  double lo, hi;
+  long rank_lo, rank_hi;
+  if (increasing) {
+    hi = coarse[peak_idx].first;
+    rank_hi = coarse[peak_idx].second;
+    size_t below = peak_idx;
+    while (below > 0 && coarse[below].second >= target) --below;
+    lo = coarse[below].first;
+    rank_lo = coarse[below].second;
+    for (int grow = 0; grow < 5 && rank_lo >= target; ++grow) {
+      lo /= 2.0;
+      rank_lo = rank_at(lo);
+    }
+  } else {
+    lo = coarse[peak_idx].first;
+    rank_lo = coarse[peak_idx].second;
+    size_t above = peak_idx;
+    while (above + 1 < coarse.size() && coarse[above].second >= target) ++above;
+    hi = coarse[above].first;
+    rank_hi = coarse[above].second;
+    for (int grow = 0; grow < 5 && rank_hi >= target; ++grow) {
+      hi *= 2.0;
+      rank_hi = rank_at(hi);
+    }
+  }
+  const bool bracketed = increasing ? (rank_lo < target && static_cast<double>(rank_hi) >= target)
+                                    : (static_cast<double>(rank_lo) >= target && rank_hi < target);
+  if (!bracketed)
+    throw SearchFailureError("bandwidth_search: could not bracket the rank budget " + std::to_string(target) +
+                                 " on the " + (increasing ? std::string("small_h") : std::string("large_h")) + " branch",
+                             res.profile);
+  double h_best = increasing ? hi : lo;
+  long rank_best = increasing ? rank_hi : rank_lo;
+  while (res.evaluations < spec.max_iters) {
+    const double mid = std::sqrt(lo * hi);
+    const long rank_mid = rank_at(mid);
+    if (std::abs(static_cast<double>(rank_mid) - target) <= std::abs(static_cast<double>(rank_best) - target)) {
+      h_best = mid;
+      rank_best = rank_mid;
+    }
+    if (std::abs(static_cast<double>(rank_mid) - target) <= spec.rank_tolerance_rows) {
+      res.converged = true;
+      break;
+    }
+    const bool go_right = increasing ? (rank_mid < target) : (rank_mid >= target);
+    if (go_right) lo = mid;
+    else hi = mid;
+  }
+  res.h_abs = h_best;
+  res.h_over_hs = h_best / h_S;
+  res.rank = rank_best;
+  return res;
+}
+
 }  // namespace kernid_b200
 
 // ====================================================================== C exports
@@ -1333,6 +1495,61 @@ int kidh_trial_svd(int32_t device, int32_t d, int64_t N, int64_t n, double xi, d
     *rel = rep.rel_error;
     *rel_fro = rep.rel_error_fro;
     if (rep.rank) std::memcpy(Vr_out, Vr.data(), sizeof(double) * Vr.a.size());
+  });
+}
+
+// interaction_fractions over gen_normal(d, N, seed) points around x_c (d values).
+int kidh_interaction_fractions(int32_t device, int32_t d, int64_t N, uint64_t seed, double h, const double* x_c,
+                               int64_t n, double* fracs) {
+  return guard([&] {
+    Device dev(device);
+    const PointSet ps = gen_normal(d, N, seed);
+    const InteractionFractions f = interaction_fractions(dev, ps, KernelSpec::gaussian(h), std::vector<double>(x_c, x_c + d), n);
+    fracs[0] = f.self_frac;
+    fracs[1] = f.nn_frac;
+    fracs[2] = f.far_frac;
+  });
+}
+
+// bandwidth_search; out = [h_abs, h_over_hs, rank, evaluations, converged]; the (h, rank) profile
+// (also on SearchFailureError, status KID_E_ERROR) into prof (2 x prof_cap), its length into n_prof.
+int kidh_bandwidth_search(int32_t device, int32_t d, int64_t N, int64_t n, double xi, double kappa, int32_t large_h,
+                          double eps, int32_t max_iters, int32_t tol_rows, uint64_t data_seed, double* out, double* prof,
+                          int32_t prof_cap, int32_t* n_prof) {
+  *n_prof = 0;
+  auto dump = [&](const std::vector<std::pair<double, long>>& p) {
+    const int32_t k = std::min<int32_t>(prof_cap, static_cast<int32_t>(p.size()));
+    for (int32_t i = 0; i < k; ++i) {
+      prof[2 * i] = p[static_cast<size_t>(i)].first;
+      prof[2 * i + 1] = static_cast<double>(p[static_cast<size_t>(i)].second);
+    }
+    *n_prof = k;
+  };
+  return guard([&] {
+    Device dev(device);
+    ExperimentConfig cfg;
+    cfg.d = d;
+    cfg.N = N;
+    cfg.n_sources = n;
+    cfg.xi = xi;
+    BandwidthSearchSpec spec;
+    spec.kappa = kappa;
+    spec.large_h_branch = large_h != 0;
+    spec.eps = eps;
+    spec.max_iters = max_iters;
+    spec.rank_tolerance_rows = tol_rows;
+    try {
+      const BandwidthResult r = bandwidth_search(dev, cfg, spec, data_seed);
+      out[0] = r.h_abs;
+      out[1] = r.h_over_hs;
+      out[2] = static_cast<double>(r.rank);
+      out[3] = r.evaluations;
+      out[4] = r.converged ? 1.0 : 0.0;
+      dump(r.profile);
+    } catch (const SearchFailureError& e) {
+      dump(e.profile);
+      throw;
+    }
   });
 }
 

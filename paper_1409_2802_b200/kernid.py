@@ -48,6 +48,9 @@ def host_lib():
         L.kidh_compress_trial.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, i32, i64, dbl, u64, dbl, P(i64), P(i64),
                                           P(dbl), P(dbl), _ip, _ip, P(i64)]
         L.kidh_trial_svd.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, P(i64), P(dbl), P(dbl), _dp]
+        L.kidh_interaction_fractions.argtypes = [i32, i32, i64, u64, dbl, _dp, i64, _dp]
+        L.kidh_bandwidth_search.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, dbl, i32, i32, u64, _dp, _dp, i32,
+                                            P(i32)]
         L.kidh_run_experiment.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, i64, _dp, i32, dbl, i32, u64, C.c_char_p,
                                           i32, dbl, i32]
         _host = L
@@ -197,3 +200,32 @@ def run_experiment(path: str, d, N, n, xi, scheme, s_grid, eps, trials=1, seed=1
                                        seed, path.encode(), mask, s_mc if s_mc else 0.0, n_mc), "run_experiment")
     with open(path) as f:
         return f.read()
+
+
+def interaction_fractions(d, N, seed, h, x_c, n, device=0):
+    """interaction_fractions (compress.hpp:327-378) over gen_normal(d, N, seed); (self, nn, far)."""
+    f = np.zeros(3)
+    _ck(host_lib().kidh_interaction_fractions(device, d, N, seed, h, np.ascontiguousarray(x_c, dtype=np.float64), n, f),
+        "interaction_fractions")
+    return tuple(float(x) for x in f)
+
+
+class SearchFailure(KidError):
+    def __init__(self, code, msg, profile):
+        super().__init__(code, msg)
+        self.profile = profile
+
+
+def bandwidth_search(d, N, n, xi, data_seed, kappa=0.2, large_h=False, eps=1e-2, max_iters=40, tol_rows=2, device=0):
+    """bandwidth_search (harness.hpp:330-438) through the mirror: dict(h_abs, h_over_hs, rank,
+    evaluations, converged, profile); raises SearchFailure (with the profile) when it cannot bracket."""
+    out = np.zeros(5)
+    prof = np.zeros(2 * 256)
+    npf = C.c_int32()
+    rc = host_lib().kidh_bandwidth_search(device, d, N, n, xi, kappa, int(large_h), eps, max_iters, tol_rows, data_seed,
+                                          out, prof, 256, C.byref(npf))
+    profile = [(float(prof[2 * i]), int(prof[2 * i + 1])) for i in range(npf.value)]
+    if rc:
+        raise SearchFailure(rc, f"bandwidth_search: {host_lib().kidh_last_error().decode(errors='replace')}", profile)
+    return dict(h_abs=float(out[0]), h_over_hs=float(out[1]), rank=int(out[2]), evaluations=int(out[3]),
+                converged=bool(out[4]), profile=profile)

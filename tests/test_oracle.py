@@ -413,3 +413,24 @@ def test_oracle_apply_skeleton_and_errors(oracle):
     assert oracle.svd_error_norm(K, Vr) == pytest.approx(np.linalg.norm(K @ Vr @ Vr.T - K, 2), rel=1e-12)
     with pytest.raises(oracle.OracleError):
         oracle.mc_error(K, res.skeleton, res.P, 1.5, 2, 7)
+
+
+def test_interaction_fractions_constant_kernel(oracle):  # test_compress.cpp:180-190
+    """A kernel that evaluates to exactly one (Gaussian with an enormous bandwidth stands in for
+    the reference's polynomial kernel): fractions 1/2, 1/2, sqrt(1/2) for N = 4n."""
+    n = 40
+    ps = oracle.gen_normal(3, 4 * n, 71)
+    f = oracle.interaction_fractions(ps, 1e100, np.zeros(3), n)
+    assert f[0] == pytest.approx(0.5, rel=1e-10)
+    assert f[1] == pytest.approx(0.5, rel=1e-10)
+    assert f[2] == pytest.approx(math.sqrt(0.5), rel=1e-10)
+    with pytest.raises(oracle.OracleError):
+        oracle.interaction_fractions(ps, 1e100, np.zeros(3), 2 * n + 1)
+
+
+def test_bandwidth_search_brackets_both_branches(oracle):  # test_harness.cpp:244-266
+    seed = oracle.derive_seed(3, 0, 0xB5)
+    small = oracle.bandwidth_search(2, 4000, 100, 1.0, seed, kappa=0.2, eps=1e-2, tol_rows=2)
+    assert small[4] and abs(small[2] - 20) <= 2
+    large = oracle.bandwidth_search(2, 4000, 100, 1.0, seed, kappa=0.2, eps=1e-2, tol_rows=2, large_h=True)
+    assert large[4] and large[0] > small[0]
