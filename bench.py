@@ -430,7 +430,9 @@ def run_next_pass(args):
     item 1) with C = V_perp of the config's sample (rank r by its eps): per (target, source) entry
     eval 3d + 33, ||K||^2 2, D = K V_perp 2n, D^T D n(n+1)/m (n = m - r).
     --pass tsqr: the TSQR factor of the full K (kid_tsqr_r): eval 3d + 33 and
-    the Householder fold ~2m per entry."""
+    the Householder fold ~2m per entry.
+    --pass rownorms: the EuclideanNorm weights ||K_i|| (kid_row_norms, sampling.hpp:189-196, K2):
+    3d + 35 per entry."""
     import torch
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -456,6 +458,12 @@ def run_next_pass(args):
         fpe = 3 * d + 33 + 2 + 2 * n + n * (n + 1) / m
         kern, metric = "k_proj_gram", "compress_svd error-pass entries/s (targets x sources, FP64)"
         extra = {"rank": r, "n_perp": n}
+    elif args.pass_ == "rownorms":
+        wv = torch.empty(max(prob.nt, 1), dtype=torch.float64, device="cuda")
+        fn = lambda: dev.row_norms_dev(prob.h, wv.data_ptr())
+        fpe = 3 * d + 35
+        kern, metric = "k_row_norms", "EuclideanNorm row-norm entries/s (targets x sources, FP64)"
+        extra = {}
     else:
         R = torch.empty(m * m, dtype=torch.float64, device="cuda")
         fn = lambda: dev.tsqr_r_dev(prob.h, R.data_ptr())
@@ -616,7 +624,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=50000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr"])
+    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -624,7 +632,7 @@ def main():
         run_reference(args)
     elif args.pass_ == "split":
         run_split(args)
-    elif args.pass_ in ("svd", "tsqr"):
+    elif args.pass_ in ("svd", "tsqr", "rownorms"):
         run_next_pass(args)
     elif args.pass_ == "apply":
         run_apply(args)

@@ -251,6 +251,9 @@ class Device:
         self._ck(self.L.kid_row_norms(self.h, h, w), "kid_row_norms")
         return w[: self.nt].copy()
 
+    def row_norms_dev(self, h: float, d_w: int):
+        self._ck(self.L.kid_row_norms_dev(self.h, h, d_w), "kid_row_norms_dev")
+
     def gram(self, h: float):
         G = np.zeros(self.m * self.m)
         sk = C.c_double()
