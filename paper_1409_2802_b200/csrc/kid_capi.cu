@@ -141,6 +141,9 @@ void kid_destroy(kid_ctx* c) {
   if (c->hbuf) cudaFreeHost(c->hbuf);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   if (c->blas) cublasDestroy(c->blas);
+  for (cudaEvent_t e : c->aux_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }

@@ -201,6 +201,8 @@ struct kid_ctx {
   size_t hbuf_cap = 0;
   int64_t* counter = nullptr;  // device counters [8]
   cublasHandle_t blas = nullptr;  // large-m fallback of the Gram passes
+  cudaStream_t aux_stream = nullptr;  // large-m path: K-batch evaluation overlapping the DGEMMs
+  cudaEvent_t aux_ev[5] = {};
   void* sort_tmp = nullptr;       // CUB radix-sort temporary storage (pass 1)
   size_t sort_tmp_cap = 0;
 

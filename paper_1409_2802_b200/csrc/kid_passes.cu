@@ -1208,34 +1208,63 @@ __global__ void __launch_bounds__(256) k_eval_batch(TargetView tv, int d_rt, con
   }
 }
 
-// out = [tr(G), sum_K2, G] with G symmetrised from the upper triangle
-__global__ void k_large_finish(double* __restrict__ G, int n, const double* __restrict__ sk_part, int nsk,
-                               double* __restrict__ out) {
+// out = [tr(G), sum_K2, G] with G symmetrised from the upper triangle. Block 0 also folds the
+// ||K||^2 partials: lane-strided sums, then a fixed shuffle / warp order (deterministic).
+__global__ void __launch_bounds__(256) k_large_finish(double* __restrict__ G, int n, const double* __restrict__ sk_part,
+                                                      int nsk, double* __restrict__ out) {
   const int64_t total = (int64_t)n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int x = (int)(e % n), y = (int)(e / n);
     out[2 + e] = x <= y ? G[x + (int64_t)y * n] : G[y + (int64_t)x * n];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double tr = 0.0, sk = 0.0;
-    for (int x = 0; x < n; ++x) tr += G[x + (int64_t)x * n];
-    for (int b = 0; b < nsk; ++b) sk += sk_part[b];
-    out[0] = tr;
-    out[1] = sk;
+  if (blockIdx.x == 0) {
+    __shared__ double red[8];
+    double sk = 0.0;
+    for (int b = threadIdx.x; b < nsk; b += blockDim.x) sk += sk_part[b];
+    sk = warp_sum(sk);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sk;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tr = 0.0, t = 0.0;
+      for (int x = 0; x < n; ++x) tr += G[x + (int64_t)x * n];
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      out[0] = tr;
+      out[1] = t;
+    }
   }
 }
 
 // G (n x n, full) = D^T D (+ G when accumulate) for a tall D (rows x n, col-major, ld): cuBLAS'
 // SYRK parallelises over output tiles only, which for n << rows leaves most SMs idle (one 3.5 ms
 // call per 262k x 47 batch at c5); here the rows are split into nch chunks, one strided-batched
-// DGEMM computes the per-chunk D_c^T D_c, and a fixed-order sum folds them (bitwise reproducible).
-__global__ void k_sum_partials(const double* __restrict__ part, int nparts, int64_t len, double* __restrict__ G,
-                               bool accumulate) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
-    double acc = accumulate ? G[e] : 0.0;
+// DGEMM computes the per-chunk D_c^T D_c, and a fixed-order sum folds them (bitwise reproducible):
+// 32 elements x 8 part groups per block, groups combined in order.
+__global__ void __launch_bounds__(256) k_sum_partials(const double* __restrict__ part, int nparts, int64_t len,
+                                                      double* __restrict__ G, bool accumulate) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < len; base += (int64_t)gridDim.x * 32) {
+    const int64_t e = base + lane;
     double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += part[(size_t)p * len + e];
-    G[e] = acc + s;
+    if (e < len)
+      for (int p = g; p < nparts; p += 8) s += part[(size_t)p * len + e];
+    red[g][lane] = s;
+    __syncthreads();
+    if (g == 0 && e < len) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += red[q][lane];
+      G[e] = (accumulate ? G[e] : 0.0) + t;
+    }
+    __syncthreads();
+  }
+}
+
+// P2 row-major (r x SP) -> column-major (r x meff) for the DGEMM
+__global__ void k_p2_colmajor(const double* __restrict__ P2, int r, int SP, int meff, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)r * meff;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e % r), nn = (int)(e / r);
+    out[e] = P2[(size_t)k * SP + nn];
   }
 }
 
@@ -1257,7 +1286,7 @@ int tall_syrk(kid_ctx* c, const double* D, int rows, int ld, int n, double* G, b
       return fail(c, KID_E_CUDA, "cublasDgemm failed");
     c->launches++;
   }
-  k_sum_partials<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nn + 255) / 256, c->sms * 4)), 256, 0, c->stream>>>(
+  k_sum_partials<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nn + 31) / 32, c->sms * 8)), 256, 0, c->stream>>>(
       part, nch + (rem > 0 ? 1 : 0), nn, G, accumulate);
   KID_LAUNCHED(c);
   return KID_OK;
@@ -1269,10 +1298,15 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   if (!c->blas) {
     if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return fail(c, KID_E_CUDA, "cublasCreate failed");
   }
+  if (!c->aux_stream) {
+    KID_CK(c, cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 5; ++i) KID_CK(c, cudaEventCreateWithFlags(&c->aux_ev[i], cudaEventDisableTiming));
+  }
   cublasSetStream(c->blas, c->stream);
   cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
   const int64_t nt = c->nt;
-  // batch of B target rows: a 1 GB transient K buffer (HBM holds 180 GB)
+  // batches of B target rows through two 1 GB K buffers: the eval of batch b + 1 (aux stream, FP64
+  // exp) overlaps the DGEMM / Gram of batch b (launching stream, DMMA)
   const int B = (int)std::max<int64_t>(1024, std::min<int64_t>(nt, (int64_t)(1ll << 30) / (8ll * m)));
   const int64_t nbatch = (nt + B - 1) / B;
   const int ev_rows = (B + 255) / 256;
@@ -1281,40 +1315,52 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   const bool ev_staged = sizeof(double) * (size_t)d * ceil_to(m, 4) <= 160 * 1024;
   const size_t ev_smem = ev_staged ? sizeof(double) * (size_t)d * ceil_to(m, 4) : 0;
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
-  // scratch: K batch (B x m) | G (meff x meff) | P2 col-major (r x meff) | sk partials
+  // scratch: 2 K batches (B x m) | G (meff x meff) | P2 col-major (r x meff) | sk partials | Gram parts
   const size_t kb = (size_t)B * m, gb = (size_t)meff * meff, pb = (size_t)std::max<int64_t>(r, 1) * meff;
-  char* base = (char*)scratch(c, sizeof(double) * (kb + gb + pb + (size_t)nbatch * ev_blocks + (size_t)kSyrkParts * gb + 64));
+  char* base = (char*)scratch(c, sizeof(double) * (2 * kb + gb + pb + (size_t)nbatch * ev_blocks + (size_t)kSyrkParts * gb + 64));
   if (!base) return KID_E_OOM;
-  double* Kb = (double*)base;
-  double* G = Kb + kb;
+  double* Kbuf[2] = {(double*)base, (double*)base + kb};
+  double* G = Kbuf[1] + kb;
   double* P2c = G + gb;
   double* skp = P2c + pb;
   double* gpart = skp + (size_t)nbatch * ev_blocks;
-  if (r > 0) {  // P2 (row-major r x SP on the device) -> column-major r x meff
-    const int SP = frag_stride(meff);
-    std::vector<double> h_row((size_t)r * SP), h_col((size_t)r * meff);
-    KID_CK(c, cudaMemcpyAsync(h_row.data(), c->P2, sizeof(double) * h_row.size(), cudaMemcpyDeviceToHost, c->stream));
-    KID_CK(c, cudaStreamSynchronize(c->stream));
-    for (int64_t k = 0; k < r; ++k)
-      for (int n = 0; n < meff; ++n) h_col[k + (size_t)n * r] = h_row[k * SP + n];
-    KID_CK(c, cudaMemcpyAsync(P2c, h_col.data(), sizeof(double) * h_col.size(), cudaMemcpyHostToDevice, c->stream));
+  if (r > 0) {
+    k_p2_colmajor<<<(unsigned)std::min<int64_t>(((int64_t)r * meff + 255) / 256, 1024), 256, 0, c->stream>>>(
+        c->P2, (int)r, frag_stride(meff), meff, P2c);
+    KID_LAUNCHED(c);
   }
   const double* src = r > 0 ? c->src_perm : c->src;
   const double cscale = std::sqrt(1.0 / (2.0 * h * h));
   const double one = 1.0, mone = -1.0;
+  cudaEvent_t ev_start = c->aux_ev[0], ev_eval[2] = {c->aux_ev[1], c->aux_ev[2]}, ev_free[2] = {c->aux_ev[3], c->aux_ev[4]};
   prof_begin(c);
-  for (int64_t b = 0; b < nbatch; ++b) {
+  KID_CK(c, cudaEventRecord(ev_start, c->stream));
+  KID_CK(c, cudaStreamWaitEvent(c->aux_stream, ev_start, 0));
+  auto eval = [&](int64_t b) -> int {
     const int64_t t0 = b * (int64_t)B;
     const int rows = (int)std::min<int64_t>(B, nt - t0);
-#define LAUNCH(DD)                                                                                        \
-  {                                                                                                       \
-    cudaFuncSetAttribute(k_eval_batch<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ev_smem);     \
-    k_eval_batch<DD><<<dim3(ev_rows, ev_cols), 256, ev_smem, c->stream>>>(view(c), d, src, m, cscale, t0, rows, \
-                                                                         Kb, skp + b * ev_blocks, ev_staged); \
+    if (b >= 2) KID_CK(c, cudaStreamWaitEvent(c->aux_stream, ev_free[b & 1], 0));
+#define LAUNCH(DD)                                                                                         \
+  {                                                                                                        \
+    cudaFuncSetAttribute(k_eval_batch<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ev_smem);      \
+    k_eval_batch<DD><<<dim3(ev_rows, ev_cols), 256, ev_smem, c->aux_stream>>>(view(c), d, src, m, cscale, t0, rows, \
+                                                                             Kbuf[b & 1], skp + b * ev_blocks, ev_staged); \
   }
     KID_DISPATCH_D(d, LAUNCH)
 #undef LAUNCH
     KID_LAUNCHED(c);
+    KID_CK(c, cudaEventRecord(ev_eval[b & 1], c->aux_stream));
+    return KID_OK;
+  };
+  if (nbatch > 0)
+    if (int rc = eval(0)) return rc;
+  for (int64_t b = 0; b < nbatch; ++b) {
+    if (b + 1 < nbatch)
+      if (int rc = eval(b + 1)) return rc;
+    const int64_t t0 = b * (int64_t)B;
+    const int rows = (int)std::min<int64_t>(B, nt - t0);
+    double* Kb = Kbuf[b & 1];
+    KID_CK(c, cudaStreamWaitEvent(c->stream, ev_eval[b & 1], 0));
     double* KN = Kb + (size_t)r * rows;  // non-skeleton columns follow the r skeleton columns
     if (r > 0) {
       if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, meff, (int)r, &mone, Kb, rows, P2c, (int)r, &one, KN,
@@ -1323,6 +1369,7 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
       c->launches++;
     }
     if (int rc = tall_syrk(c, KN, rows, rows, meff, G, b > 0, gpart, kSyrkParts)) return rc;
+    KID_CK(c, cudaEventRecord(ev_free[b & 1], c->stream));
   }
   prof_end(c);
   k_large_finish<<<std::max(1, std::min(c->sms * 4, (meff * meff + 255) / 256)), 256, 0, c->stream>>>(
