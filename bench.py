@@ -576,24 +576,35 @@ def cpu_baseline(prob, budget_s=15.0):
                       f"reference's Eigen build), {dt:.1f} s"}
 
 
+class OracleProblem:
+    """The same trial as our arm (harness seed streams), set up on the host by the oracle alone:
+    points, RandomPoint center, split, EuclideanNorm sample, host ID -- no device code."""
+
+    def __init__(self, wl, threads, seed=1):
+        from oracle import oracle as O
+        d, N, m, xi = wl["d"], wl["N"], wl["m"], wl["xi"]
+        data_seed = O.derive_seed(seed, 0, 0)
+        t = O.prepare_trial(d, N, m, xi, data_seed, h_value=wl["h_value"])
+        self.wl, self.h, self.nt = wl, t.h, t.targets.shape[0]
+        self.targets_sample, self.sources = t.targets, t.sources
+        w = np.concatenate([O.row_norms(O.kernel_matrix(t.targets[i:i + 100_000], t.sources, t.h, threads=threads))
+                            for i in range(0, self.nt, 100_000)])
+        rows = O.sample_rows(O.SCHEME_EUCLIDEAN, self.nt, wl["s"], O.derive_seed(data_seed, 0, 1), w)
+        Ks = O.kernel_matrix(t.targets[rows], t.sources, t.h, threads=threads)
+        r = O.epsilon_rank(O.singular_values(Ks), wl["eps"])
+        self.skel, self.P = O.interpolative_decomposition(Ks, r)
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU implementation of the path (oracle port, since the
-    reference needs Eigen which is absent) on this arm's config, rank 0 only."""
+    """--impl reference: the reference's CPU implementation of the path (the oracle port: the
+    reference itself needs Eigen, absent here) on this arm's config and trial, rank 0 only, all
+    host threads. Setup and timed region are host-only (no device code)."""
     ws, rank, local = dist_env()
     if rank != 0:
         return
-    import torch
     wl = WORKLOADS[args.config]
-    torch.cuda.set_device(local)
-    from paper_1409_2802_b200._lib import Device
-    # the skeleton / P fed to the error path come from the same trial as our arm
-    dev = Device(local)
-    prob = Problem(wl, dev, torch, 1, 0)
-    prob.split()
-    prob.skeleton()
-    _prep_cpu(prob)
-    dev.close()
     threads = os.cpu_count() or 1
+    prob = OracleProblem(wl, threads)
     rows = args.ref_rows
     for _ in range(args.warmup):
         reference_pipeline_sample(prob, rows, threads)
@@ -608,7 +619,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"BASELINE configs[1] {args.config}"},
+            "config": {"workload": f"BASELINE configs[1] {args.config}", "skeleton_rank": int(len(prob.skel))},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
