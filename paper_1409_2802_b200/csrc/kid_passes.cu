@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(kPT, 1) k_proj_gram(const ProjArgs A) {
 // of upper-triangular factors) until one R remains. R is unique up to row signs; its singular
 // values and right singular vectors are those of K.
 constexpr int kQW = 16, kQThreads = kQW * 32;
-constexpr int kQCols = 4;  // owned columns updated together (independent shuffle reductions)
+constexpr int kQB = 8;  // panel width (one DMMA block)
 
 struct TsqrArgs {
   TargetView tv;       // EVAL mode: rows of K(T, S)
@@ -833,28 +833,43 @@ struct TsqrArgs {
 };
 
 size_t tsqr_smem_bytes(int m, int d, int rows) {
-  const int m4 = ceil_to(m, 4);
-  return sizeof(double) * ((size_t)m * m + (size_t)m4 * rows + (size_t)d * m4);
+  const int m8 = ceil_to(m, 8), m4 = ceil_to(m, 4);
+  return sizeof(double) * ((size_t)m * (m + 1) / 2 + (size_t)m8 * (rows + 4) + (size_t)kQB * (rows + 4) +
+                           2 * (size_t)kQB * (m8 + 4) + (size_t)d * m4);
 }
 
-// ROWS-row tiles (ROWS / 32 rows per lane). Per column step j the reflector parameters
-// (beta, tau, 1/v0) come from shared memory, computed one step ahead by the warp that owns
-// column j: it updates column j first in step j - 1 and derives them from the updated column
-// (lookahead), so a step is one barrier plus each warp's batch of column updates.
+// Blocked (compact-WY) Householder fold of ROWS-row tiles of K into the CTA's triangular factor.
+// The reflector of column j of the stacked [R; A] touches only R[j, :] and the tile, so for a
+// panel of kQB = 8 columns j0 .. j0 + 7, Y = [e_j0 .. e_j0+7 ; V] (V = the tile parts) and
+// H_j0 ... H_j0+7 = I - Y T Y^T (T upper triangular, y_i^T y_j = v_i^T v_j):
+//   panel   warp 0, registers only (lane = tile rows lane + 32q): the 8 reflectors, V, T;
+//   W       = R[panel rows, trail] + V^T A[:, trail]   (DMMA, one 8-column block per warp);
+//   W'      = T^T W;  R[panel rows, trail] -= W'         (scalar, 8 x trail);
+//   A       -= V W'                                       (DMMA, 8x8 blocks over the warps).
+// Four barriers per panel instead of one per column; the trailing update runs on the FP64
+// tensor pipe. R is kept column-packed (R[j][k] at k(k+1)/2 + j) in shared memory.
 template <int D, bool EVAL, int ROWS>
 __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
-  constexpr int RL = ROWS / 32;  // rows per lane
+  constexpr int RL = ROWS / 32;   // tile rows per lane in the panel warp
+  constexpr int SA = ROWS + 4;    // tile column stride (= 4 mod 16: conflict-free DMMA gathers)
   const int d = D ? D : A.d;
-  const int m = A.m, m4 = ceil_to(m, 4);
+  const int m = A.m, m4 = ceil_to(m, 4), m8 = ceil_to(m, 8), NBm = m8 / 8;
+  const int SW = m8 + 4;
   extern __shared__ __align__(16) double sm_q[];
-  double* sR = sm_q;                         // m x m col-major (upper triangle used)
-  double* sA = sR + (size_t)m * m;           // tile, column-major [k][i], m4 x ROWS
-  double* s_src = sA + (size_t)m4 * ROWS;    // d x m4 scaled sources (EVAL)
+  double* sR = sm_q;                          // packed upper triangle
+  double* sA = sR + m * (m + 1) / 2;          // tile [k][t], m8 x SA (columns >= m stay 0)
+  double* sV = sA + (size_t)m8 * SA;          // panel reflectors [i][t], kQB x SA
+  double* sW = sV + kQB * SA;                 // W  [i][k], kQB x SW
+  double* sW2 = sW + kQB * SW;                // -W' [i][k]
+  double* s_src = sW2 + kQB * SW;             // d x m4 scaled sources (EVAL)
   __shared__ double s_tab[kExpTabWords];
-  __shared__ double s_par[2][4];             // per step parity: beta, tau, 1/v0, live
+  __shared__ double sT[kQB][kQB];             // T (upper)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fk = lane & 3;    // DMMA fragment coordinates
+  auto rp = [](int j, int k) { return k * (k + 1) / 2 + j; };
   if (EVAL) stage_exp_table(s_tab, tid, kQThreads);
-  for (int e = tid; e < m * m; e += kQThreads) sR[e] = 0.0;
+  for (int e = tid; e < m * (m + 1) / 2; e += kQThreads) sR[e] = 0.0;
+  for (int e = tid; e < m8 * SA; e += kQThreads) sA[e] = 0.0;
   if (EVAL)
     for (int e = tid; e < d * m4; e += kQThreads) {
       const int k = e / m4, j = e - k * m4;
@@ -862,36 +877,12 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
     }
   const int64_t t_lo = A.ntiles * blockIdx.x / gridDim.x, t_hi = A.ntiles * (blockIdx.x + 1) / gridDim.x;
   const double* tabl = s_tab + lane;
-  // reflector parameters of column j from its current entries (x0 = R[j][j], a = A[:, j])
-  auto params = [&](int j, int slot) {
-    double sq = 0.0;
-#pragma unroll
-    for (int q = 0; q < RL; ++q) {
-      const double a = sA[j * ROWS + lane + 32 * q];
-      sq = fma(a, a, sq);
-    }
-    const double sig = warp_sum(sq);
-    if (lane == 0) {
-      const double x0 = sR[j + (size_t)j * m];
-      if (sig == 0.0) {
-        s_par[slot][3] = 0.0;  // H_j = I
-      } else {
-        const double nrm = sqrt(fma(x0, x0, sig));
-        const double beta = x0 >= 0.0 ? -nrm : nrm;
-        const double v0 = x0 - beta;
-        s_par[slot][0] = beta;
-        s_par[slot][1] = -v0 / beta;
-        s_par[slot][2] = 1.0 / v0;
-        s_par[slot][3] = 1.0;
-      }
-    }
-  };
   for (int64_t tile = t_lo; tile < t_hi; ++tile) {
-    __syncthreads();  // previous tile's last column step done (and the staging above)
+    __syncthreads();  // previous tile done (and the staging above)
     const int64_t row0 = tile * ROWS;
     if (EVAL) {
       constexpr int DR = D ? D : 1;
-      for (int q = 0; q < RL; ++q) {
+      for (int q = 0; q < ROWS / 32; ++q) {
         const int64_t row = row0 + lane + 32 * q;
         const bool live = row < A.nrows;
         double t[DR];
@@ -904,7 +895,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
           double kv[4] = {0.0, 0.0, 0.0, 0.0};
           for (int k = 0; k < d; ++k) {
             const double tk = D ? t[D ? k : 0] : (live ? tcoord(A.tv, row, k) * A.cscale : 0.0);
-            const double* xk = s_src + (size_t)k * m4 + j;
+            const double* xk = s_src + k * m4 + j;
             const double a0 = tk - xk[0], a1 = tk - xk[1], a2 = tk - xk[2], a3 = tk - xk[3];
             kv[0] = fma(a0, a0, kv[0]);
             kv[1] = fma(a1, a1, kv[1]);
@@ -913,7 +904,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
           }
           exp_neg_fast_n<4>(kv, tabl);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sA[(j + u) * ROWS + lane + 32 * q] = live ? kv[u] : 0.0;
+          for (int u = 0; u < 4; ++u) sA[(j + u) * SA + lane + 32 * q] = live ? kv[u] : 0.0;
         }
       }
     } else {
@@ -926,63 +917,152 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
           const int j = (int)(gr - b * m);
           v = k >= j ? A.Rin[(size_t)b * m * m + j + (size_t)k * m] : 0.0;
         }
-        sA[e] = v;
+        sA[k * SA + i] = v;
       }
     }
     __syncthreads();
-    if (warp == 0) params(0, 0);
-    __syncthreads();
-    for (int j = 0; j < m; ++j) {
-      const double* par = s_par[j & 1];
-      if (par[3] != 0.0) {  // uniform over the CTA
-        const double beta = par[0], tau = par[1], iv0 = par[2];
-        double v[RL];
+    for (int j0 = 0; j0 < m; j0 += kQB) {
+      // ---- panel: warp 0 factors columns j0 .. j0 + 7 in registers
+      if (warp == 0) {
+        double P[kQB][RL];
 #pragma unroll
-        for (int q = 0; q < RL; ++q) v[q] = sA[j * ROWS + lane + 32 * q] * iv0;
-        if (warp == j % kQW && lane == 0) sR[j + (size_t)j * m] = beta;  // nobody reads R[j][j] again
-        // owned columns k > j, k = warp (mod kQW); the owner of column j + 1 takes it first
-        int k = j + 1 + ((warp - (j + 1)) % kQW + kQW) % kQW;
-        for (; k < m; k += kQCols * kQW) {
-          double b[kQCols][RL], dot[kQCols];
+        for (int c = 0; c < kQB; ++c)
 #pragma unroll
-          for (int c = 0; c < kQCols; ++c) {
-            const int kc = k + c * kQW;
-            dot[c] = 0.0;
+          for (int q = 0; q < RL; ++q) P[c][q] = sA[(j0 + c) * SA + lane + 32 * q];
+        double tau[kQB];
 #pragma unroll
-            for (int q = 0; q < RL; ++q) {
-              b[c][q] = kc < m ? sA[kc * ROWS + lane + 32 * q] : 0.0;
-              dot[c] = fma(v[q], b[c][q], dot[c]);
-            }
+        for (int j = 0; j < kQB; ++j) {
+          double sq = 0.0;
+#pragma unroll
+          for (int q = 0; q < RL; ++q) sq = fma(P[j][q], P[j][q], sq);
+          const double sig = warp_sum(sq);
+          const bool col = j0 + j < m;
+          const double x0 = col ? sR[rp(j0 + j, j0 + j)] : 0.0;
+          double beta = x0, iv0 = 0.0;
+          tau[j] = 0.0;
+          if (sig != 0.0) {
+            const double nrm = sqrt(fma(x0, x0, sig));
+            beta = x0 >= 0.0 ? -nrm : nrm;
+            const double v0 = x0 - beta;
+            tau[j] = -v0 / beta;
+            iv0 = 1.0 / v0;
+          }
+#pragma unroll
+          for (int q = 0; q < RL; ++q) P[j][q] *= iv0;  // v_j
+          double dot[kQB];
+#pragma unroll
+          for (int k = j + 1; k < kQB; ++k) {
+            dot[k] = 0.0;
+#pragma unroll
+            for (int q = 0; q < RL; ++q) dot[k] = fma(P[j][q], P[k][q], dot[k]);
           }
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-            for (int c = 0; c < kQCols; ++c) dot[c] += __shfl_xor_sync(0xffffffffu, dot[c], o);
-          double w[kQCols];
+            for (int k = j + 1; k < kQB; ++k) dot[k] += __shfl_xor_sync(0xffffffffu, dot[k], o);
 #pragma unroll
-          for (int c = 0; c < kQCols; ++c) {
-            const int kc = k + c * kQW;
-            w[c] = kc < m ? tau * (sR[j + (size_t)kc * m] + dot[c]) : 0.0;
-            if (kc < m) {
+          for (int k = j + 1; k < kQB; ++k) {
+            const bool in = j0 + k < m;
+            const double w = in ? tau[j] * (sR[rp(j0 + j, j0 + k)] + dot[k]) : 0.0;
 #pragma unroll
-              for (int q = 0; q < RL; ++q) sA[kc * ROWS + lane + 32 * q] = fma(-w[c], v[q], b[c][q]);
-            }
+            for (int q = 0; q < RL; ++q) P[k][q] = fma(-w, P[j][q], P[k][q]);
+            __syncwarp();
+            if (lane == 0 && in) sR[rp(j0 + j, j0 + k)] -= w;
           }
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && col) sR[rp(j0 + j, j0 + j)] = beta;
+        }
+        // V to shared memory; T by the forward recurrence T[0:j, j] = -tau_j T[0:j, 0:j] (V^T v_j)
 #pragma unroll
-            for (int c = 0; c < kQCols; ++c) {
-              const int kc = k + c * kQW;
-              if (kc < m) sR[j + (size_t)kc * m] -= w[c];
-            }
+        for (int c = 0; c < kQB; ++c)
+#pragma unroll
+          for (int q = 0; q < RL; ++q) sV[c * SA + lane + 32 * q] = P[c][q];
+        double g[kQB][kQB];  // g[i][j] = v_i^T v_j, i < j
+#pragma unroll
+        for (int j = 1; j < kQB; ++j)
+#pragma unroll
+          for (int i = 0; i < j; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < RL; ++q) s = fma(P[i][q], P[j][q], s);
+            g[i][j] = s;
           }
-          if (k == j + 1) {  // lookahead: the next step's reflector from the updated column j + 1
-            __syncwarp();
-            params(j + 1, (j + 1) & 1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int j = 1; j < kQB; ++j)
+#pragma unroll
+            for (int i = 0; i < j; ++i) g[i][j] += __shfl_xor_sync(0xffffffffu, g[i][j], o);
+        double T[kQB][kQB];
+#pragma unroll
+        for (int j = 0; j < kQB; ++j) {
+#pragma unroll
+          for (int i = 0; i < kQB; ++i) T[i][j] = 0.0;
+          T[j][j] = tau[j];
+#pragma unroll
+          for (int i = 0; i < j; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = i; l < j; ++l) s = fma(T[i][l], g[l][j], s);
+            T[i][j] = -tau[j] * s;
           }
         }
-      } else if (j + 1 < m && warp == (j + 1) % kQW) {
-        params(j + 1, (j + 1) & 1);
+        // lane l writes T rows l / 8 and l / 8 + 4 (compile-time register indices only)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int i = lane / kQB + 4 * h2, j = lane % kQB;
+          double tv = 0.0;
+#pragma unroll
+          for (int a = 0; a < kQB; ++a)
+#pragma unroll
+            for (int b = 0; b < kQB; ++b)
+              if (a == i && b == j) tv = T[a][b];
+          sT[i][j] = tv;
+        }
+      }
+      __syncthreads();
+      const int kt = j0 + kQB;  // first trailing column
+      if (kt >= m) continue;
+      const int NBt = (m8 - kt) / 8;
+      // ---- W = R[panel rows, trail] + V^T A[:, trail]: warp w -> 8-column block w (two chains)
+      for (int nb = warp; nb < NBt; nb += kQW) {
+        double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+        const double* pa = sV + fr * SA + fk;
+        const double* pb = sA + (size_t)(kt + nb * 8 + fr) * SA + fk;
+#pragma unroll 4
+        for (int k0 = 0; k0 < ROWS; k0 += 8) {
+          dmma884(c0[0], c0[1], pa[k0], pb[k0]);
+          dmma884(c1[0], c1[1], pa[k0 + 4], pb[k0 + 4]);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int k = kt + nb * 8 + 2 * fk + e;
+          const double r = k < m ? sR[rp(j0 + fr, k)] : 0.0;
+          sW[fr * SW + k] = c0[e] + c1[e] + r;
+        }
+      }
+      __syncthreads();
+      // ---- W' = T^T W; R[panel rows, trail] -= W'; sW2 = -W'
+      for (int e = tid; e < kQB * (m8 - kt); e += kQThreads) {
+        const int i = e / (m8 - kt), k = kt + e % (m8 - kt);
+        double s = 0.0;
+#pragma unroll
+        for (int l = 0; l < kQB; ++l)
+          if (l <= i) s = fma(sT[l][i], sW[l * SW + k], s);
+        sW2[i * SW + k] = -s;
+        if (k < m && j0 + i < m) sR[rp(j0 + i, k)] -= s;
+      }
+      __syncthreads();
+      // ---- A[:, trail] -= V W' on DMMA: (row block, column block) units over the warps
+      for (int u = warp; u < (ROWS / 8) * NBt; u += kQW) {
+        const int rb = u % (ROWS / 8), nb = u / (ROWS / 8);
+        double* cp = sA + (size_t)(kt + nb * 8 + 2 * fk) * SA + rb * 8 + fr;
+        double c[2] = {cp[0], cp[SA]};
+#pragma unroll
+        for (int k0 = 0; k0 < kQB; k0 += 4)
+          dmma884(c[0], c[1], sV[(k0 + fk) * SA + rb * 8 + fr], sW2[(k0 + fk) * SW + kt + nb * 8 + fr]);
+        cp[0] = c[0];
+        cp[SA] = c[1];
       }
       __syncthreads();
     }
@@ -991,7 +1071,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
   double* out = A.Rout + (size_t)blockIdx.x * m * m;
   for (int e = tid; e < m * m; e += kQThreads) {
     const int k = e / m, j = e - k * m;
-    out[e] = j <= k ? sR[e] : 0.0;
+    out[e] = j <= k ? sR[rp(j, k)] : 0.0;
   }
 }
 
@@ -1708,11 +1788,11 @@ int tsqr_dev(kid_ctx* c, double h, const double* d_Rin, int64_t nR, int64_t m64,
   const int m = eval ? (int)c->m : (int)m64, d = eval ? c->d : 1;
   if (m < 1) return fail(c, KID_E_RANGE, "tsqr: requires m >= 1");
   if (m > 128) return fail(c, KID_E_DIM, "tsqr: m > 128 does not fit the shared-memory factor (use the Gram route)");
-  // 128-row tiles where the factor and the tile fit shared memory, else 64
-  const int rows = tsqr_smem_bytes(m, d, 128) <= 200 * 1024 ? 128 : 64;
+  // 128-row tiles where the factor and the tile fit shared memory (210 KB dynamic + 17 KB static), else 64
+  const int rows = tsqr_smem_bytes(m, d, 128) <= 210 * 1024 ? 128 : 64;
   const size_t smem = tsqr_smem_bytes(m, d, rows);
   const size_t smem_red = tsqr_smem_bytes(m, 1, rows);
-  if (smem > 200 * 1024) return fail(c, KID_E_DIM, "tsqr: m*d too large for shared memory");
+  if (smem > 210 * 1024) return fail(c, KID_E_DIM, "tsqr: m*d too large for shared memory");
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   const size_t mm = (size_t)m * m;
   const int64_t nrows0 = eval ? c->nt : nR * m;
