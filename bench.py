@@ -432,7 +432,9 @@ def run_next_pass(args):
     --pass tsqr: the TSQR factor of the full K (kid_tsqr_r): eval 3d + 33 and
     the Householder fold ~2m per entry.
     --pass rownorms: the EuclideanNorm weights ||K_i|| (kid_row_norms, sampling.hpp:189-196, K2):
-    3d + 35 per entry."""
+    3d + 35 per entry.
+    --pass gram: K^T K of the full block (kid_gram, the right factor / leverage Gram, K3):
+    3d + 33 + (m + 1) per entry."""
     import torch
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -458,6 +460,12 @@ def run_next_pass(args):
         fpe = 3 * d + 33 + 2 + 2 * n + n * (n + 1) / m
         kern, metric = "k_proj_gram", "compress_svd error-pass entries/s (targets x sources, FP64)"
         extra = {"rank": r, "n_perp": n}
+    elif args.pass_ == "gram":
+        G = torch.empty(2 + m * m, dtype=torch.float64, device="cuda")
+        fn = lambda: dev.gram_dev(prob.h, G.data_ptr())
+        fpe = 3 * d + 33 + (m + 1)
+        kern, metric = "k_gram (mode K) / large-m batched Gram", "Gram K^T K entries/s (targets x sources, FP64)"
+        extra = {}
     elif args.pass_ == "rownorms":
         wv = torch.empty(max(prob.nt, 1), dtype=torch.float64, device="cuda")
         fn = lambda: dev.row_norms_dev(prob.h, wv.data_ptr())
@@ -635,7 +643,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=50000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms"])
+    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms", "gram"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -643,7 +651,7 @@ def main():
         run_reference(args)
     elif args.pass_ == "split":
         run_split(args)
-    elif args.pass_ in ("svd", "tsqr", "rownorms"):
+    elif args.pass_ in ("svd", "tsqr", "rownorms", "gram"):
         run_next_pass(args)
     elif args.pass_ == "apply":
         run_apply(args)

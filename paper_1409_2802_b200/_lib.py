@@ -260,6 +260,10 @@ class Device:
         self._ck(self.L.kid_gram(self.h, h, G, C.byref(sk)), "kid_gram")
         return G.reshape(self.m, self.m).T.copy(), sk.value
 
+    def gram_dev(self, h: float, d_out: int):
+        """d_out (device) <- [sumsq_K, sumsq_K, K^T K (m x m)] (kid_gram_dev)."""
+        self._ck(self.L.kid_gram_dev(self.h, h, d_out, None), "kid_gram_dev")
+
     def leverage(self, h: float, W: np.ndarray) -> np.ndarray:
         r = W.shape[1]
         out = np.zeros(max(self.nt, 1))

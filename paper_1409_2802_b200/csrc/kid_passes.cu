@@ -1320,7 +1320,7 @@ __global__ void __launch_bounds__(256) k_large_finish(double* __restrict__ G, in
 // DGEMM computes the per-chunk D_c^T D_c, and a fixed-order sum folds them (bitwise reproducible):
 // 32 elements x 8 part groups per block, groups combined in order.
 __global__ void __launch_bounds__(256) k_sum_partials(const double* __restrict__ part, int nparts, int64_t len,
-                                                      double* __restrict__ G, bool accumulate) {
+                                                      double* __restrict__ G, bool accumulate, int rows_c, int ldG) {
   __shared__ double red[8][33];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   for (int64_t base = (int64_t)blockIdx.x * 32; base < len; base += (int64_t)gridDim.x * 32) {
@@ -1333,7 +1333,8 @@ __global__ void __launch_bounds__(256) k_sum_partials(const double* __restrict__
     if (g == 0 && e < len) {
       double t = 0.0;
       for (int q = 0; q < 8; ++q) t += red[q][lane];
-      G[e] = (accumulate ? G[e] : 0.0) + t;
+      const int64_t ge = e % rows_c + (e / rows_c) * ldG;  // (rows_c x ...) block of G, leading dim ldG
+      G[ge] = (accumulate ? G[ge] : 0.0) + t;
     }
     __syncthreads();
   }
@@ -1353,22 +1354,30 @@ int tall_syrk(kid_ctx* c, const double* D, int rows, int ld, int n, double* G, b
   const double one = 1.0, zero = 0.0;
   const int nch = std::max(1, std::min(max_parts - 1, rows / 2048));
   const int chunk = rows / nch, rem = rows - nch * chunk;
-  const int64_t nn = (int64_t)n * n;
-  if (chunk > 0 &&
-      cublasDgemmStridedBatched(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, n, n, chunk, &one, D, ld, chunk, D, ld, chunk, &zero,
-                                part, n, nn, nch) != CUBLAS_STATUS_SUCCESS)
-    return fail(c, KID_E_CUDA, "cublasDgemmStridedBatched failed");
-  c->launches++;
-  if (rem > 0) {
-    const double* Dr = D + (size_t)nch * chunk;
-    if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, n, n, rem, &one, Dr, ld, Dr, ld, &zero, part + nch * nn, n) !=
-        CUBLAS_STATUS_SUCCESS)
-      return fail(c, KID_E_CUDA, "cublasDgemm failed");
-    c->launches++;
-  }
-  k_sum_partials<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nn + 31) / 32, c->sms * 8)), 256, 0, c->stream>>>(
-      part, nch + (rem > 0 ? 1 : 0), nn, G, accumulate);
-  KID_LAUNCHED(c);
+  // n > 128: only the upper block triangle of 128-column blocks (the full Gram by GEMM would
+  // double the flops: 10 of 16 block pairs at n = 512, 3 of 4 at n = 256)
+  const int bs = n > 128 ? 128 : n;
+  for (int i0 = 0; i0 < n; i0 += bs)
+    for (int j0 = i0; j0 < n; j0 += bs) {
+      const int ni = std::min(bs, n - i0), nj = std::min(bs, n - j0);
+      const int64_t nn = (int64_t)ni * nj;
+      const double* Di = D + (size_t)i0 * ld;
+      const double* Dj = D + (size_t)j0 * ld;
+      if (chunk > 0 &&
+          cublasDgemmStridedBatched(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ni, nj, chunk, &one, Di, ld, chunk, Dj, ld, chunk,
+                                    &zero, part, ni, nn, nch) != CUBLAS_STATUS_SUCCESS)
+        return fail(c, KID_E_CUDA, "cublasDgemmStridedBatched failed");
+      c->launches++;
+      if (rem > 0) {
+        if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ni, nj, rem, &one, Di + (size_t)nch * chunk, ld,
+                        Dj + (size_t)nch * chunk, ld, &zero, part + nch * nn, ni) != CUBLAS_STATUS_SUCCESS)
+          return fail(c, KID_E_CUDA, "cublasDgemm failed");
+        c->launches++;
+      }
+      k_sum_partials<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nn + 31) / 32, c->sms * 8)), 256, 0,
+                       c->stream>>>(part, nch + (rem > 0 ? 1 : 0), nn, G + i0 + (size_t)j0 * n, accumulate, ni, n);
+      KID_LAUNCHED(c);
+    }
   return KID_OK;
 }
 constexpr int kSyrkParts = 297;
