@@ -434,7 +434,9 @@ def run_next_pass(args):
     --pass rownorms: the EuclideanNorm weights ||K_i|| (kid_row_norms, sampling.hpp:189-196, K2):
     3d + 35 per entry.
     --pass gram: K^T K of the full block (kid_gram, the right factor / leverage Gram, K3):
-    3d + 33 + (m + 1) per entry."""
+    3d + 33 + (m + 1) per entry.
+    --pass leverage: l_i = ||K_i W||^2 (kid_leverage, lowrank.hpp:304-305, K4) with an m x r
+    orthonormal W, r = the config's ID rank: 3d + 33 + 2r per entry."""
     import torch
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -466,6 +468,15 @@ def run_next_pass(args):
         fpe = 3 * d + 33 + (m + 1)
         kern, metric = "k_gram (mode K) / large-m batched Gram", "Gram K^T K entries/s (targets x sources, FP64)"
         extra = {}
+    elif args.pass_ == "leverage":
+        rl = max(1, prob.r)
+        Wm = np.linalg.qr(np.random.default_rng(0).standard_normal((m, rl)))[0]
+        Wd = torch.tensor(np.ascontiguousarray(Wm.T).ravel(), dtype=torch.float64, device="cuda")  # m x r col-major
+        lv = torch.empty(max(prob.nt, 1), dtype=torch.float64, device="cuda")
+        fn = lambda: dev.leverage_dev(prob.h, Wd.data_ptr(), rl, lv.data_ptr())
+        fpe = 3 * d + 33 + 2 * rl
+        kern, metric = "k_leverage", "leverage-score entries/s (targets x sources, FP64)"
+        extra = {"rank": rl}
     elif args.pass_ == "rownorms":
         wv = torch.empty(max(prob.nt, 1), dtype=torch.float64, device="cuda")
         fn = lambda: dev.row_norms_dev(prob.h, wv.data_ptr())
@@ -643,7 +654,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=50000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms", "gram"])
+    ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms", "gram", "leverage"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -651,7 +662,7 @@ def main():
         run_reference(args)
     elif args.pass_ == "split":
         run_split(args)
-    elif args.pass_ in ("svd", "tsqr", "rownorms", "gram"):
+    elif args.pass_ in ("svd", "tsqr", "rownorms", "gram", "leverage"):
         run_next_pass(args)
     elif args.pass_ == "apply":
         run_apply(args)

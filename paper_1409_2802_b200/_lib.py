@@ -264,6 +264,9 @@ class Device:
         """d_out (device) <- [sumsq_K, sumsq_K, K^T K (m x m)] (kid_gram_dev)."""
         self._ck(self.L.kid_gram_dev(self.h, h, d_out, None), "kid_gram_dev")
 
+    def leverage_dev(self, h: float, d_W: int, r: int, d_scores: int):
+        self._ck(self.L.kid_leverage_dev(self.h, h, d_W, r, d_scores), "kid_leverage_dev")
+
     def leverage(self, h: float, W: np.ndarray) -> np.ndarray:
         r = W.shape[1]
         out = np.zeros(max(self.nt, 1))

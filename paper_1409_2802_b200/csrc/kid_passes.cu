@@ -1861,6 +1861,68 @@ int tsqr_dev(kid_ctx* c, double h, const double* d_Rin, int64_t nR, int64_t m64,
   return KID_OK;
 }
 
+// scores[t0 + i] = sum_j KW[i + j * rows]^2 (KW rows x r column-major, coalesced over i)
+__global__ void k_rowsq(const double* __restrict__ KW, int rows, int r, double* __restrict__ scores) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < r; ++j) {
+      const double v = KW[i + (size_t)j * rows];
+      s = fma(v, v, s);
+    }
+    scores[i] = s;
+  }
+}
+
+// Leverage for W that does not fit shared memory (c4 m = 256, c5 m = 512): a 1 GB batch of K
+// rows (k_eval_batch), KW = K_b W by DGEMM (W read once per batch instead of once per tile),
+// row sums of squares.
+int leverage_dev_large(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores) {
+  const int m = (int)c->m, d = c->d, rr = (int)r;
+  if (!c->blas) {
+    if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return fail(c, KID_E_CUDA, "cublasCreate failed");
+  }
+  cublasSetStream(c->blas, c->stream);
+  cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
+  const int64_t nt = c->nt;
+  const int B = (int)std::max<int64_t>(1024, std::min<int64_t>(nt, (int64_t)(1ll << 30) / (8ll * (m + rr))));
+  const int64_t nbatch = (nt + B - 1) / B;
+  const int ev_rows = (B + 255) / 256;
+  const int ev_cols = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_to(m, 4) / 4, (4ll * c->sms + ev_rows - 1) / ev_rows));
+  const int ev_blocks = ev_rows * ev_cols;
+  const bool ev_staged = sizeof(double) * (size_t)d * ceil_to(m, 4) <= 160 * 1024;
+  const size_t ev_smem = ev_staged ? sizeof(double) * (size_t)d * ceil_to(m, 4) : 0;
+  char* base = (char*)scratch(c, sizeof(double) * ((size_t)B * (m + rr) + (size_t)ev_blocks + 64));
+  if (!base) return KID_E_OOM;
+  double* Kb = (double*)base;
+  double* KW = Kb + (size_t)B * m;
+  double* skp = KW + (size_t)B * rr;  // ||K||^2 partials (unused here)
+  const double cscale = std::sqrt(1.0 / (2.0 * h * h));
+  const double one = 1.0, zero = 0.0;
+  prof_begin(c);
+  for (int64_t b = 0; b < nbatch; ++b) {
+    const int64_t t0 = b * (int64_t)B;
+    const int rows = (int)std::min<int64_t>(B, nt - t0);
+#define LAUNCH(DD)                                                                                         \
+  {                                                                                                        \
+    cudaFuncSetAttribute(k_eval_batch<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ev_smem);      \
+    k_eval_batch<DD><<<dim3(ev_rows, ev_cols), 256, ev_smem, c->stream>>>(view(c), d, c->src, m, cscale, t0, \
+                                                                         rows, Kb, skp, ev_staged);        \
+  }
+    KID_DISPATCH_D(d, LAUNCH)
+#undef LAUNCH
+    KID_LAUNCHED(c);
+    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, rr, m, &one, Kb, rows, d_W, m, &zero, KW, rows) !=
+        CUBLAS_STATUS_SUCCESS)
+      return fail(c, KID_E_CUDA, "cublasDgemm failed");
+    c->launches++;
+    k_rowsq<<<(unsigned)std::min<int64_t>((rows + 255) / 256, (int64_t)c->sms * 8), 256, 0, c->stream>>>(KW, rows, rr,
+                                                                                                      d_scores + t0);
+    KID_LAUNCHED(c);
+  }
+  prof_end(c);
+  return KID_OK;
+}
+
 int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores) {
   if (int rc = check_block(c, h)) return rc;
   if (r < 1 || r > c->m) return fail(c, KID_E_RANGE, "leverage: requires 1 <= r <= m");
@@ -1871,7 +1933,10 @@ int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_s
   const size_t wbytes = sizeof(double) * (size_t)m4 * SW;
   bool w_in_smem = smem + wbytes <= 190 * 1024;
   if (w_in_smem) smem += wbytes;
-  if (smem > 205 * 1024) return fail(c, KID_E_DIM, "leverage: tile does not fit shared memory");
+  if (!w_in_smem || smem > 205 * 1024 || getenv("KID_FORCE_LARGE")) {
+    if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
+    return leverage_dev_large(c, h, d_W, r, d_scores);
+  }
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   LevArgs A{view(c), d, c->src, m, rr, -1.0 / (2.0 * h * h), d_W, w_in_smem, d_scores};
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;

@@ -127,6 +127,29 @@ def test_recon_error_vs_oracle(oracle, dev, d, eps, n):
     assert abs(rel - res.rel_error) <= max(1e-10 * res.rel_error, floor)
 
 
+@pytest.mark.parametrize("d,n,rs", [(16, 256, (8, 64)), (8, 200, (30,))])
+def test_leverage_large(oracle, dev, monkeypatch, d, n, rs):
+    """W beyond shared memory (c4-like m = 256, d = 16): the batched path (K batch, DGEMM K W,
+    row sums of squares); the same bar as test_leverage."""
+    t, K = _block(oracle, d=d, N=30_000, n=n)
+    dev.set_points(t.points)
+    dev.split(t.center, n, 2.0)
+    sv, V = oracle.right_factor(K)
+    for r in rs:
+        W = V[:, :r] / sv[:r]
+        ref, _ = oracle.row_leverage_scores(K, r)
+        got = dev.leverage(t.h, W)
+        assert np.max(np.abs(got - ref)) <= 1e-10 * max(1.0, ref.max())
+    monkeypatch.setenv("KID_FORCE_LARGE", "1")  # small m through the batched path too
+    t, K = _block(oracle, d=3)
+    dev.set_points(t.points)
+    dev.split(t.center, 100, 2.0)
+    sv, V = oracle.right_factor(K)
+    W = V[:, :20] / sv[:20]
+    ref, _ = oracle.row_leverage_scores(K, 20)
+    assert np.max(np.abs(dev.leverage(t.h, W) - ref)) <= 1e-10 * max(1.0, ref.max())
+
+
 def test_leverage(oracle, dev):
     t, K = _block(oracle, d=3)
     dev.set_points(t.points)
