@@ -8,7 +8,7 @@
 //                 mode D: T = K_N - K_S P2  -> D^T D, ||D||_F^2 = tr(D^T D)
 //                         (compress.hpp:141-159: D = K - K[:,skel] P; the skeleton
 //                          columns of D are exactly zero because P[:, skel] = I)
-//   k_leverage    l_i = ||K_i W||^2                      lowrank.hpp:304-305
+//   k_proj_gram   LEV mode: l_i = ||K_i W||^2              lowrank.hpp:304-305
 //   k_eval_rows   K[rows, :] gathered                     compress.hpp:130-137
 // The m x m accumulators live in registers (DMMA C fragments) across all tiles of a
 // CTA's contiguous target chunk; partials are reduced in a fixed chunk order so results
@@ -539,106 +539,6 @@ __global__ void __launch_bounds__(1024) k_gram_reduce(const double* __restrict__
   }
 }
 
-// ------------------------------------------------------------------ leverage
-struct LevArgs {
-  TargetView tv;
-  int d;
-  const double* src;
-  int m, r;
-  double negc;
-  const double* W;  // m x r col-major (device)
-  bool w_in_smem;
-  double* scores;
-};
-
-template <int D>
-__global__ void __launch_bounds__(kNT) k_leverage(LevArgs A) {
-  const int d = D ? D : A.d;
-  const int m = A.m, r = A.r;
-  const int m4 = ceil_to(m, 4);
-  const int SN = frag_stride(m4);
-  const int SW = frag_stride(r);
-  const int NBR = ceil_to(r, 8) / 8;
-  extern __shared__ __align__(16) double smem[];
-  double* s_src = smem;
-  double* s_t = s_src + (size_t)d * m;
-  double* KN = s_t + (size_t)d * kTM;       // kTM x SN
-  double* rowpart = KN + (size_t)kTM * SN;  // kTM x NBR
-  double* sW = rowpart + (size_t)kTM * NBR; // m4 x SW (row-major) when w_in_smem
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ double s_tab[kExpTabWords];
-  stage_exp_table(s_tab, tid, blockDim.x);
-  const int t_init = tid / m, j_init = tid - (tid / m) * m;
-  const int step_t = kNT / m, step_j = kNT - (kNT / m) * m;
-  for (int e = tid; e < m * d; e += kNT) s_src[e] = A.src[e];
-  for (int e = tid; e < kTM * SN; e += kNT) KN[e] = 0.0;
-  if (A.w_in_smem)
-    for (int e = tid; e < m4 * SW; e += kNT) {
-      const int k = e / SW, n = e % SW;
-      sW[e] = (k < m && n < r) ? A.W[k + (size_t)n * m] : 0.0;
-    }
-  __syncthreads();
-  const int64_t ntiles = (A.tv.nt + kTM - 1) / kTM;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t t0 = tile * kTM;
-    for (int e = tid; e < kTM * d; e += kNT) {
-      const int t = e % kTM, k = e / kTM;
-      s_t[t + k * kTM] = (t0 + t < A.tv.nt) ? tcoord(A.tv, t0 + t, k) : 0.0;
-    }
-    __syncthreads();
-    const int64_t rows_left = A.tv.nt - t0;
-    for (int t = t_init, j = j_init; t < kTM;) {
-      double kv = 0.0;
-      if (t < rows_left) {
-        double sq = 0.0;
-#pragma unroll
-        for (int k = 0; k < (D ? D : 64); ++k) {
-          if (!D && k >= d) break;
-          const double diff = __dsub_rn(s_t[t + k * kTM], s_src[j + k * m]);
-          sq = __dadd_rn(sq, __dmul_rn(diff, diff));
-        }
-        kv = exp_fast(sq * A.negc, s_tab + (threadIdx.x & 31));
-      }
-      KN[t * SN + j] = kv;
-      j += step_j;
-      t += step_t;
-      if (j >= m) {
-        j -= m;
-        ++t;
-      }
-    }
-    __syncthreads();
-    for (int nb = warp; nb < NBR; nb += kNW) {
-      double c[kTM / 8][2];
-#pragma unroll
-      for (int rb = 0; rb < kTM / 8; ++rb) c[rb][0] = c[rb][1] = 0.0;
-      for (int k0 = 0; k0 < m4; k0 += 4) {
-        const int kk = k0 + (lane & 3), nn = nb * 8 + (lane >> 2);
-        const double b = A.w_in_smem ? sW[kk * SW + nn] : ((kk < m && nn < r) ? A.W[kk + (size_t)nn * m] : 0.0);
-#pragma unroll
-        for (int rb = 0; rb < kTM / 8; ++rb) {
-          const double a = KN[(rb * 8 + (lane >> 2)) * SN + k0 + (lane & 3)];
-          dmma884(c[rb][0], c[rb][1], a, b);
-        }
-      }
-#pragma unroll
-      for (int rb = 0; rb < kTM / 8; ++rb) {
-        double q = c[rb][0] * c[rb][0] + c[rb][1] * c[rb][1];
-        q += __shfl_xor_sync(0xffffffffu, q, 1);
-        q += __shfl_xor_sync(0xffffffffu, q, 2);
-        if ((lane & 3) == 0) rowpart[(rb * 8 + (lane >> 2)) * NBR + nb] = q;
-      }
-    }
-    __syncthreads();
-    if (tid < kTM && t0 + tid < A.tv.nt) {
-      double s = 0.0;
-      for (int nb = 0; nb < NBR; ++nb) s += rowpart[tid * NBR + nb];
-      A.scores[t0 + tid] = s;
-    }
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------------------------ projected Gram
 // G += (K C)^T (K C) for an arbitrary m x n coefficient matrix C, ||K C||_F^2 and ||K||_F^2.
 // The compress_svd error pass (compress.hpp:243-262): with C = V_perp, an
@@ -660,6 +560,7 @@ struct ProjArgs {
   double* partial;    // [nworkers][LG][LG]
   int LG;             // ceil8(n)
   double* partial_sk; // [nworkers] sum K^2, then [nworkers] tr(D^T D)
+  double* scores;     // LEV mode: l_i = ||(K C)_i||^2 per target (no Gram)
 };
 constexpr int kPG = 2, kPW = 8, kPT = kPG * kPW * 32;
 constexpr int kPMaxBlk = 17;  // SYRK blocks per warp: n <= 128 -> 136 upper blocks over 8 warps
@@ -669,7 +570,9 @@ size_t proj_smem_bytes(int m, int n, int d) {
   return sizeof(double) * ((size_t)m4 * frag_stride(n) + (size_t)d * m4 + (size_t)kPG * (m4 + n8) * kST);
 }
 
-template <int D>
+// LEV: the leverage pass (lowrank.hpp:304-305) -- C = W = V_r Sigma_r^-1, per target the row sum
+// of squares of K W replaces the Gram (rows of the tile summed over column blocks in order).
+template <int D, bool LEV>
 __global__ void __launch_bounds__(kPT, 1) k_proj_gram(const ProjArgs A) {
   const int d = D ? D : A.d;
   const int m = A.m, n = A.n;
@@ -750,12 +653,30 @@ __global__ void __launch_bounds__(kPT, 1) k_proj_gram(const ProjArgs A) {
         dmma884(c[0][0], c[0][1], pa[k0 * kST], b);
         dmma884(c[1][0], c[1][1], pa[k0 * kST + 8], b);
       }
+      if (LEV) {  // row partial over this block's 8 columns -> sD[nb][t]
 #pragma unroll
-      for (int rb = 0; rb < 2; ++rb)
+        for (int rb = 0; rb < 2; ++rb) {
+          double q = fma(c[rb][0], c[rb][0], c[rb][1] * c[rb][1]);
+          q += __shfl_xor_sync(0xffffffffu, q, 1);
+          q += __shfl_xor_sync(0xffffffffu, q, 2);
+          if ((lane & 3) == 0) sD[nb * kST + rh * 16 + rb * 8 + (lane >> 2)] = q;
+        }
+      } else {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) sD[(nb * 8 + 2 * (lane & 3) + e) * kST + rh * 16 + rb * 8 + (lane >> 2)] = c[rb][e];
+        for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) sD[(nb * 8 + 2 * (lane & 3) + e) * kST + rh * 16 + rb * 8 + (lane >> 2)] = c[rb][e];
+      }
     }
     nbar_sync(bar, nthr);
+    if (LEV) {  // warp 0 of the group: scores of the tile's 32 targets
+      if (gw == 0 && live) {
+        double sc = 0.0;
+        for (int nb = 0; nb < NB; ++nb) sc += sD[nb * kST + lane];
+        A.scores[row] = sc;
+      }
+      continue;
+    }
     // G += D^T D over the tile's 32 targets (8 k-steps)
 #pragma unroll
     for (int kk = 0; kk < kTM / 4; ++kk) {
@@ -772,6 +693,7 @@ __global__ void __launch_bounds__(kPT, 1) k_proj_gram(const ProjArgs A) {
       }
     }
   }
+  if (LEV) return;
   // per-worker partial: upper blocks at (a8 + row) + (b8 + col) * LG; trace from the diagonal blocks
   double tr = 0.0;
   double* P = A.partial + (size_t)worker * A.LG * A.LG;
@@ -1717,10 +1639,11 @@ int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n64, double* 
     A.partial = (double*)base;
     A.LG = LG;
     A.partial_sk = A.partial + (size_t)nworkers * LG * LG;
+    A.scores = nullptr;
 #define LAUNCH(DD)                                                                                   \
   {                                                                                                  \
-    cudaFuncSetAttribute(k_proj_gram<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
-    k_proj_gram<DD><<<blocks, kPT, smem, c->stream>>>(A);                                            \
+    cudaFuncSetAttribute(k_proj_gram<DD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_proj_gram<DD, false><<<blocks, kPT, smem, c->stream>>>(A);                                          \
   }
     prof_begin(c);
     KID_DISPATCH_D(d, LAUNCH)
@@ -1927,24 +1850,30 @@ int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_s
   if (int rc = check_block(c, h)) return rc;
   if (r < 1 || r > c->m) return fail(c, KID_E_RANGE, "leverage: requires 1 <= r <= m");
   if (c->nt == 0) return KID_OK;
-  const int m = (int)c->m, d = c->d, rr = (int)r;
-  const int m4 = ceil_to(m, 4), SN = frag_stride(m4), SW = frag_stride(rr), NBR = ceil_to(rr, 8) / 8;
-  size_t smem = sizeof(double) * ((size_t)d * m + (size_t)d * kTM + (size_t)kTM * SN + (size_t)kTM * NBR);
-  const size_t wbytes = sizeof(double) * (size_t)m4 * SW;
-  bool w_in_smem = smem + wbytes <= 190 * 1024;
-  if (w_in_smem) smem += wbytes;
-  if (!w_in_smem || smem > 205 * 1024 || getenv("KID_FORCE_LARGE")) {
-    if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
-    return leverage_dev_large(c, h, d_W, r, d_scores);
-  }
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
-  LevArgs A{view(c), d, c->src, m, rr, -1.0 / (2.0 * h * h), d_W, w_in_smem, d_scores};
+  const int m = (int)c->m, d = c->d, rr = (int)r;
+  const size_t smem = proj_smem_bytes(m, rr, d);
+  if (ceil_to(rr, 8) > 128 || smem > 200 * 1024 || getenv("KID_FORCE_LARGE"))
+    return leverage_dev_large(c, h, d_W, r, d_scores);
+  // the projected-Gram kernel in leverage mode: K tile by exp, K W on DMMA, row sums of squares
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;
-  const int blocks = (int)std::min<int64_t>(ntiles, (int64_t)c->sms * 2);
-#define LAUNCH(DD)                                                                                \
-  {                                                                                               \
-    cudaFuncSetAttribute(k_leverage<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k_leverage<DD><<<blocks, kNT, smem, c->stream>>>(A);                                          \
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms, (ntiles + kPG - 1) / kPG));
+  ProjArgs A{};
+  A.tv = view(c);
+  A.d = d;
+  A.m = m;
+  A.n = rr;
+  A.cscale = std::sqrt(1.0 / (2.0 * h * h));
+  A.src = c->src;
+  A.C = d_W;
+  A.ntiles = ntiles;
+  A.nworkers = blocks * kPG;
+  A.LG = ceil_to(rr, 8);
+  A.scores = d_scores;
+#define LAUNCH(DD)                                                                                       \
+  {                                                                                                      \
+    cudaFuncSetAttribute(k_proj_gram<DD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_proj_gram<DD, true><<<blocks, kPT, smem, c->stream>>>(A);                                          \
   }
   prof_begin(c);
   KID_DISPATCH_D(d, LAUNCH)
