@@ -235,6 +235,13 @@ int kid_split(kid_ctx* c, const double* center, int64_t n, double xi, int64_t* s
   if (n < 1 || n >= c->N) return fail(c, KID_E_RANGE, "split_sources_targets: requires 1 <= n < N");
   if (xi < 0.0) return fail(c, KID_E_RANGE, "split_sources_targets: requires xi >= 0");
   if (int rc = set_device(c)) return rc;
+  {
+    const int rc = getenv("KID_SPLIT_HOST") ? 1 : split_device(c, center, n, xi, src_idx_out, rho_out, n_targets_out);
+    if (rc == KID_OK && *n_targets_out == 0)
+      return fail(c, KID_E_NO_TARGETS,
+                  "split_sources_targets: no targets at separation xi = " + std::to_string(xi) + " (try a smaller xi)");
+    if (rc != 1) return rc;
+  }
   std::vector<double> cd(n);
   std::vector<int64_t> ci(n);
   if (int rc = split_candidates(c, center, n, cd.data(), ci.data())) return rc;

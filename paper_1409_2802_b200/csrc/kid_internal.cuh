@@ -238,6 +238,8 @@ int split_candidates(kid_ctx* c, const double* center_h, int64_t n, double* cand
                      int64_t* cand_idx_h);
 int split_finish(kid_ctx* c, const int64_t* src_idx_h, int64_t n, const double* src_pts_h, double rho,
                  double xi, int64_t* n_targets_out);
+int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64_t* src_idx_out, double* rho_out,
+                 int64_t* n_targets_out);
 int row_norms_dev(kid_ctx* c, double h, double* d_w);
 int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out);
 int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores);

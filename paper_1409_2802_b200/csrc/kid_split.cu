@@ -148,7 +148,12 @@ __global__ void __launch_bounds__(kCT) k_compact(const double* __restrict__ dist
                                                  int64_t n_src, int64_t* __restrict__ out,
                                                  unsigned long long* __restrict__ tile_status,
                                                  unsigned int* __restrict__ tile_counter,
-                                                 int64_t* __restrict__ total_out, int64_t ntiles) {
+                                                 int64_t* __restrict__ total_out, int64_t ntiles,
+                                                 const double* __restrict__ rho_dev, double xi) {
+  if (rho_dev) {  // rho from the device-side selection; cutoff = xi * rho as on the host (geometry.hpp:57)
+    rho = *rho_dev;
+    cutoff = xi * rho;
+  }
   __shared__ unsigned int tile_s;
   __shared__ long long warp_tot[kCT / 32];
   __shared__ long long excl_s;
@@ -239,6 +244,82 @@ __global__ void __launch_bounds__(kCT) k_compact(const double* __restrict__ dist
   }
 }
 
+// Device-side selection of the n sources (single CTA, the candidate count is read on the device):
+// bitonic sort of the <= kSelMax candidates by (dist, idx) -- nth_element's comparator
+// (geometry.hpp:40-47) -- rho = the n-th key (geometry.hpp:52-53), the n indices sorted ascending
+// (geometry.hpp:50-51), the source coordinates gathered. ctrl = [rho, overflow flag].
+constexpr int kSelMax = 8192, kSelT = 1024;
+__device__ __forceinline__ bool pair_gt(unsigned long long ka, unsigned long long ia, unsigned long long kb,
+                                        unsigned long long ib) {
+  return ka > kb || (ka == kb && ia > ib);
+}
+__device__ void block_bitonic(unsigned long long* key, unsigned long long* idx, int P) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool asc = (i & k) == 0;
+          const bool gt = pair_gt(key[i], idx[i], key[ixj], idx[ixj]);
+          if (gt == asc) {
+            const unsigned long long tk = key[i], ti = idx[i];
+            key[i] = key[ixj];
+            idx[i] = idx[ixj];
+            key[ixj] = tk;
+            idx[ixj] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+__global__ void __launch_bounds__(kSelT) k_split_select(const unsigned long long* __restrict__ ck,
+                                                       const unsigned long long* __restrict__ ci,
+                                                       const unsigned long long* __restrict__ count, int64_t cap,
+                                                       int nl, const double* __restrict__ pts, int64_t N, int d,
+                                                       int64_t* __restrict__ src_local, double* __restrict__ src,
+                                                       double* __restrict__ ctrl) {
+  extern __shared__ unsigned long long sel_sm[];
+  unsigned long long* key = sel_sm;
+  unsigned long long* idx = sel_sm + kSelMax;
+  const unsigned long long total = *count;
+  const unsigned long long lim = (unsigned long long)(cap < kSelMax ? cap : kSelMax);
+  const int cnt = (int)(total < lim ? total : lim);
+  if (threadIdx.x == 0) ctrl[1] = (total > lim || total < (unsigned long long)nl) ? 1.0 : 0.0;
+  int P = 1;
+  while (P < max(cnt, nl)) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    key[i] = i < cnt ? ck[i] : ~0ull;
+    idx[i] = i < cnt ? ci[i] : ~0ull;
+  }
+  __syncthreads();
+  block_bitonic(key, idx, P);
+  if (threadIdx.x == 0) ctrl[0] = __longlong_as_double((long long)key[nl - 1]);  // rho: the largest of the n
+  // the n indices ascending: keys <- indices, padded
+  int Q = 1;
+  while (Q < nl) Q <<= 1;
+  unsigned long long* k2 = key + P;  // scratch after the first P entries (P + Q <= 2 kSelMax)
+  unsigned long long* i2 = idx + P;
+  if (P + Q > kSelMax) { k2 = key; i2 = idx; }  // reuse in place (only the first nl are needed)
+  __syncthreads();
+  unsigned long long vals[kSelMax / kSelT];
+  int nv = 0;
+  for (int i = threadIdx.x; i < Q; i += blockDim.x) vals[nv++] = i < nl ? idx[i] : ~0ull;
+  __syncthreads();
+  nv = 0;
+  for (int i = threadIdx.x; i < Q; i += blockDim.x) {
+    k2[i] = vals[nv++];
+    i2[i] = 0;
+  }
+  __syncthreads();
+  block_bitonic(k2, i2, Q);
+  for (int j = threadIdx.x; j < nl; j += blockDim.x) {
+    const int64_t li = (int64_t)k2[j];
+    src_local[j] = li;
+    for (int k = 0; k < d; ++k) src[j + (int64_t)k * nl] = pts[li + k * N];
+  }
+}
+
 int sort_candidates(kid_ctx* c, unsigned long long* key, unsigned long long* idx, int64_t count,
                     unsigned long long* key_alt, unsigned long long* idx_alt, int end_bit_idx) {
   // stable LSD order: by idx first, then stably by key -> (dist, idx) lexicographic
@@ -256,6 +337,89 @@ int sort_candidates(kid_ctx* c, unsigned long long* key, unsigned long long* idx
 }
 
 }  // namespace
+
+// Single-rank split with one host synchronisation (kid_split): sample threshold, distances and
+// candidates, device-side selection (k_split_select), compaction with rho read on the device.
+// Returns 1 (not taken: fall back to split_candidates / split_finish) when the candidate buffer
+// would exceed one CTA's sort or overflowed.
+int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64_t* src_idx_out, double* rho_out,
+                 int64_t* n_targets_out) {
+  const int64_t N = c->N;
+  const int d = c->d;
+  if (!c->pts || N < 1 || d > 64 || n > kSelT || n > N) return 1;
+  const int64_t nl = n;
+  const int64_t S = N <= std::max<int64_t>(kSampleMax, 4 * nl) ? N : std::max<int64_t>(kSampleMax, 4 * nl);
+  int64_t cap = std::max<int64_t>(4 * nl + 1024, (int64_t)((double)N * (double)nl / (double)S * 2.0) + 4096);
+  cap = std::min<int64_t>(cap, N);
+  if (cap > kSelMax) return 1;
+  if (ensure(c, (void**)&c->dist, &c->dist_cap, sizeof(double) * N)) return KID_E_OOM;
+  if (ensure(c, (void**)&c->tgt_idx, &c->tgt_cap, sizeof(int64_t) * N)) return KID_E_OOM;
+  if (ensure(c, (void**)&c->src, &c->src_cap, sizeof(double) * n * d)) return KID_E_OOM;
+  const int64_t ntiles = (N + kTile - 1) / kTile;
+  // scratch: center | ctrl | count | tile status | sample keys (2x) | candidates | src_local
+  const size_t bytes = 512 + 64 + 16 + sizeof(unsigned long long) * (ntiles + 8) + 2 * sizeof(unsigned long long) * S +
+                       2 * sizeof(unsigned long long) * cap + sizeof(int64_t) * (n + 8);
+  char* base = (char*)scratch(c, bytes);
+  if (!base) return KID_E_OOM;
+  double* center = (double*)base;
+  double* ctrl = (double*)(base + 512);
+  unsigned long long* count = (unsigned long long*)(base + 512 + 64);
+  unsigned long long* status = count + 2;
+  unsigned long long* skeys = status + ntiles + 8;
+  unsigned long long* skeys2 = skeys + S;
+  unsigned long long* ck = skeys2 + S;
+  unsigned long long* ci = ck + cap;
+  int64_t* src_local = (int64_t*)(ci + cap);
+  KID_CK(c, cudaMemcpyAsync(center, center_h, sizeof(double) * d, cudaMemcpyHostToDevice, c->stream));
+  KID_CK(c, cudaMemsetAsync(count, 0, sizeof(unsigned long long) * (2 + ntiles + 8), c->stream));
+  KID_CK(c, cudaMemsetAsync(c->counter, 0, sizeof(int64_t) * 2, c->stream));
+  k_sample_keys<<<(unsigned)((S + 255) / 256), 256, 0, c->stream>>>(c->pts, N, d, center, S, skeys);
+  KID_LAUNCHED(c);
+  size_t tmpb = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmpb, skeys, skeys2, (int)S, 0, 64, c->stream);
+  if (ensure(c, &c->sort_tmp, &c->sort_tmp_cap, tmpb)) return KID_E_OOM;
+  KID_CK(c, cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmpb, skeys, skeys2, (int)S, 0, 64, c->stream));
+  c->launches += 4;
+  prof_begin(c);
+  k_dist_cand<<<c->sms * 8, 256, 0, c->stream>>>(c->pts, N, d, center, skeys2 + (nl - 1), c->dist, ck, ci, count, cap);
+  prof_end(c);
+  KID_LAUNCHED(c);
+  const size_t sel_smem = 2 * sizeof(unsigned long long) * kSelMax;
+  cudaFuncSetAttribute(k_split_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
+  k_split_select<<<1, kSelT, sel_smem, c->stream>>>(ck, ci, count, cap, (int)nl, c->pts, N, d, src_local, c->src, ctrl);
+  KID_LAUNCHED(c);
+  prof_begin(c);
+  k_compact<<<(unsigned)ntiles, kCT, 0, c->stream>>>(c->dist, N, 0.0, 0.0, src_local, nl, c->tgt_idx, status,
+                                                     (unsigned int*)c->counter, c->counter + 1, ntiles, ctrl, xi);
+  prof_end(c);
+  KID_LAUNCHED(c);
+  // one D2H of [rho, overflow | nt | source indices | source coordinates] and one synchronisation
+  const size_t hb = sizeof(double) * (2 + 1 + (size_t)n + (size_t)n * d);
+  if (ensure_pinned(c, hb)) return KID_E_OOM;
+  double* h = c->hbuf;
+  KID_CK(c, cudaMemcpyAsync(h, ctrl, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaMemcpyAsync(h + 2, c->counter + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaMemcpyAsync(h + 3, src_local, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaMemcpyAsync(h + 3 + n, c->src, sizeof(double) * n * d, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  if (h[1] != 0.0) return 1;  // candidate overflow (adversarial ordering): the general path
+  int64_t nt = 0;
+  std::memcpy(&nt, h + 2, sizeof(int64_t));
+  const int64_t* sl = (const int64_t*)(h + 3);
+  for (int64_t k = 0; k < n; ++k) src_idx_out[k] = sl[k] + c->offset;
+  *rho_out = h[0];
+  c->src_host.assign(h + 3 + n, h + 3 + n + (size_t)n * d);
+  c->n_split_targets = nt;
+  c->tbase = c->pts;
+  c->tld = N;
+  c->tidx = c->tgt_idx;
+  c->nt = nt;
+  c->m = n;
+  c->r = 0;
+  c->sub_active = false;
+  *n_targets_out = nt;
+  return KID_OK;
+}
 
 // Local n smallest (dist, idx) keys, ascending; indices are GLOBAL (offset added).
 int split_candidates(kid_ctx* c, const double* center_h, int64_t n, double* cand_dist_h,
@@ -378,7 +542,7 @@ int split_finish(kid_ctx* c, const int64_t* src_idx_h, int64_t n, const double* 
   const double cutoff = xi * rho;  // geometry.hpp:57
   prof_begin(c);
   k_compact<<<(unsigned)ntiles, kCT, 0, c->stream>>>(c->dist, N, cutoff, rho, src_local, nloc, c->tgt_idx, status,
-                                                     (unsigned int*)c->counter, c->counter + 1, ntiles);
+                                                     (unsigned int*)c->counter, c->counter + 1, ntiles, nullptr, 0.0);
   prof_end(c);
   KID_LAUNCHED(c);
   int64_t nt = 0;
