@@ -35,6 +35,17 @@ __device__ __forceinline__ double point_dist(const double* __restrict__ pts, int
   return __dsqrt_rn(acc);
 }
 
+// 32-bit sample keys: the distance rounded UP to float (monotone), so the n-th smallest of them,
+// widened back to double, still bounds the n-th smallest sample distance from above -- half the
+// radix passes of the 64-bit keys.
+__global__ void k_sample_keys32(const double* __restrict__ pts, int64_t N, int d, const double* __restrict__ center,
+                                int64_t S, unsigned int* __restrict__ keys) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const int64_t i = (S == N) ? j : (int64_t)(((__int128)j * N) / S);
+  keys[j] = (unsigned int)__float_as_int(__double2float_ru(point_dist(pts, N, d, i, center)));
+}
+
 __global__ void k_sample_keys(const double* __restrict__ pts, int64_t N, int d,
                               const double* __restrict__ center, int64_t S,
                               unsigned long long* __restrict__ keys) {
@@ -52,11 +63,12 @@ __global__ void __launch_bounds__(256) k_dist_cand(const double* __restrict__ pt
                                                    unsigned long long* __restrict__ cand_key,
                                                    unsigned long long* __restrict__ cand_idx,
                                                    unsigned long long* __restrict__ cand_count,
-                                                   int64_t cap) {
+                                                   int64_t cap, const unsigned int* __restrict__ T32 = nullptr) {
   __shared__ double c_s[64];
   if (threadIdx.x < d) c_s[threadIdx.x] = center[threadIdx.x];
   __syncthreads();
-  const unsigned long long T = *T_key;
+  const unsigned long long T =
+      T32 ? (unsigned long long)__double_as_longlong((double)__int_as_float((int)*T32)) : *T_key;
   const int lane = threadIdx.x & 31;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < N; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
@@ -365,23 +377,24 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   double* ctrl = (double*)(base + 512);
   unsigned long long* count = (unsigned long long*)(base + 512 + 64);
   unsigned long long* status = count + 2;
-  unsigned long long* skeys = status + ntiles + 8;
-  unsigned long long* skeys2 = skeys + S;
-  unsigned long long* ck = skeys2 + S;
+  unsigned int* skeys = (unsigned int*)(status + ntiles + 8);
+  unsigned int* skeys2 = skeys + S;
+  unsigned long long* ck = (unsigned long long*)(skeys2 + S + (S & 1));
   unsigned long long* ci = ck + cap;
   int64_t* src_local = (int64_t*)(ci + cap);
   KID_CK(c, cudaMemcpyAsync(center, center_h, sizeof(double) * d, cudaMemcpyHostToDevice, c->stream));
   KID_CK(c, cudaMemsetAsync(count, 0, sizeof(unsigned long long) * (2 + ntiles + 8), c->stream));
   KID_CK(c, cudaMemsetAsync(c->counter, 0, sizeof(int64_t) * 2, c->stream));
-  k_sample_keys<<<(unsigned)((S + 255) / 256), 256, 0, c->stream>>>(c->pts, N, d, center, S, skeys);
+  k_sample_keys32<<<(unsigned)((S + 255) / 256), 256, 0, c->stream>>>(c->pts, N, d, center, S, skeys);
   KID_LAUNCHED(c);
   size_t tmpb = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, tmpb, skeys, skeys2, (int)S, 0, 64, c->stream);
+  cub::DeviceRadixSort::SortKeys(nullptr, tmpb, skeys, skeys2, (int)S, 0, 32, c->stream);
   if (ensure(c, &c->sort_tmp, &c->sort_tmp_cap, tmpb)) return KID_E_OOM;
-  KID_CK(c, cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmpb, skeys, skeys2, (int)S, 0, 64, c->stream));
+  KID_CK(c, cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmpb, skeys, skeys2, (int)S, 0, 32, c->stream));
   c->launches += 4;
   prof_begin(c);
-  k_dist_cand<<<c->sms * 8, 256, 0, c->stream>>>(c->pts, N, d, center, skeys2 + (nl - 1), c->dist, ck, ci, count, cap);
+  k_dist_cand<<<c->sms * 8, 256, 0, c->stream>>>(c->pts, N, d, center, nullptr, c->dist, ck, ci, count, cap,
+                                                 skeys2 + (nl - 1));
   prof_end(c);
   KID_LAUNCHED(c);
   const size_t sel_smem = 2 * sizeof(unsigned long long) * kSelMax;
