@@ -245,10 +245,18 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out);
 int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores);
 int tsqr_dev(kid_ctx* c, double h, const double* d_Rin, int64_t nR, int64_t m, double* d_R);
 int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n, double* d_out);
+// large-m building blocks (kid_passes.cu), shared with kid_next.cu
+constexpr int kSyrkParts = 297;  // row chunks of the batched Gram (+1 remainder)
+int tall_syrk(kid_ctx* c, const double* D, int rows, int ld, int n, double* G, bool accumulate, double* part,
+              int max_parts);
+int launch_gram_reduce(kid_ctx* c, const double* partial, int nchunks, int LG, int n, const double* partial_sk,
+                       int nparts, double* out);
+int launch_eval_batch(kid_ctx* c, cudaStream_t st, const double* src, double cscale, int64_t t0, int rows, int ev_rows,
+                      int ev_cols, bool staged, double* Kb, double* skp);
+int launch_large_finish(kid_ctx* c, double* G, int n, const double* skp, int nsk, double* out);
 int eval_rows_dev(kid_ctx* c, double h, const int64_t* d_rows, int64_t count, double* d_Ks);
 int apply_skeleton_dev(kid_ctx* c, double h, const int64_t* skel, int64_t r, const double* q_skel, double* d_u);
 int select_rows(kid_ctx* c, const int64_t* rows, int64_t n);
-int init_device_tables();
 int exp_check_dev(kid_ctx* c, const double* d_x, int64_t n, double* d_y);
 // event pair bracketing the dominant kernel of a pass (no-op unless profiling)
 void prof_begin(kid_ctx* c);
