@@ -455,12 +455,20 @@ def run_next_pass(args):
         _, sv, Vt = np.linalg.svd(Ks, full_matrices=True)
         r = H.epsilon_rank(sv, wl["eps"])
         n = m - r
-        Vp = Vt.T[:, r:]  # m x n: V_perp
-        Cm = torch.tensor(np.ascontiguousarray(Vp.T).ravel(), dtype=torch.float64, device="cuda")  # column-major
         out = torch.empty(2 + n * n, dtype=torch.float64, device="cuda")
-        fn = lambda: dev.proj_gram_dev(prob.h, Cm.data_ptr(), n, out.data_ptr())
-        fpe = 3 * d + 33 + 2 + 2 * n + n * (n + 1) / m
-        kern, metric = "k_proj_gram", "compress_svd error-pass entries/s (targets x sources, FP64)"
+        if os.environ.get("KID_SVD_PROJ"):  # the generic projected Gram over V_perp
+            Vp = Vt.T[:, r:]
+            Cm = torch.tensor(np.ascontiguousarray(Vp.T).ravel(), dtype=torch.float64, device="cuda")
+            fn = lambda: dev.proj_gram_dev(prob.h, Cm.data_ptr(), n, out.data_ptr())
+            fpe = 3 * d + 33 + 2 + 2 * n + n * (n + 1) / m
+            kern = "k_proj_gram"
+        else:  # the product route (kernid_b200::compress_svd): the fused residual pass on the ID of V_r^T
+            a, Pa = H.interpolative_decomposition(np.ascontiguousarray(Vt[:r]), r)
+            dev.recon_prepare(a, Pa)
+            fn = lambda: dev.recon_error_dev(prob.h, out.data_ptr())
+            fpe = flops_per_entry_strict(d, m, r)
+            kern = "k_gram (residual mode on the ID of V_r^T)"
+        metric = "compress_svd error-pass entries/s (targets x sources, FP64)"
         extra = {"rank": r, "n_perp": n}
     elif args.pass_ == "gram":
         G = torch.empty(2 + m * m, dtype=torch.float64, device="cuda")

@@ -754,8 +754,9 @@ std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, 
 }
 
 // compress.hpp:219-273 with the error pass on the device: ||K - K V_r V_r^T||_2 = ||K V_perp||_2,
-// V_perp = the trailing m - r columns of the full right factor, by kid_proj_gram (the N_T x m
-// difference is never formed).
+// V_perp = the trailing m - r columns of the full right factor, through the fused residual-Gram
+// pass (kid_recon_error) on the ID of V_r^T (the N_T x m difference is never formed; the generic
+// kid_proj_gram computes the same Gram directly at about twice the cost).
 std::pair<Matrix, CompressionReport> compress_svd(const KernelBlock& K, const RowSample& sample, const RankRule& rule,
                                                   const CompressOptions& opts) {
   if (sample.indices.empty()) throw RangeError("compress_svd: empty row sample");
@@ -788,10 +789,46 @@ std::pair<Matrix, CompressionReport> compress_svd(const KernelBlock& K, const Ro
       Matrix Vp(m, n);
       for (int64_t j = 0; j < n; ++j)
         for (int64_t i = 0; i < m; ++i) Vp(i, j) = rf.V(i, r + j);
-      Matrix DtD(n, n);
-      K.device().check(kid_proj_gram(K.device().ctx(), K.spec().h, Vp.data(), n, &sd, &sk, DtD.data()));
+      // The fused residual pass computes ||K V_perp|| too: with a = the ID skeleton of V_r^T
+      // (r x m, CPQR) and P its projection ([I, T], T = V_r[a,:]^-T V_r[b,:]^T), b the other n
+      // columns and C_b = V_perp[b, :]: K V_perp = (K_b - K_a (-T)) ... = (K - K[:, a] P)[:, b] C_b
+      // because V_r^T V_perp = 0 gives -C_a C_b^-1 = T. So D' = (K - K[:, a] P)[:, b] comes from
+      // the residual-Gram kernel and G = C_b^T (D'^T D') C_b on the host; C_b is well conditioned
+      // (its singular values are those of V_r[a, :], CPQR-selected).
+      Matrix VrT(r, m);
+      for (int64_t j = 0; j < r; ++j)
+        for (int64_t i = 0; i < m; ++i) VrT(j, i) = rf.V(i, j);
+      const IDFactorization idv = interpolative_decomposition(VrT, r);
+      Matrix DtDm(m, m);
+      double sdp = 0.0;
+      K.device().check(kid_recon_error(K.device().ctx(), K.spec().h, idv.skeleton.data(), r, idv.projection.data(),
+                                       KID_RECON_DTD, &sdp, &sk, DtDm.data(), nullptr));
+      std::vector<char> in_a(static_cast<size_t>(m), 0);
+      for (int64_t j : idv.skeleton) in_a[static_cast<size_t>(j)] = 1;
+      std::vector<int64_t> b;
+      for (int64_t i = 0; i < m; ++i)
+        if (!in_a[static_cast<size_t>(i)]) b.push_back(i);
+      Matrix Gp(n, n), Cb(n, n), T1(n, n), G(n, n);
+      for (int64_t y = 0; y < n; ++y)
+        for (int64_t x = 0; x < n; ++x) {
+          Gp(x, y) = DtDm(b[static_cast<size_t>(x)], b[static_cast<size_t>(y)]);
+          Cb(x, y) = Vp(b[static_cast<size_t>(x)], y);
+        }
+      for (int64_t y = 0; y < n; ++y)  // T1 = G' C_b
+        for (int64_t x = 0; x < n; ++x) {
+          double acc = 0.0;
+          for (int64_t l = 0; l < n; ++l) acc += Gp(x, l) * Cb(l, y);
+          T1(x, y) = acc;
+        }
+      for (int64_t y = 0; y < n; ++y)  // G = C_b^T T1
+        for (int64_t x = 0; x < n; ++x) {
+          double acc = 0.0;
+          for (int64_t l = 0; l < n; ++l) acc += Cb(l, x) * T1(l, y);
+          G(x, y) = acc;
+        }
+      for (int64_t i = 0; i < n; ++i) sd += G(i, i);
       std::vector<double> ev;
-      sym_eig(DtD, ev, nullptr);
+      sym_eig(G, ev, nullptr);
       num = std::sqrt(std::max(ev.empty() ? 0.0 : ev[0], 0.0));
     } else {
       K.gram(&sk);  // V_r spans R^m: the difference is rounding only
