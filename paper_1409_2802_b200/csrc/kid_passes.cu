@@ -140,7 +140,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // register split: 640 threads launch with 96 registers each; setmaxnreg.inc can only take what
 // the decreasing warps release: 384 (96 - E) >= 256 (M - 96)
-constexpr int kEvalRegs = 72, kMmaRegs = 128;
+constexpr int kEvalRegs = 88, kMmaRegs = 104;
 static_assert(kGT == 640, "setmaxnreg budget below assumes 640 threads (96 registers each at launch)");
 static_assert(kEW * 32 * (96 - kEvalRegs) >= kMW * 32 * (kMmaRegs - 96), "setmaxnreg.inc exceeds what .dec releases");
 
