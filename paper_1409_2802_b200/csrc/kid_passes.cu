@@ -96,14 +96,14 @@ struct GramArgs {
 constexpr int kTraceTiles = 64;
 
 // Warp-specialized pipeline (one CTA per SM), per 32-target tile:
-//   warps 0..11 (kEW "eval" warps) own a host-balanced list of work items:
+//   the kEW "eval" warps own a host-balanced list of work items:
 //     A item j      : K_S column j of the NEXT tile (exp) -> KS ring (2 slots, eval-private)
 //     B item g      : non-skeleton columns 4g..4g+3 of THIS tile: K_N by exp (4 independent
 //                     chains), then D = K_N - K_S P2 by DFMA against the K_S row of the target
 //                     (KS ring) and -P2 rows (shared memory, LDS.128 broadcasts) -> KN stage
 //     lane = target row throughout, so stores are conflict-free column-major [col][t] (stride
 //     kST = 36 = 4 mod 16, which also makes the DMMA fragment gathers conflict-free);
-//   warps 12..19 (kMW "MMA" warps): G += D^T D (DMMA.8x8x4) on static WA x 2-block warp tiles of
+//   the kMW "MMA" warps: G += D^T D (DMMA.8x8x4) on static WA x 2-block warp tiles of
 //     the upper triangle, accumulators register-resident across the CTA's whole target chunk.
 // Hand-off by named barriers: FULL[s] (eval arrive, MMA sync), EMPTY[s] (MMA arrive, eval sync),
 // EVAL (eval warps only: K_S of the next tile and the next coordinates are visible).
@@ -111,7 +111,7 @@ constexpr int kTraceTiles = 64;
 // ahead (the target index of the copy is itself loaded one tile earlier).
 // DMMA and DFMA share the FP64 datapath (tools/fp64_overlap.cu): the split keeps it fed from
 // both sides -- the MMA warps never wait on a GEMM phase, the eval warps fill the DMMA gaps.
-constexpr int kMW = 8, kEW = 12, kGT = (kMW + kEW) * 32;  // 640 threads
+constexpr int kMW = 7, kEW = 13, kGT = (kMW + kEW) * 32;  // 640 threads
 constexpr int kEvalW0 = kMW, kMmaW0 = 0;
 constexpr int kStages = 4;
 constexpr int kRing = 4;      // target-coordinate ring slots
@@ -911,8 +911,11 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     if (nb <= kMW * cand) break;
   }
   if (WA == 2 && TPW < 3) TPW = 3;  // the instantiated 16x16 layouts (KID_LAYOUT_SWITCH)
+  const int nparts = (nb + kMW * TPW - 1) / (kMW * TPW);
+  // with several parts, size the warp tile list to the part's floor/ceil share: the MMA warps
+  // dispatch only tile counts TPW, TPW - 1 and TPW - 2
+  TPW = std::max(WA == 2 ? 3 : 1, ((nb + nparts - 1) / nparts + kMW - 1) / kMW);
   const int per_part = kMW * TPW;
-  const int nparts = (nb + per_part - 1) / per_part;
   // per part: floor/ceil share per warp, valid tiles first; the extra tiles go to the lowest
   // warps, which sit on distinct SMSPs (warp % 4) for the first four -> SMSP-balanced DMMA work
   std::vector<int2> blist((size_t)nparts * per_part, make_int2(-1, -1));
