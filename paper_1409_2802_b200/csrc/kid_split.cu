@@ -256,79 +256,53 @@ __global__ void __launch_bounds__(kCT) k_compact(const double* __restrict__ dist
   }
 }
 
-// Device-side selection of the n sources (single CTA, the candidate count is read on the device):
-// bitonic sort of the <= kSelMax candidates by (dist, idx) -- nth_element's comparator
-// (geometry.hpp:40-47) -- rho = the n-th key (geometry.hpp:52-53), the n indices sorted ascending
-// (geometry.hpp:50-51), the source coordinates gathered. ctrl = [rho, overflow flag].
-constexpr int kSelMax = 8192, kSelT = 1024;
-__device__ __forceinline__ bool pair_gt(unsigned long long ka, unsigned long long ia, unsigned long long kb,
-                                        unsigned long long ib) {
-  return ka > kb || (ka == kb && ia > ib);
-}
-__device__ void block_bitonic(unsigned long long* key, unsigned long long* idx, int P) {
-  for (int k = 2; k <= P; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool asc = (i & k) == 0;
-          const bool gt = pair_gt(key[i], idx[i], key[ixj], idx[ixj]);
-          if (gt == asc) {
-            const unsigned long long tk = key[i], ti = idx[i];
-            key[i] = key[ixj];
-            idx[i] = idx[ixj];
-            key[ixj] = tk;
-            idx[ixj] = ti;
-          }
-        }
-      }
-      __syncthreads();
-    }
-}
+// Device-side selection of the n sources (single CTA; the candidate count is read on the device):
+// each candidate's rank under (dist, idx) -- nth_element's comparator (geometry.hpp:40-47) -- by
+// counting over the <= kSelMax candidates in shared memory (warp-uniform broadcast reads, no
+// sorting network, three barriers); the n of rank < n are placed by rank, rho = the largest
+// (geometry.hpp:52-53), then placed again by their rank in index order (geometry.hpp:50-51) and
+// the source coordinates gathered. ctrl = [rho, fallback flag (overflow or fewer than n)].
+constexpr int kSelMax = 4096, kSelT = 1024;
 __global__ void __launch_bounds__(kSelT) k_split_select(const unsigned long long* __restrict__ ck,
                                                        const unsigned long long* __restrict__ ci,
                                                        const unsigned long long* __restrict__ count, int64_t cap,
                                                        int nl, const double* __restrict__ pts, int64_t N, int d,
                                                        int64_t* __restrict__ src_local, double* __restrict__ src,
                                                        double* __restrict__ ctrl) {
-  extern __shared__ unsigned long long sel_sm[];
+  extern __shared__ unsigned long long sel_sm[];  // key | idx (kSelMax each) | sel_key | sel_idx (kSelT each)
   unsigned long long* key = sel_sm;
-  unsigned long long* idx = sel_sm + kSelMax;
+  unsigned long long* idx = key + kSelMax;
+  unsigned long long* sel_key = idx + kSelMax;
+  unsigned long long* sel_idx = sel_key + kSelT;
   const unsigned long long total = *count;
   const unsigned long long lim = (unsigned long long)(cap < kSelMax ? cap : kSelMax);
-  const int cnt = (int)(total < lim ? total : lim);
-  if (threadIdx.x == 0) ctrl[1] = (total > lim || total < (unsigned long long)nl) ? 1.0 : 0.0;
-  int P = 1;
-  while (P < max(cnt, nl)) P <<= 1;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    key[i] = i < cnt ? ck[i] : ~0ull;
-    idx[i] = i < cnt ? ci[i] : ~0ull;
+  const bool bad = total > lim || total < (unsigned long long)nl;
+  if (threadIdx.x == 0) ctrl[1] = bad ? 1.0 : 0.0;
+  if (bad) return;  // uniform over the CTA
+  const int cnt = (int)total;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    key[i] = ck[i];
+    idx[i] = ci[i];
   }
   __syncthreads();
-  block_bitonic(key, idx, P);
-  if (threadIdx.x == 0) ctrl[0] = __longlong_as_double((long long)key[nl - 1]);  // rho: the largest of the n
-  // the n indices ascending: keys <- indices, padded
-  int Q = 1;
-  while (Q < nl) Q <<= 1;
-  unsigned long long* k2 = key + P;  // scratch after the first P entries (P + Q <= 2 kSelMax)
-  unsigned long long* i2 = idx + P;
-  if (P + Q > kSelMax) { k2 = key; i2 = idx; }  // reuse in place (only the first nl are needed)
-  __syncthreads();
-  unsigned long long vals[kSelMax / kSelT];
-  int nv = 0;
-  for (int i = threadIdx.x; i < Q; i += blockDim.x) vals[nv++] = i < nl ? idx[i] : ~0ull;
-  __syncthreads();
-  nv = 0;
-  for (int i = threadIdx.x; i < Q; i += blockDim.x) {
-    k2[i] = vals[nv++];
-    i2[i] = 0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const unsigned long long ki = key[i], ii = idx[i];
+    int rank = 0;
+    for (int j = 0; j < cnt; ++j) rank += (key[j] < ki) || (key[j] == ki && idx[j] < ii);
+    if (rank < nl) {
+      sel_key[rank] = ki;
+      sel_idx[rank] = ii;
+    }
   }
   __syncthreads();
-  block_bitonic(k2, i2, Q);
-  for (int j = threadIdx.x; j < nl; j += blockDim.x) {
-    const int64_t li = (int64_t)k2[j];
-    src_local[j] = li;
-    for (int k = 0; k < d; ++k) src[j + (int64_t)k * nl] = pts[li + k * N];
+  if (threadIdx.x == 0) ctrl[0] = __longlong_as_double((long long)sel_key[nl - 1]);  // rho: the largest of the n
+  for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+    const unsigned long long ii = sel_idx[i];
+    int rank = 0;
+    for (int j = 0; j < nl; ++j) rank += sel_idx[j] < ii;
+    const int64_t li = (int64_t)ii;
+    src_local[rank] = li;
+    for (int k = 0; k < d; ++k) src[rank + (int64_t)k * nl] = pts[li + k * N];
   }
 }
 
@@ -360,10 +334,12 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   const int d = c->d;
   if (!c->pts || N < 1 || d > 64 || n > kSelT || n > N) return 1;
   const int64_t nl = n;
-  const int64_t S = N <= std::max<int64_t>(kSampleMax, 4 * nl) ? N : std::max<int64_t>(kSampleMax, 4 * nl);
-  int64_t cap = std::max<int64_t>(4 * nl + 1024, (int64_t)((double)N * (double)nl / (double)S * 2.0) + 4096);
-  cap = std::min<int64_t>(cap, N);
-  if (cap > kSelMax) return 1;
+  // sample size and the sample quantile used as the threshold: the k_s-th smallest of S strided
+  // sample distances lets about k_s N / S points through (2.5 n + 4 N / S, a few hundred to a few
+  // thousand candidates); fewer than n (rare) or more than kSelMax take the general path
+  const int64_t S = std::min<int64_t>(N, std::max<int64_t>(16384, std::min<int64_t>(kSampleMax, N / 64)));
+  const int64_t ks = S == N ? nl : std::min<int64_t>(S, (int64_t)std::ceil(2.5 * (double)nl * (double)S / (double)N) + 4);
+  const int64_t cap = std::min<int64_t>(kSelMax, N);
   if (ensure(c, (void**)&c->dist, &c->dist_cap, sizeof(double) * N)) return KID_E_OOM;
   if (ensure(c, (void**)&c->tgt_idx, &c->tgt_cap, sizeof(int64_t) * N)) return KID_E_OOM;
   if (ensure(c, (void**)&c->src, &c->src_cap, sizeof(double) * n * d)) return KID_E_OOM;
@@ -394,10 +370,10 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   c->launches += 4;
   prof_begin(c);
   k_dist_cand<<<c->sms * 8, 256, 0, c->stream>>>(c->pts, N, d, center, nullptr, c->dist, ck, ci, count, cap,
-                                                 skeys2 + (nl - 1));
+                                                 skeys2 + (ks - 1));
   prof_end(c);
   KID_LAUNCHED(c);
-  const size_t sel_smem = 2 * sizeof(unsigned long long) * kSelMax;
+  const size_t sel_smem = sizeof(unsigned long long) * 2 * (kSelMax + kSelT);
   cudaFuncSetAttribute(k_split_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
   k_split_select<<<1, kSelT, sel_smem, c->stream>>>(ck, ci, count, cap, (int)nl, c->pts, N, d, src_local, c->src, ctrl);
   KID_LAUNCHED(c);
