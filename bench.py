@@ -483,7 +483,7 @@ def run_next_pass(args):
         lv = torch.empty(max(prob.nt, 1), dtype=torch.float64, device="cuda")
         fn = lambda: dev.leverage_dev(prob.h, Wd.data_ptr(), rl, lv.data_ptr())
         fpe = 3 * d + 33 + 2 * rl
-        kern, metric = "k_leverage", "leverage-score entries/s (targets x sources, FP64)"
+        kern, metric = "k_proj_gram (leverage mode) / batched", "leverage-score entries/s (targets x sources, FP64)"
         extra = {"rank": rl}
     elif args.pass_ == "rownorms":
         wv = torch.empty(max(prob.nt, 1), dtype=torch.float64, device="cuda")
