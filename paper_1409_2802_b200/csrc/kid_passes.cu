@@ -872,23 +872,97 @@ int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
   return KID_OK;
 }
 
+// ||K||_F^2 alone (the full-rank skeleton of the residual pass: D == 0): one thread per target,
+// four exp chains, per-block partials folded in a fixed order. d_out = [0, ||K||_F^2].
+template <int D>
+__global__ void __launch_bounds__(256) k_sumsq(TargetView tv, int d_rt, const double* __restrict__ src, int m,
+                                               double cscale, double* __restrict__ part) {
+  const int d = D ? D : d_rt;
+  const int m4 = ceil_to(m, 4);
+  extern __shared__ __align__(16) double sm_sq[];  // d x m4 scaled sources
+  __shared__ double s_tab[kExpTabWords];
+  __shared__ double red[8];
+  stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+  for (int e = threadIdx.x; e < d * m4; e += blockDim.x) {
+    const int k = e / m4, j = e - k * m4;
+    sm_sq[e] = j < m ? src[j + (int64_t)k * m] * cscale : 1.0e4;
+  }
+  __syncthreads();
+  const double* tabl = s_tab + (threadIdx.x & 31);
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tv.nt; i += (int64_t)gridDim.x * blockDim.x) {
+    constexpr int DR = D ? D : 1;
+    double t[DR];
+    if constexpr (D > 0) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[k] = tcoord(tv, i, k) * cscale;
+    }
+    for (int j = 0; j < m4; j += 4) {
+      double kv[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < d; ++k) {
+        const double tk = D ? t[D ? k : 0] : tcoord(tv, i, k) * cscale;
+        const double* xk = sm_sq + k * m4 + j;
+        const double a0 = tk - xk[0], a1 = tk - xk[1], a2 = tk - xk[2], a3 = tk - xk[3];
+        kv[0] = fma(a0, a0, kv[0]);
+        kv[1] = fma(a1, a1, kv[1]);
+        kv[2] = fma(a2, a2, kv[2]);
+        kv[3] = fma(a3, a3, kv[3]);
+      }
+      exp_neg_fast_n<4>(kv, tabl);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = fma(kv[u], kv[u], acc);
+    }
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_sumsq_finish(const double* __restrict__ part, int n, double* __restrict__ out) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < n; b += 32) s += part[b];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) {
+    out[0] = 0.0;
+    out[1] = s;
+  }
+}
+
+int sumsq_dev(kid_ctx* c, double h, double* d_out) {
+  const int m = (int)c->m, d = c->d;
+  const size_t smem = sizeof(double) * (size_t)d * ceil_to(m, 4);
+  if (smem > 160 * 1024) return fail(c, KID_E_DIM, "sumsq: m*d too large for shared memory");
+  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((c->nt + 255) / 256, (int64_t)c->sms * 4));
+  double* part = (double*)scratch(c, sizeof(double) * (blocks + 8));
+  if (!part) return KID_E_OOM;
+  const double cscale = std::sqrt(1.0 / (2.0 * h * h));
+#define LAUNCH(DD)                                                                                  \
+  {                                                                                                 \
+    cudaFuncSetAttribute(k_sumsq<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+    k_sumsq<DD><<<blocks, 256, smem, c->stream>>>(view(c), d, c->src, m, cscale, part);             \
+  }
+  prof_begin(c);
+  KID_DISPATCH_D(d, LAUNCH)
+  prof_end(c);
+#undef LAUNCH
+  KID_LAUNCHED(c);
+  k_sumsq_finish<<<1, 32, 0, c->stream>>>(part, blocks, d_out);
+  KID_LAUNCHED(c);
+  return KID_OK;
+}
+
 int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   (void)flags;
   if (int rc = check_block(c, h)) return rc;
   const int m = (int)c->m, d = c->d;
   const int meff = (int)(m - r);
-  if (meff < 1) {
-    // full-rank skeleton: D == 0 exactly; ||K||_F^2 still comes from a K-mode pass
-    double* tmp = nullptr;
-    KID_CK(c, cudaMallocAsync((void**)&tmp, sizeof(double) * (2 + (size_t)m * m), c->stream));
-    int rc = gram_dev(c, h, 0, flags, tmp);
-    if (!rc) {
-      KID_CK(c, cudaMemsetAsync(d_out, 0, sizeof(double), c->stream));
-      KID_CK(c, cudaMemcpyAsync(d_out + 1, tmp + 1, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    }
-    KID_CK(c, cudaFreeAsync(tmp, c->stream));
-    return rc;
-  }
+  if (meff < 1) return sumsq_dev(c, h, d_out);  // full-rank skeleton: D == 0 exactly, only ||K||_F^2
   const int NBN = ceil_to(meff, 8) / 8;
   const int LG = NBN * 8;
   // upper-triangular warp tiles of WA x 2 blocks (8x16 when NBN <= 12, else 16x16), row-major,
