@@ -50,6 +50,9 @@ WORKLOADS = {
     # configs[1] (quoted config of the metric): d in {1,2,3}, 1e6 targets, m=100, D_WS=2
     "c2-d3": dict(d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-2),
     "c2-d2": dict(d=2, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-8),
+    "c2-d3-e4": dict(d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-4),
+    "c2-d3-e6": dict(d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-6),
+    "c2-d3-e8": dict(d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-8),
     "c1": dict(d=2, N=100_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-8),
     "c3-d5": dict(d=5, N=1_000_000, m=100, xi=3.0, h_value=1.0, s=0.02, eps=1e-8),
     "c4-d16": dict(d=16, N=12_000_000, m=256, xi=2.0, h_value=1.0, s=0.002, eps=1e-2),
