@@ -355,7 +355,7 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   unsigned long long* status = count + 2;
   unsigned int* skeys = (unsigned int*)(status + ntiles + 8);
   unsigned int* skeys2 = skeys + S;
-  unsigned long long* ck = (unsigned long long*)(skeys2 + S + (S & 1));
+  unsigned long long* ck = (unsigned long long*)(skeys2 + S);  // 2S 32-bit keys: 8-byte aligned
   unsigned long long* ci = ck + cap;
   int64_t* src_local = (int64_t*)(ci + cap);
   KID_CK(c, cudaMemcpyAsync(center, center_h, sizeof(double) * d, cudaMemcpyHostToDevice, c->stream));

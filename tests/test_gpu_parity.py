@@ -267,3 +267,21 @@ def test_split_high_dimension(oracle, dev):
     assert np.all(np.abs(w[nz] - ref[nz]) <= 1e-12 * ref[nz])
     G, _ = dev.gram(t.h)
     assert _gram_ok(G, K.T @ K)
+
+
+@pytest.mark.parametrize("n", [1, 7, 100, 1024, 1025])
+def test_split_lattice_ties_and_selection_paths(oracle, dev, n):
+    """Many exactly equal distances (an integer lattice around its centre point) through the
+    device-side selection (n <= 1024, one synchronisation) and the general path (n > 1024):
+    sources, rho and targets bit-exact against nth_element's (dist, idx) order."""
+    g = np.arange(-40, 41, dtype=np.float64)
+    xx, yy = np.meshgrid(g, g, indexing="ij")
+    ps = np.stack([xx.ravel(), yy.ravel()], axis=1)  # 6561 points, exact integer coordinates
+    ps = ps[np.random.default_rng(n).permutation(ps.shape[0])]
+    center = np.array([0.0, 0.0])
+    dev.set_points(ps)
+    src, rho, nt = dev.split(center, n, 1.5)
+    ref = oracle.split_sources_targets(ps, center, n, 1.5)
+    assert np.array_equal(src, ref.source_indices)
+    assert rho == ref.rho
+    assert np.array_equal(dev.targets(), ref.target_indices)
