@@ -285,3 +285,39 @@ def test_split_lattice_ties_and_selection_paths(oracle, dev, n):
     assert np.array_equal(src, ref.source_indices)
     assert rho == ref.rho
     assert np.array_equal(dev.targets(), ref.target_indices)
+
+
+def test_generic_dimension_passes(oracle, dev):
+    """d = 7 (not one of the compiled dimensions 1, 2, 3, 4, 5, 8, 16): every pass through the
+    generic-d kernels against the oracle."""
+    t, K = _block(oracle, d=7, N=12_000, n=60, xi=1.5)
+    dev.set_points(t.points)
+    src, rho, nt = dev.split(t.center, 60, 1.5)
+    assert np.array_equal(src, t.split.source_indices) and rho == t.split.rho
+    assert np.allclose(dev.row_norms(t.h), oracle.row_norms(K), rtol=1e-12, atol=0)
+    G, sk = dev.gram(t.h)
+    assert _gram_ok(G, K.T @ K) and sk == pytest.approx(np.sum(K * K), rel=1e-12)
+    R = dev.tsqr_r(t.h)
+    s1 = oracle.spectral_norm_exact(K)
+    assert np.allclose(R.T @ R, K.T @ K, rtol=0, atol=1e-12 * s1 * s1)
+    sv, V = oracle.right_factor(K)
+    W = V[:, :10] / sv[:10]
+    ref, _ = oracle.row_leverage_scores(K, 10)
+    assert np.max(np.abs(dev.leverage(t.h, W) - ref)) <= 1e-10 * max(1.0, ref.max())
+
+
+def test_full_rank_residual_device_pass(oracle, dev):
+    """r = m through the device entry point (kid_recon_error_dev): D == 0 exactly and
+    ||K||_F^2 from the reduction-only kernel."""
+    import torch
+    t, K = _block(oracle, d=3, N=20_000, n=40)
+    dev.set_points(t.points)
+    dev.split(t.center, 40, 2.0)
+    skel = np.arange(40)
+    dev.recon_prepare(skel, np.eye(40))
+    out = torch.full((8,), -1.0, dtype=torch.float64, device="cuda")
+    dev.recon_error_dev(t.h, out.data_ptr())
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert o[0] == 0.0
+    assert o[1] == pytest.approx(np.sum(K * K), rel=1e-12)
