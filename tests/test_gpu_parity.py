@@ -321,3 +321,20 @@ def test_full_rank_residual_device_pass(oracle, dev):
     o = out.cpu().numpy()
     assert o[0] == 0.0
     assert o[1] == pytest.approx(np.sum(K * K), rel=1e-12)
+
+
+def test_empty_block_all_passes(oracle, dev):
+    """A block with no targets (kid_set_block with nt = 0): every pass returns the empty result."""
+    sr = oracle.gen_normal(3, 12, 5)
+    dev.set_block(np.zeros((0, 3)), sr)
+    assert dev.row_norms(0.5).size == 0
+    G, sk = dev.gram(0.5)
+    assert np.all(G == 0.0) and sk == 0.0
+    skel, P = np.array([0, 3]), np.zeros((2, 12))
+    P[:, skel] = np.eye(2)
+    sd, sk, DtD, _ = dev.recon_error(0.5, skel, P)
+    assert sd == 0.0 and sk == 0.0 and np.all(DtD == 0.0)
+    sd, sk, Gp = dev.proj_gram(0.5, np.eye(12)[:, :5])
+    assert sd == 0.0 and sk == 0.0 and np.all(Gp == 0.0)
+    assert np.all(dev.tsqr_r(0.5) == 0.0)
+    assert dev.leverage(0.5, np.eye(12)[:, :3]).size == 0
