@@ -1453,12 +1453,8 @@ int kidh_compress_trial(int32_t device, int32_t d, int64_t N, int64_t n, double 
     if (sc.kind == SchemeKind::Leverage) {
       if (lev_rank > 0) {
         sc.rank_for_leverage = lev_rank;
-      } else {
-        std::vector<double> ev;
-        sym_eig(K.gram(), ev, nullptr);
-        std::vector<double> sv(ev.size());
-        for (size_t i = 0; i < ev.size(); ++i) sv[i] = std::sqrt(std::max(ev[i], 0.0));
-        sc.rank_for_leverage = std::max<int64_t>(1, rule.resolve(sv));
+      } else {  // auto rank from the full spectrum (harness.hpp:176-184): device TSQR
+        sc.rank_for_leverage = std::max<int64_t>(1, rule.resolve(K.singular_values()));
       }
     }
     SampleContext ctx;

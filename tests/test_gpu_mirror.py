@@ -16,6 +16,8 @@ def _oracle_trial(O, d, N, n, xi, data_seed, scheme, s, sample_seed, eps, lev_ra
     if scheme == O.SCHEME_EUCLIDEAN:
         w = O.row_norms(K)
     elif scheme == O.SCHEME_LEVERAGE:
+        if lev_rank <= 0:  # auto rank from the full spectrum (harness.hpp:176-184)
+            lev_rank = max(1, O.epsilon_rank(O.singular_values(K), eps))
         w, _ = O.row_leverage_scores(K, lev_rank)
     rows = O.sample_rows(scheme, K.shape[0], s, sample_seed, w)
     res = O.compress_id(K, rows, eps=eps)
@@ -23,7 +25,7 @@ def _oracle_trial(O, d, N, n, xi, data_seed, scheme, s, sample_seed, eps, lev_ra
 
 
 @pytest.mark.parametrize("d,scheme,eps,lev", [(2, 2, 1e-8, 0), (3, 2, 1e-2, 0), (2, 0, 1e-8, 0), (3, 4, 1e-4, 8),
-                                              (1, 2, 1e-8, 0)])
+                                              (1, 2, 1e-8, 0), (3, 4, 1e-6, 0), (2, 4, 1e-9, 0)])
 def test_compress_trial_matches_oracle(oracle, d, scheme, eps, lev):
     from paper_1409_2802_b200 import kernid as H
     N, n, xi = 20000, 100, 2.0
