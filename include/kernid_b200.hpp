@@ -132,7 +132,7 @@ class KernelBlock {
   // on the device (kid_tsqr_r) + a Jacobi SVD of the m x m factor for m <= 128 -- every sigma
   // to ~u sigma_1; the Gram route (sqrt(eig(K^T K)), ~sqrt(u) sigma_1 floor) above that.
   RightFactor right_factor() const;
-  std::vector<double> singular_values() const { return right_factor().singular_values; }
+  std::vector<double> singular_values() const;  // values only: m > 128 by the Gram eigenvalues (sym_eigvals)
 
  private:
   Device* dev_;
@@ -156,7 +156,8 @@ std::vector<double> singular_values(const Matrix& A);                       // l
 int64_t epsilon_rank(const std::vector<double>& sv, double eps,
                      std::optional<double> reference_sigma1 = std::nullopt);  // :117-126
 IDFactorization interpolative_decomposition(const Matrix& A, int64_t r);     // :235-262
-void sym_eig(const Matrix& A, std::vector<double>& evals, Matrix* evecs);   // Gram route
+void sym_eig(const Matrix& A, std::vector<double>& evals, Matrix* evecs);   // Gram route (Jacobi)
+std::vector<double> sym_eigvals(const Matrix& A);                           // tridiagonal + QL, values only
 LeverageScores row_leverage_scores(const KernelBlock& K, int64_t r);        // :296-308 (device)
 
 // ------------------------------------------------------------- sampling.hpp
@@ -245,6 +246,7 @@ Matrix complement_basis(const Matrix& Vr);
 
 // ------------------------------------------------------------- harness.hpp (compress sweep)
 enum class CompressionMethod { ID, SVD };  // compress.hpp:57-60
+enum class CenterMode { Origin, RandomPoint };  // config.hpp:69 (the reference default is Origin)
 struct ExperimentConfig {
   int d = 2;
   int64_t N = 100000;
@@ -262,12 +264,15 @@ struct ExperimentConfig {
   double theorem_eps = 0.5;
   int trials = 1;
   std::uint64_t seed = 1;
+  CenterMode center_mode = CenterMode::Origin;                    // config.hpp:69
   std::vector<CompressionMethod> methods{CompressionMethod::ID};  // config.hpp:79
   std::optional<double> s_mc;                                     // config.hpp:85-86 (mc_error)
   int n_mc = 1;
 };
 // harness.hpp:143-328 for the Normal dataset / RandomPoint center / ID method.
 void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out, std::ostream* log = nullptr);
+// resolve_center (harness.hpp:85-101): the origin, or row below(N) of the 0xCE stream
+std::vector<double> resolve_center(const ExperimentConfig& cfg, const PointSet& points, std::uint64_t data_seed);
 
 // compress.hpp:327-378: spectral-norm fractions of the source-source, neighbour-source and
 // far-field blocks of the N x n matrix of all points against the n points closest to x_c.

@@ -420,10 +420,11 @@ class Trial:
 
 
 def prepare_trial(d: int, N: int, n_sources: int, xi: float, data_seed: int, h_value: float = 1.0,
-                  silverman_units: bool = True) -> Trial:
-    """prepare_trial (harness.hpp:107-129) for the Normal dataset, RandomPoint center."""
+                  silverman_units: bool = True, center: str = "random") -> Trial:
+    """prepare_trial (harness.hpp:107-129) for the Normal dataset; center "random" (RandomPoint,
+    the BASELINE configs) or "origin" (the reference default, harness.hpp:88)."""
     points = gen_normal(d, N, derive_seed(data_seed, 0xDA7A))
-    center = points[random_center_index(N, data_seed)].copy()
+    center = points[random_center_index(N, data_seed)].copy() if center == "random" else np.zeros(d)
     split = split_sources_targets(points, center, n_sources, xi)
     sources = gather_points(points, split.source_indices)
     targets = gather_points(points, split.target_indices)
@@ -455,11 +456,12 @@ def interaction_fractions(points: np.ndarray, h: float, x_c, n: int):
             spectral_norm_exact(KF) / total if far.shape[0] else 0.0)
 
 
-def bandwidth_search(d, N, n, xi, data_seed, kappa=0.2, large_h=False, eps=1e-2, max_iters=40, tol_rows=2):
+def bandwidth_search(d, N, n, xi, data_seed, kappa=0.2, large_h=False, eps=1e-2, max_iters=40, tol_rows=2,
+                     center="origin"):
     """bandwidth_search (harness.hpp:345-438) on the oracle's K and singular_values; returns
     (h_abs, h_over_hs, rank, evaluations, converged, profile) or raises OracleError with the
     profile in .profile when the budget cannot be bracketed."""
-    t = prepare_trial(d, N, n, xi, data_seed)
+    t = prepare_trial(d, N, n, xi, data_seed, center=center)
     h_S = silverman_bandwidth(d, N)
     target = kappa * n
     profile = []

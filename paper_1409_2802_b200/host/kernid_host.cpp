@@ -318,6 +318,16 @@ RightFactor right_factor(const Matrix& A) {
   return rf;
 }
 
+std::vector<double> KernelBlock::singular_values() const {
+  const int64_t m = cols();
+  if (m <= 128) return right_factor().singular_values;
+  const std::vector<double> ev = sym_eigvals(gram());  // Gram route, eigenvalues only
+  std::vector<double> sv(ev.size());
+  for (size_t i = 0; i < ev.size(); ++i) sv[i] = std::sqrt(std::max(ev[i], 0.0));
+  sv.resize(static_cast<size_t>(std::min(rows(), m)));
+  return sv;
+}
+
 RightFactor KernelBlock::right_factor() const {
   const int64_t m = cols();
   RightFactor rf;
@@ -478,6 +488,93 @@ void sym_eig(const Matrix& A_in, std::vector<double>& evals, Matrix* evecs) {
     if (evecs)
       for (int64_t k = 0; k < n; ++k) (*evecs)(k, i) = V(k, order[static_cast<size_t>(i)]);
   }
+}
+
+// Eigenvalues (descending) of a symmetric matrix without vectors: Householder reduction to
+// tridiagonal form (A22 <- H A22 H by the rank-2 update A22 - v w^T - w v^T), then the implicit
+// QL iteration with Wilkinson shifts on the tridiagonal. O(n^3) with a small constant: the
+// eigenvalue-only host step for the m = 256 / 512 Grams, where Jacobi sweeps cost seconds.
+std::vector<double> sym_eigvals(const Matrix& A_in) {
+  const int64_t n = A_in.rows;
+  if (A_in.cols != n) throw DimensionError("sym_eigvals: matrix must be square");
+  std::vector<double> a(A_in.a);  // column-major, symmetric: a[i + j n]
+  auto at = [&](int64_t i, int64_t j) -> double& { return a[static_cast<size_t>(i + j * n)]; };
+  std::vector<double> d(static_cast<size_t>(n)), e(static_cast<size_t>(n), 0.0);
+  std::vector<double> v(static_cast<size_t>(n)), p(static_cast<size_t>(n)), w(static_cast<size_t>(n));
+  for (int64_t k = 0; k + 2 < n; ++k) {
+    const int64_t m = n - k - 1;  // length of x = A[k+1:, k]
+    double nrm = 0.0;
+    for (int64_t i = 0; i < m; ++i) nrm += at(k + 1 + i, k) * at(k + 1 + i, k);
+    nrm = std::sqrt(nrm);
+    const double x0 = at(k + 1, k);
+    if (nrm == 0.0) continue;
+    const double alpha = x0 >= 0.0 ? -nrm : nrm;
+    double vn = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      v[static_cast<size_t>(i)] = at(k + 1 + i, k) - (i == 0 ? alpha : 0.0);
+      vn += v[static_cast<size_t>(i)] * v[static_cast<size_t>(i)];
+    }
+    if (vn == 0.0) continue;
+    const double beta = 2.0 / vn;  // H = I - beta v v^T
+    double K = 0.0;
+    for (int64_t i = 0; i < m; ++i) {  // p = beta A22 v
+      double acc = 0.0;
+      for (int64_t j = 0; j < m; ++j) acc += at(k + 1 + i, k + 1 + j) * v[static_cast<size_t>(j)];
+      p[static_cast<size_t>(i)] = beta * acc;
+      K += v[static_cast<size_t>(i)] * p[static_cast<size_t>(i)];
+    }
+    K *= 0.5 * beta;
+    for (int64_t i = 0; i < m; ++i) w[static_cast<size_t>(i)] = p[static_cast<size_t>(i)] - K * v[static_cast<size_t>(i)];
+    for (int64_t j = 0; j < m; ++j)  // A22 -= v w^T + w v^T
+      for (int64_t i = 0; i < m; ++i)
+        at(k + 1 + i, k + 1 + j) -= v[static_cast<size_t>(i)] * w[static_cast<size_t>(j)] +
+                                    w[static_cast<size_t>(i)] * v[static_cast<size_t>(j)];
+    at(k + 1, k) = at(k, k + 1) = alpha;
+    for (int64_t i = 1; i < m; ++i) at(k + 1 + i, k) = at(k, k + 1 + i) = 0.0;
+  }
+  for (int64_t i = 0; i < n; ++i) d[static_cast<size_t>(i)] = at(i, i);
+  for (int64_t i = 0; i + 1 < n; ++i) e[static_cast<size_t>(i)] = at(i + 1, i);
+  // implicit QL with shifts on (d, e), e[i] coupling i and i + 1
+  for (int64_t l = 0; l < n; ++l) {
+    for (int iter = 0; iter < 100; ++iter) {
+      int64_t m = l;
+      for (; m + 1 < n; ++m) {
+        const double dd = std::fabs(d[static_cast<size_t>(m)]) + std::fabs(d[static_cast<size_t>(m + 1)]);
+        if (std::fabs(e[static_cast<size_t>(m)]) <= 1e-16 * dd) break;
+      }
+      if (m == l) break;
+      double g = (d[static_cast<size_t>(l + 1)] - d[static_cast<size_t>(l)]) / (2.0 * e[static_cast<size_t>(l)]);
+      double r = std::hypot(g, 1.0);
+      g = d[static_cast<size_t>(m)] - d[static_cast<size_t>(l)] + e[static_cast<size_t>(l)] / (g + (g >= 0.0 ? r : -r));
+      double sn = 1.0, c = 1.0, pp = 0.0;
+      int64_t i = m - 1;
+      bool early = false;
+      for (; i >= l; --i) {
+        const double f = sn * e[static_cast<size_t>(i)], b = c * e[static_cast<size_t>(i)];
+        r = std::hypot(f, g);
+        e[static_cast<size_t>(i + 1)] = r;
+        if (r == 0.0) {
+          d[static_cast<size_t>(i + 1)] -= pp;
+          e[static_cast<size_t>(m)] = 0.0;
+          early = true;
+          break;
+        }
+        sn = f / r;
+        c = g / r;
+        g = d[static_cast<size_t>(i + 1)] - pp;
+        r = (d[static_cast<size_t>(i)] - g) * sn + 2.0 * c * b;
+        pp = sn * r;
+        d[static_cast<size_t>(i + 1)] = g + pp;
+        g = c * r - b;
+      }
+      if (early) continue;
+      d[static_cast<size_t>(l)] -= pp;
+      e[static_cast<size_t>(l)] = g;
+      e[static_cast<size_t>(m)] = 0.0;
+    }
+  }
+  std::sort(d.begin(), d.end(), std::greater<double>());
+  return d;
 }
 
 LeverageScores row_leverage_scores(const KernelBlock& K, int64_t r) {
@@ -1006,6 +1103,16 @@ const std::vector<std::string>& compress_csv_header() {
 }
 }  // namespace
 
+std::vector<double> resolve_center(const ExperimentConfig& cfg, const PointSet& points, std::uint64_t data_seed) {
+  std::vector<double> center(static_cast<size_t>(points.cols), 0.0);
+  if (cfg.center_mode == CenterMode::RandomPoint) {
+    Rng crng(derive_seed(data_seed, 0xCE));
+    const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(points.rows)));
+    for (int64_t k = 0; k < points.cols; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+  }
+  return center;
+}
+
 // harness.hpp:143-328 (Normal dataset, RandomPoint center, method "id").
 void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out, std::ostream* log) {
   struct Accum {
@@ -1022,10 +1129,7 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
       const std::uint64_t data_seed = derive_seed(cfg.seed, static_cast<std::uint64_t>(trial), scheme_idx);
       // prepare_trial (harness.hpp:107-129)
       const PointSet points = gen_normal(cfg.d, cfg.N, derive_seed(data_seed, 0xDA7A));
-      Rng crng(derive_seed(data_seed, 0xCE));
-      const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(points.rows)));
-      std::vector<double> center(static_cast<size_t>(cfg.d));
-      for (int k = 0; k < cfg.d; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+      const std::vector<double> center = resolve_center(cfg, points, data_seed);
       SourceTargetSplit split;
       bool trial_failed = false;
       try {
@@ -1159,6 +1263,10 @@ double lambda_max(const Matrix& G) {
     sym_eig(G, ev, nullptr);
     return ev.empty() ? 0.0 : std::max(ev[0], 0.0);
   }
+  {
+    const std::vector<double> ev = sym_eigvals(G);
+    return ev.empty() ? 0.0 : std::max(ev[0], 0.0);
+  }
   std::vector<double> x(static_cast<size_t>(n), 1.0 / std::sqrt(static_cast<double>(n))), y(static_cast<size_t>(n));
   double lam = 0.0;
   for (int it = 0; it < 100000; ++it) {
@@ -1229,10 +1337,7 @@ BandwidthResult bandwidth_search(Device& dev, const ExperimentConfig& cfg, const
                                  std::uint64_t data_seed) {
   // prepare_trial(cfg, data_seed, /*assemble_matrix=*/false) (harness.hpp:107-129)
   const PointSet points = gen_normal(cfg.d, cfg.N, derive_seed(data_seed, 0xDA7A));
-  Rng crng(derive_seed(data_seed, 0xCE));
-  const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(points.rows)));
-  std::vector<double> center(static_cast<size_t>(cfg.d));
-  for (int k = 0; k < cfg.d; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+  const std::vector<double> center = resolve_center(cfg, points, data_seed);
   const SourceTargetSplit split = split_sources_targets(dev, points, center, cfg.n_sources, cfg.xi);
   const double h_S = silverman_bandwidth(cfg.d, points.rows);
   const double target = spec.kappa * static_cast<double>(cfg.n_sources);
@@ -1396,6 +1501,13 @@ int kidh_sym_eig(const double* A, int64_t n, double* evals, double* evecs) {
   });
 }
 
+int kidh_sym_eigvals(const double* A, int64_t n, double* evals) {
+  return guard([&] {
+    const std::vector<double> ev = sym_eigvals(wrap(A, n, n));
+    std::memcpy(evals, ev.data(), sizeof(double) * ev.size());
+  });
+}
+
 // kind: 0 Uniform, 1 Bernoulli, 2 EuclideanNorm, 4 Leverage (weights given: host draw only)
 int kidh_draw(int32_t kind, int32_t replacement, int64_t m, const double* weights, double s, uint64_t seed,
               int64_t* out, int64_t* count) {
@@ -1548,7 +1660,7 @@ int kidh_interaction_fractions(int32_t device, int32_t d, int64_t N, uint64_t se
 // (also on SearchFailureError, status KID_E_ERROR) into prof (2 x prof_cap), its length into n_prof.
 int kidh_bandwidth_search(int32_t device, int32_t d, int64_t N, int64_t n, double xi, double kappa, int32_t large_h,
                           double eps, int32_t max_iters, int32_t tol_rows, uint64_t data_seed, double* out, double* prof,
-                          int32_t prof_cap, int32_t* n_prof) {
+                          int32_t prof_cap, int32_t* n_prof, int32_t center_random) {
   *n_prof = 0;
   auto dump = [&](const std::vector<std::pair<double, long>>& p) {
     const int32_t k = std::min<int32_t>(prof_cap, static_cast<int32_t>(p.size()));
@@ -1565,6 +1677,7 @@ int kidh_bandwidth_search(int32_t device, int32_t d, int64_t N, int64_t n, doubl
     cfg.N = N;
     cfg.n_sources = n;
     cfg.xi = xi;
+    cfg.center_mode = center_random ? CenterMode::RandomPoint : CenterMode::Origin;
     BandwidthSearchSpec spec;
     spec.kappa = kappa;
     spec.large_h_branch = large_h != 0;
@@ -1607,6 +1720,7 @@ int kidh_run_experiment(int32_t device, int32_t d, int64_t N, int64_t n, double 
     cfg.rank_rule = RankRule::from_eps(eps);
     cfg.trials = trials;
     cfg.seed = seed;
+    cfg.center_mode = CenterMode::RandomPoint;  // BASELINE.json configs: center uniformly among the points
     cfg.methods.clear();  // bit 0: id, bit 1: svd (config "methods", in that order)
     if (methods_mask & 1) cfg.methods.push_back(CompressionMethod::ID);
     if (methods_mask & 2) cfg.methods.push_back(CompressionMethod::SVD);

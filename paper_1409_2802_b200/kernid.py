@@ -41,6 +41,7 @@ def host_lib():
         L.kidh_epsilon_rank.argtypes = [_dp, i64, dbl, dbl, P(i64)]
         L.kidh_interpolative_decomposition.argtypes = [_dp, i64, i64, i64, _ip, _dp]
         L.kidh_sym_eig.argtypes = [_dp, i64, _dp, C.c_void_p]
+        L.kidh_sym_eigvals.argtypes = [_dp, i64, _dp]
         L.kidh_draw.argtypes = [i32, i32, i64, C.c_void_p, dbl, u64, _ip, P(i64)]
         L.kidh_kernel_rows.argtypes = [_dp, i64, i32, _ip, _ip, i64, _ip, i64, dbl, _dp]
         L.kidh_trial_next_rows.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, dbl, i32, u64, _dp,
@@ -50,7 +51,7 @@ def host_lib():
         L.kidh_trial_svd.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, P(i64), P(dbl), P(dbl), _dp]
         L.kidh_interaction_fractions.argtypes = [i32, i32, i64, u64, dbl, _dp, i64, _dp]
         L.kidh_bandwidth_search.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, dbl, i32, i32, u64, _dp, _dp, i32,
-                                            P(i32)]
+                                            P(i32), i32]
         L.kidh_run_experiment.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, i64, _dp, i32, dbl, i32, u64, C.c_char_p,
                                           i32, dbl, i32]
         _host = L
@@ -106,6 +107,15 @@ def interpolative_decomposition(A, r: int):
     P = np.zeros(max(r, 1) * n)
     _ck(host_lib().kidh_interpolative_decomposition(_cm(A), m, n, r, skel, P), "interpolative_decomposition")
     return skel[:r].copy(), _uncm(P[: r * n], r, n)
+
+
+def sym_eigvals(A):
+    """Eigenvalues (descending) of a symmetric matrix: Householder tridiagonalisation + QL."""
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    ev = np.zeros(n)
+    _ck(host_lib().kidh_sym_eigvals(_cm(A), n, ev), "sym_eigvals")
+    return ev
 
 
 def sym_eig(A):
@@ -216,14 +226,16 @@ class SearchFailure(KidError):
         self.profile = profile
 
 
-def bandwidth_search(d, N, n, xi, data_seed, kappa=0.2, large_h=False, eps=1e-2, max_iters=40, tol_rows=2, device=0):
-    """bandwidth_search (harness.hpp:330-438) through the mirror: dict(h_abs, h_over_hs, rank,
+def bandwidth_search(d, N, n, xi, data_seed, kappa=0.2, large_h=False, eps=1e-2, max_iters=40, tol_rows=2, device=0,
+                     center="origin"):
+    """bandwidth_search (harness.hpp:330-438) through the mirror (center: "origin", the reference
+    default, or "random"): dict(h_abs, h_over_hs, rank,
     evaluations, converged, profile); raises SearchFailure (with the profile) when it cannot bracket."""
     out = np.zeros(5)
     prof = np.zeros(2 * 256)
     npf = C.c_int32()
     rc = host_lib().kidh_bandwidth_search(device, d, N, n, xi, kappa, int(large_h), eps, max_iters, tol_rows, data_seed,
-                                          out, prof, 256, C.byref(npf))
+                                          out, prof, 256, C.byref(npf), int(center == "random"))
     profile = [(float(prof[2 * i]), int(prof[2 * i + 1])) for i in range(npf.value)]
     if rc:
         raise SearchFailure(rc, f"bandwidth_search: {host_lib().kidh_last_error().decode(errors='replace')}", profile)

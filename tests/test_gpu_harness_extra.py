@@ -68,3 +68,19 @@ def test_bandwidth_search_degenerate_budget(oracle):
         assert r["rank"] >= 90
     except H.SearchFailure as e:
         assert len(e.profile) > 0
+
+
+def test_bandwidth_search_acceptance(oracle):
+    """acceptance.cpp criterion 2: d = 4, N = 1e5, n = 500, xi = 1, kappa = 0.2, eps = 1e-2, seed
+    20240601; mean h / h_S over 5 seeds: small_h branch 0.1656 +- 0.024, large_h 1.1719 +- 0.05
+    (m = 500: the Gram route, eigenvalues by the tridiagonal QL solver)."""
+    from paper_1409_2802_b200 import kernid as H
+    ratios = {False: [], True: []}
+    for large in (False, True):
+        for seed_idx in range(5):
+            r = H.bandwidth_search(4, 100_000, 500, 1.0, oracle.derive_seed(20240601, seed_idx, 0xB5), kappa=0.2,
+                                   large_h=large, eps=1e-2, max_iters=40, tol_rows=2)
+            ratios[large].append(r["h_over_hs"])
+    small, large_ = np.mean(ratios[False]), np.mean(ratios[True])
+    assert abs(small - 0.1656) <= 0.024, ratios
+    assert abs(large_ - 1.1719) <= 0.05, ratios

@@ -117,3 +117,22 @@ def test_host_errors_mirror_reference(H):
     with pytest.raises(KidError) as e:
         H.interpolative_decomposition(u @ v.T, 3)
     assert e.value.code == KID_E_ILLCOND
+
+
+def test_sym_eigvals_vs_lapack():
+    """The eigenvalue-only host solver (Householder tridiagonalisation + implicit QL) used for the
+    m > 128 spectra, against LAPACK: random PSD, a Gaussian-kernel Gram with a fast-decaying
+    spectrum, repeated eigenvalues and the 1 x 1 case."""
+    import numpy as np
+    from paper_1409_2802_b200 import kernid as H
+    rng = np.random.default_rng(0)
+    for n in (1, 2, 7, 64, 300):
+        X = rng.standard_normal((n + 5, n))
+        A = X.T @ X
+        ref = np.linalg.eigvalsh(A)[::-1]
+        assert np.max(np.abs(H.sym_eigvals(A) - ref)) <= 1e-13 * ref[0]
+    x = np.linspace(0.0, 1.0, 257)
+    K = np.exp(-(x[:, None] - x[None, :]) ** 2 / 0.01)
+    ref = np.linalg.eigvalsh(K)[::-1]
+    assert np.max(np.abs(H.sym_eigvals(K) - ref)) <= 1e-13 * ref[0]
+    assert np.allclose(H.sym_eigvals(np.eye(9) * 3.0), 3.0, rtol=0, atol=1e-15)
