@@ -439,7 +439,15 @@ IDFactorization interpolative_decomposition(const Matrix& A, int64_t r) {
 }
 
 // Cyclic Jacobi eigen-solver for the symmetric m x m Grams (descending eigenvalues).
+namespace {
+void sym_tridiag_ql(const Matrix& A_in, std::vector<double>& d, Matrix* Z);
+}  // namespace
+
 void sym_eig(const Matrix& A_in, std::vector<double>& evals, Matrix* evecs) {
+  if (A_in.rows > 128) {  // Jacobi sweeps cost seconds at m = 256 / 512
+    sym_tridiag_ql(A_in, evals, evecs);
+    return;
+  }
   Matrix A = A_in;
   const int64_t n = A.rows;
   Matrix V(n, n);
@@ -490,25 +498,30 @@ void sym_eig(const Matrix& A_in, std::vector<double>& evals, Matrix* evecs) {
   }
 }
 
-// Eigenvalues (descending) of a symmetric matrix without vectors: Householder reduction to
-// tridiagonal form (A22 <- H A22 H by the rank-2 update A22 - v w^T - w v^T), then the implicit
-// QL iteration with Wilkinson shifts on the tridiagonal. O(n^3) with a small constant: the
-// eigenvalue-only host step for the m = 256 / 512 Grams, where Jacobi sweeps cost seconds.
-std::vector<double> sym_eigvals(const Matrix& A_in) {
+// Symmetric eigen-solver for the m > 128 host steps (m = 256 / 512 Grams), where Jacobi sweeps
+// cost seconds: Householder reduction to tridiagonal form (A22 <- H A22 H by the rank-2 update
+// A22 - v w^T - w v^T, the reflectors accumulated into Z when vectors are wanted), then the
+// implicit QL iteration with Wilkinson shifts on the tridiagonal, its Givens rotations applied to
+// Z. O(n^3). Eigenvalues descending; Z's columns are the matching eigenvectors.
+namespace {
+void sym_tridiag_ql(const Matrix& A_in, std::vector<double>& d, Matrix* Z) {
   const int64_t n = A_in.rows;
-  if (A_in.cols != n) throw DimensionError("sym_eigvals: matrix must be square");
+  if (A_in.cols != n) throw DimensionError("sym_eig: matrix must be square");
   std::vector<double> a(A_in.a);  // column-major, symmetric: a[i + j n]
   auto at = [&](int64_t i, int64_t j) -> double& { return a[static_cast<size_t>(i + j * n)]; };
-  std::vector<double> d(static_cast<size_t>(n)), e(static_cast<size_t>(n), 0.0);
-  std::vector<double> v(static_cast<size_t>(n)), p(static_cast<size_t>(n)), w(static_cast<size_t>(n));
+  d.assign(static_cast<size_t>(n), 0.0);
+  std::vector<double> e(static_cast<size_t>(n), 0.0), p(static_cast<size_t>(n)), w(static_cast<size_t>(n));
+  std::vector<std::vector<double>> vs(static_cast<size_t>(std::max<int64_t>(n - 2, 0)));
+  std::vector<double> betas(static_cast<size_t>(std::max<int64_t>(n - 2, 0)), 0.0);
   for (int64_t k = 0; k + 2 < n; ++k) {
     const int64_t m = n - k - 1;  // length of x = A[k+1:, k]
     double nrm = 0.0;
     for (int64_t i = 0; i < m; ++i) nrm += at(k + 1 + i, k) * at(k + 1 + i, k);
     nrm = std::sqrt(nrm);
-    const double x0 = at(k + 1, k);
     if (nrm == 0.0) continue;
-    const double alpha = x0 >= 0.0 ? -nrm : nrm;
+    const double x0 = at(k + 1, k), alpha = x0 >= 0.0 ? -nrm : nrm;
+    std::vector<double>& v = vs[static_cast<size_t>(k)];
+    v.assign(static_cast<size_t>(m), 0.0);
     double vn = 0.0;
     for (int64_t i = 0; i < m; ++i) {
       v[static_cast<size_t>(i)] = at(k + 1 + i, k) - (i == 0 ? alpha : 0.0);
@@ -516,6 +529,7 @@ std::vector<double> sym_eigvals(const Matrix& A_in) {
     }
     if (vn == 0.0) continue;
     const double beta = 2.0 / vn;  // H = I - beta v v^T
+    betas[static_cast<size_t>(k)] = beta;
     double K = 0.0;
     for (int64_t i = 0; i < m; ++i) {  // p = beta A22 v
       double acc = 0.0;
@@ -534,6 +548,22 @@ std::vector<double> sym_eigvals(const Matrix& A_in) {
   }
   for (int64_t i = 0; i < n; ++i) d[static_cast<size_t>(i)] = at(i, i);
   for (int64_t i = 0; i + 1 < n; ++i) e[static_cast<size_t>(i)] = at(i + 1, i);
+  if (Z) {  // Z = H_0 H_1 ... H_{n-3}, accumulated backwards
+    *Z = Matrix(n, n);
+    for (int64_t i = 0; i < n; ++i) (*Z)(i, i) = 1.0;
+    for (int64_t k = n - 3; k >= 0; --k) {
+      const std::vector<double>& v = vs[static_cast<size_t>(k)];
+      const double beta = betas[static_cast<size_t>(k)];
+      if (beta == 0.0) continue;
+      const int64_t m = n - k - 1;
+      for (int64_t j = k + 1; j < n; ++j) {
+        double s = 0.0;
+        for (int64_t i = 0; i < m; ++i) s += v[static_cast<size_t>(i)] * (*Z)(k + 1 + i, j);
+        s *= beta;
+        for (int64_t i = 0; i < m; ++i) (*Z)(k + 1 + i, j) -= s * v[static_cast<size_t>(i)];
+      }
+    }
+  }
   // implicit QL with shifts on (d, e), e[i] coupling i and i + 1
   for (int64_t l = 0; l < n; ++l) {
     for (int iter = 0; iter < 100; ++iter) {
@@ -547,9 +577,8 @@ std::vector<double> sym_eigvals(const Matrix& A_in) {
       double r = std::hypot(g, 1.0);
       g = d[static_cast<size_t>(m)] - d[static_cast<size_t>(l)] + e[static_cast<size_t>(l)] / (g + (g >= 0.0 ? r : -r));
       double sn = 1.0, c = 1.0, pp = 0.0;
-      int64_t i = m - 1;
       bool early = false;
-      for (; i >= l; --i) {
+      for (int64_t i = m - 1; i >= l; --i) {
         const double f = sn * e[static_cast<size_t>(i)], b = c * e[static_cast<size_t>(i)];
         r = std::hypot(f, g);
         e[static_cast<size_t>(i + 1)] = r;
@@ -566,6 +595,12 @@ std::vector<double> sym_eigvals(const Matrix& A_in) {
         pp = sn * r;
         d[static_cast<size_t>(i + 1)] = g + pp;
         g = c * r - b;
+        if (Z)
+          for (int64_t k = 0; k < n; ++k) {
+            const double zf = (*Z)(k, i + 1);
+            (*Z)(k, i + 1) = sn * (*Z)(k, i) + c * zf;
+            (*Z)(k, i) = c * (*Z)(k, i) - sn * zf;
+          }
       }
       if (early) continue;
       d[static_cast<size_t>(l)] -= pp;
@@ -573,7 +608,24 @@ std::vector<double> sym_eigvals(const Matrix& A_in) {
       e[static_cast<size_t>(m)] = 0.0;
     }
   }
-  std::sort(d.begin(), d.end(), std::greater<double>());
+  std::vector<int64_t> order(static_cast<size_t>(n));
+  std::iota(order.begin(), order.end(), int64_t{0});
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return d[static_cast<size_t>(x)] > d[static_cast<size_t>(y)]; });
+  std::vector<double> ds(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) ds[static_cast<size_t>(i)] = d[static_cast<size_t>(order[static_cast<size_t>(i)])];
+  d = ds;
+  if (Z) {
+    Matrix Zs(n, n);
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < n; ++i) Zs(i, j) = (*Z)(i, order[static_cast<size_t>(j)]);
+    *Z = std::move(Zs);
+  }
+}
+}  // namespace
+
+std::vector<double> sym_eigvals(const Matrix& A) {
+  std::vector<double> d;
+  sym_tridiag_ql(A, d, nullptr);
   return d;
 }
 

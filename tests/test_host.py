@@ -136,3 +136,20 @@ def test_sym_eigvals_vs_lapack():
     ref = np.linalg.eigvalsh(K)[::-1]
     assert np.max(np.abs(H.sym_eigvals(K) - ref)) <= 1e-13 * ref[0]
     assert np.allclose(H.sym_eigvals(np.eye(9) * 3.0), 3.0, rtol=0, atol=1e-15)
+
+
+def test_sym_eig_vectors_large():
+    """sym_eig for n > 128 (tridiagonal + QL with accumulated vectors): eigenpairs of a
+    Gaussian-kernel Gram against LAPACK -- residual ||A V - V L|| and orthogonality at ~u."""
+    import numpy as np
+    from paper_1409_2802_b200 import kernid as H
+    rng = np.random.default_rng(1)
+    n = 200
+    x = np.sort(rng.standard_normal(n))
+    K = np.exp(-(x[:, None] - x[None, :]) ** 2 / 0.1)
+    A = K.T @ K
+    ev, V = H.sym_eig(A)
+    ref = np.linalg.eigvalsh(A)[::-1]
+    assert np.max(np.abs(ev - ref)) <= 1e-13 * ref[0]
+    assert np.max(np.abs(A @ V - V * ev)) <= 1e-13 * ref[0]
+    assert np.max(np.abs(V.T @ V - np.eye(n))) <= 1e-12
