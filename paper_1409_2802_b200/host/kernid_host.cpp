@@ -902,6 +902,51 @@ std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, 
   return {std::move(id), rep};
 }
 
+namespace {
+// G = (K V_perp)^T (K V_perp) through the fused residual-Gram pass: with a = the ID skeleton of
+// V_r^T (CPQR) and P = [I, T] its projection, V_r^T V_perp = 0 gives T = -C_a C_b^-1 (C = V_perp
+// split by rows a / b), hence K V_perp = (K - K[:, a] P)[:, b] C_b: kid_recon_error on (a, P)
+// yields D'^T D' and G = C_b^T (D'^T D') C_b (C_b shares its singular values with V_r[a, :]).
+// Any orthonormal basis V_perp of the complement works. Optionally K^T K of the same pass.
+Matrix svd_residual_gram(Device& dev, double h, const Matrix& Vr, const Matrix& Vp, double* sumsq_K, Matrix* KtK) {
+  const int64_t m = Vr.rows, r = Vr.cols, n = m - r;
+  Matrix VrT(r, m);
+  for (int64_t j = 0; j < r; ++j)
+    for (int64_t i = 0; i < m; ++i) VrT(j, i) = Vr(i, j);
+  const IDFactorization idv = interpolative_decomposition(VrT, r);
+  Matrix DtDm(m, m);
+  double sdp = 0.0, sk = 0.0;
+  dev.check(kid_recon_error(dev.ctx(), h, idv.skeleton.data(), r, idv.projection.data(),
+                            KID_RECON_DTD | (KtK ? KID_RECON_KTK : 0u), &sdp, &sk, DtDm.data(),
+                            KtK ? KtK->data() : nullptr));
+  if (sumsq_K) *sumsq_K = sk;
+  std::vector<char> in_a(static_cast<size_t>(m), 0);
+  for (int64_t j : idv.skeleton) in_a[static_cast<size_t>(j)] = 1;
+  std::vector<int64_t> b;
+  for (int64_t i = 0; i < m; ++i)
+    if (!in_a[static_cast<size_t>(i)]) b.push_back(i);
+  Matrix Gp(n, n), Cb(n, n), T1(n, n), G(n, n);
+  for (int64_t y = 0; y < n; ++y)
+    for (int64_t x = 0; x < n; ++x) {
+      Gp(x, y) = DtDm(b[static_cast<size_t>(x)], b[static_cast<size_t>(y)]);
+      Cb(x, y) = Vp(b[static_cast<size_t>(x)], y);
+    }
+  for (int64_t y = 0; y < n; ++y)  // T1 = G' C_b
+    for (int64_t x = 0; x < n; ++x) {
+      double acc = 0.0;
+      for (int64_t l = 0; l < n; ++l) acc += Gp(x, l) * Cb(l, y);
+      T1(x, y) = acc;
+    }
+  for (int64_t y = 0; y < n; ++y)  // G = C_b^T T1
+    for (int64_t x = 0; x < n; ++x) {
+      double acc = 0.0;
+      for (int64_t l = 0; l < n; ++l) acc += Cb(l, x) * T1(l, y);
+      G(x, y) = acc;
+    }
+  return G;
+}
+}  // namespace
+
 // compress.hpp:219-273 with the error pass on the device: ||K - K V_r V_r^T||_2 = ||K V_perp||_2,
 // V_perp = the trailing m - r columns of the full right factor, through the fused residual-Gram
 // pass (kid_recon_error) on the ID of V_r^T (the N_T x m difference is never formed; the generic
@@ -938,43 +983,7 @@ std::pair<Matrix, CompressionReport> compress_svd(const KernelBlock& K, const Ro
       Matrix Vp(m, n);
       for (int64_t j = 0; j < n; ++j)
         for (int64_t i = 0; i < m; ++i) Vp(i, j) = rf.V(i, r + j);
-      // The fused residual pass computes ||K V_perp|| too: with a = the ID skeleton of V_r^T
-      // (r x m, CPQR) and P its projection ([I, T], T = V_r[a,:]^-T V_r[b,:]^T), b the other n
-      // columns and C_b = V_perp[b, :]: K V_perp = (K_b - K_a (-T)) ... = (K - K[:, a] P)[:, b] C_b
-      // because V_r^T V_perp = 0 gives -C_a C_b^-1 = T. So D' = (K - K[:, a] P)[:, b] comes from
-      // the residual-Gram kernel and G = C_b^T (D'^T D') C_b on the host; C_b is well conditioned
-      // (its singular values are those of V_r[a, :], CPQR-selected).
-      Matrix VrT(r, m);
-      for (int64_t j = 0; j < r; ++j)
-        for (int64_t i = 0; i < m; ++i) VrT(j, i) = rf.V(i, j);
-      const IDFactorization idv = interpolative_decomposition(VrT, r);
-      Matrix DtDm(m, m);
-      double sdp = 0.0;
-      K.device().check(kid_recon_error(K.device().ctx(), K.spec().h, idv.skeleton.data(), r, idv.projection.data(),
-                                       KID_RECON_DTD, &sdp, &sk, DtDm.data(), nullptr));
-      std::vector<char> in_a(static_cast<size_t>(m), 0);
-      for (int64_t j : idv.skeleton) in_a[static_cast<size_t>(j)] = 1;
-      std::vector<int64_t> b;
-      for (int64_t i = 0; i < m; ++i)
-        if (!in_a[static_cast<size_t>(i)]) b.push_back(i);
-      Matrix Gp(n, n), Cb(n, n), T1(n, n), G(n, n);
-      for (int64_t y = 0; y < n; ++y)
-        for (int64_t x = 0; x < n; ++x) {
-          Gp(x, y) = DtDm(b[static_cast<size_t>(x)], b[static_cast<size_t>(y)]);
-          Cb(x, y) = Vp(b[static_cast<size_t>(x)], y);
-        }
-      for (int64_t y = 0; y < n; ++y)  // T1 = G' C_b
-        for (int64_t x = 0; x < n; ++x) {
-          double acc = 0.0;
-          for (int64_t l = 0; l < n; ++l) acc += Gp(x, l) * Cb(l, y);
-          T1(x, y) = acc;
-        }
-      for (int64_t y = 0; y < n; ++y)  // G = C_b^T T1
-        for (int64_t x = 0; x < n; ++x) {
-          double acc = 0.0;
-          for (int64_t l = 0; l < n; ++l) acc += Cb(l, x) * T1(l, y);
-          G(x, y) = acc;
-        }
+      const Matrix G = svd_residual_gram(K.device(), K.spec().h, Vr, Vp, &sk, nullptr);
       for (int64_t i = 0; i < n; ++i) sd += G(i, i);
       std::vector<double> ev;
       sym_eig(G, ev, nullptr);
@@ -1087,10 +1096,16 @@ std::vector<double> mc_error_svd(const KernelBlock& K, const Matrix& Vr, double 
     if (rows.indices.empty()) rows = sample_rows(bern, ctx, s_mc, derive_seed(seed, static_cast<std::uint64_t>(rep), 1));
     if (rows.indices.empty()) throw Error("mc_error: Bernoulli draw empty twice; s_mc is too small for this matrix");
     K.device().check(kid_select_rows(c, rows.indices.data(), static_cast<int64_t>(rows.indices.size())));
-    Matrix KtK(m, m), DtD(std::max<int64_t>(n, 1), std::max<int64_t>(n, 1));
-    double sd = 0.0, sk = 0.0;
-    int rc = kid_gram(c, K.spec().h, KtK.data(), &sk);
-    if (!rc && n > 0) rc = kid_proj_gram(c, K.spec().h, Vp.data(), n, &sd, &sk, DtD.data());
+    Matrix KtK(m, m), DtD;
+    double sk = 0.0;
+    int rc = KID_OK;
+    try {  // the row subset is restored whatever happens
+      if (n > 0) DtD = svd_residual_gram(K.device(), K.spec().h, Vr, Vp, &sk, &KtK);
+      else rc = kid_gram(c, K.spec().h, KtK.data(), &sk);
+    } catch (...) {
+      kid_select_rows(c, nullptr, -1);
+      throw;
+    }
     K.device().check(kid_select_rows(c, nullptr, -1));
     K.device().check(rc);
     std::vector<double> ed, ek;
