@@ -1321,39 +1321,12 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
 
 // ------------------------------------------------------------------ interaction fractions
 namespace {
-// largest eigenvalue of a symmetric PSD matrix: Jacobi for small n, else power iteration
-// (Rayleigh quotient to 1e-15 relative change)
+// largest eigenvalue of a symmetric PSD matrix
 double lambda_max(const Matrix& G) {
-  const int64_t n = G.rows;
-  if (n <= 128) {
-    std::vector<double> ev;
-    sym_eig(G, ev, nullptr);
-    return ev.empty() ? 0.0 : std::max(ev[0], 0.0);
-  }
-  {
-    const std::vector<double> ev = sym_eigvals(G);
-    return ev.empty() ? 0.0 : std::max(ev[0], 0.0);
-  }
-  std::vector<double> x(static_cast<size_t>(n), 1.0 / std::sqrt(static_cast<double>(n))), y(static_cast<size_t>(n));
-  double lam = 0.0;
-  for (int it = 0; it < 100000; ++it) {
-    for (int64_t i = 0; i < n; ++i) {
-      double acc = 0.0;
-      for (int64_t j = 0; j < n; ++j) acc += G(i, j) * x[static_cast<size_t>(j)];
-      y[static_cast<size_t>(i)] = acc;
-    }
-    double nrm = 0.0, rq = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      nrm += y[static_cast<size_t>(i)] * y[static_cast<size_t>(i)];
-      rq += x[static_cast<size_t>(i)] * y[static_cast<size_t>(i)];
-    }
-    nrm = std::sqrt(nrm);
-    if (nrm == 0.0) return 0.0;
-    for (int64_t i = 0; i < n; ++i) x[static_cast<size_t>(i)] = y[static_cast<size_t>(i)] / nrm;
-    if (it > 3 && std::fabs(rq - lam) <= 1e-15 * rq) return rq;
-    lam = rq;
-  }
-  return lam;
+  std::vector<double> ev;
+  if (G.rows <= 128) sym_eig(G, ev, nullptr);  // Jacobi
+  else ev = sym_eigvals(G);                     // tridiagonal + QL
+  return ev.empty() ? 0.0 : std::max(ev[0], 0.0);
 }
 }  // namespace
 
