@@ -57,6 +57,8 @@ WORKLOADS = {
     "c3-d5": dict(d=5, N=1_000_000, m=100, xi=3.0, h_value=1.0, s=0.02, eps=1e-8),
     "c4-d16": dict(d=16, N=12_000_000, m=256, xi=2.0, h_value=1.0, s=0.002, eps=1e-2),
     "c5-d8-shard": dict(d=8, N=12_515_000, m=512, xi=2.0, h_value=1.0, s=0.002, eps=1e-2),
+    # configs[4] at N=1 GPU: the largest single-GPU configuration (1.0012e8 points, 6.4 GB)
+    "c5": dict(d=8, N=100_120_000, m=512, xi=2.0, h_value=1.0, s=4e-5, eps=1e-2),
 }
 
 
@@ -462,7 +464,7 @@ def run_next_pass(args):
         r = H.epsilon_rank(sv, wl["eps"])
         n = m - r
         out = torch.empty(2 + n * n, dtype=torch.float64, device="cuda")
-        if os.environ.get("KID_SVD_PROJ"):  # the generic projected Gram over V_perp
+        if args.svd_proj:  # the generic projected Gram over V_perp
             Vp = Vt.T[:, r:]
             Cm = torch.tensor(np.ascontiguousarray(Vp.T).ravel(), dtype=torch.float64, device="cuda")
             fn = lambda: dev.proj_gram_dev(prob.h, Cm.data_ptr(), n, out.data_ptr())
@@ -667,6 +669,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=50000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--svd-proj", action="store_true", help="--pass svd through kid_proj_gram (C = V_perp) instead of the ID route")
     ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms", "gram", "leverage"])
     args = ap.parse_args()
     if args.warmup < 3:

@@ -158,6 +158,7 @@ int64_t epsilon_rank(const std::vector<double>& sv, double eps,
 IDFactorization interpolative_decomposition(const Matrix& A, int64_t r);     // :235-262
 void sym_eig(const Matrix& A, std::vector<double>& evals, Matrix* evecs);   // Gram route (Jacobi)
 std::vector<double> sym_eigvals(const Matrix& A);                           // tridiagonal + QL, values only
+double lambda_max(const Matrix& G);  // largest eigenvalue of a symmetric PSD matrix (Jacobi / Lanczos)
 LeverageScores row_leverage_scores(const KernelBlock& K, int64_t r);        // :296-308 (device)
 
 // ------------------------------------------------------------- sampling.hpp

@@ -43,7 +43,7 @@ extern "C" {
 
 /* kid_recon_error flags */
 #define KID_RECON_DTD 1u     /* accumulate the residual Gram D^T D (spectral norm, compress.hpp:141-154) */
-#define KID_RECON_KTK 2u     /* also accumulate K^T K in the same pass (matrix_norm, compress.hpp:156-159) */
+#define KID_RECON_KTK 2u     /* also form K^T K (matrix_norm, compress.hpp:156-159): a second Gram pass over the block */
 
 typedef struct kid_ctx kid_ctx;
 
@@ -59,6 +59,13 @@ const char* kid_last_error(const kid_ctx* ctx);
 /* Run subsequent work on an external cudaStream_t (NULL: the context's own stream). */
 int kid_set_stream(kid_ctx* ctx, void* cuda_stream);
 int kid_synchronize(kid_ctx* ctx);
+/* Kernel family of the Gram / leverage / projected passes. AUTO: the single-CTA fused kernels where the
+   block fits one SM, the 2-CTA cluster kernel otherwise (m = 256 / 512). CLUSTER: always the cluster
+   kernel (used by the tests to check both families on the same small blocks). Replaces no reference
+   interface: the reference has one dense path (kernel.hpp:202-208). */
+#define KID_PATH_AUTO 0
+#define KID_PATH_CLUSTER 1
+int kid_set_path(kid_ctx* ctx, int32_t path);
 
 /* ---- point set (PointSet, kernel.hpp:14): N x d column-major ----
  * index_offset: global index of local row 0 when the point set is sharded across ranks. */

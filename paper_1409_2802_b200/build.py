@@ -16,7 +16,7 @@ CUDA_SO = os.path.join(PKG, "libkernid_cuda.so")
 HOST_SO = os.path.join(PKG, "libkernid_host.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SRCS = ["kid_capi.cu", "kid_split.cu", "kid_passes.cu", "kid_next.cu"]
+CU_SRCS = ["kid_capi.cu", "kid_split.cu", "kid_passes.cu", "kid_next.cu", "kid_fused.cu"]
 HOST_SRCS = ["kernid_host.cpp"]
 
 
@@ -32,7 +32,7 @@ def build_cuda(force=False, verbose=False):
     if not force and not _stale(CUDA_SO, deps):
         return CUDA_SO
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-warn-spills", "-o", CUDA_SO] + [os.path.join(CSRC, f) for f in CU_SRCS] + ["-lcublas"]
+           "-Xptxas", "-warn-spills", "-o", CUDA_SO] + [os.path.join(CSRC, f) for f in CU_SRCS]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

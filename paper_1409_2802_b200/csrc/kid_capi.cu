@@ -140,10 +140,6 @@ void kid_destroy(kid_ctx* c) {
     if (p) cudaFree(p);
   if (c->hbuf) cudaFreeHost(c->hbuf);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
-  if (c->blas) cublasDestroy(c->blas);
-  for (cudaEvent_t e : c->aux_ev)
-    if (e) cudaEventDestroy(e);
-  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -153,6 +149,13 @@ const char* kid_last_error(const kid_ctx* c) { return c ? c->err.c_str() : "null
 int kid_set_stream(kid_ctx* c, void* s) {
   if (!c) return KID_E_ERROR;
   c->stream = s ? (cudaStream_t)s : c->own_stream;
+  return KID_OK;
+}
+
+int kid_set_path(kid_ctx* c, int32_t path) {
+  if (!c) return KID_E_ERROR;
+  if (path != KID_PATH_AUTO && path != KID_PATH_CLUSTER) return fail(c, KID_E_RANGE, "kid_set_path: unknown path");
+  c->path = path;
   return KID_OK;
 }
 
@@ -236,7 +239,7 @@ int kid_split(kid_ctx* c, const double* center, int64_t n, double xi, int64_t* s
   if (xi < 0.0) return fail(c, KID_E_RANGE, "split_sources_targets: requires xi >= 0");
   if (int rc = set_device(c)) return rc;
   {
-    const int rc = getenv("KID_SPLIT_HOST") ? 1 : split_device(c, center, n, xi, src_idx_out, rho_out, n_targets_out);
+    const int rc = split_device(c, center, n, xi, src_idx_out, rho_out, n_targets_out);
     if (rc == KID_OK && *n_targets_out == 0)
       return fail(c, KID_E_NO_TARGETS,
                   "split_sources_targets: no targets at separation xi = " + std::to_string(xi) + " (try a smaller xi)");
@@ -319,7 +322,7 @@ int kid_gram_dev(kid_ctx* c, double h, double* d_G, double* d_sumsq) {
   if (!c || !d_G) return KID_E_ERROR;
   // d_G receives [sumsq_K (unused slot), sumsq_K, G (m x m)] when d_sumsq is null
   (void)d_sumsq;
-  return gram_dev(c, h, 0, 0, d_G);
+  return gram_dev(c, h, 0, d_G);
 }
 
 int kid_gram(kid_ctx* c, double h, double* G_out, double* sumsq_K_out) {
@@ -328,7 +331,7 @@ int kid_gram(kid_ctx* c, double h, double* G_out, double* sumsq_K_out) {
   const int64_t m = c->m;
   double* d_out = out_buffer(c, 2 + m * m);
   if (!d_out) return KID_E_OOM;
-  if (int rc = gram_dev(c, h, 0, 0, d_out)) return rc;
+  if (int rc = gram_dev(c, h, 0, d_out)) return rc;
   std::vector<double> tmp(2);
   KID_CK(c, cudaMemcpyAsync(tmp.data(), d_out, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
   KID_CK(c, cudaMemcpyAsync(G_out, d_out + 2, sizeof(double) * m * m, cudaMemcpyDeviceToHost, c->stream));
@@ -452,6 +455,7 @@ int kid_recon_prepare(kid_ctx* c, const int64_t* skel, int64_t r, const double* 
   if (ensure(c, (void**)&c->P2, &c->P2_cap, sizeof(double) * p2.size())) return KID_E_OOM;
   KID_CK(c, cudaMemcpyAsync(c->P2, p2.data(), sizeof(double) * p2.size(), cudaMemcpyHostToDevice, c->stream));
   KID_CK(c, cudaStreamSynchronize(c->stream));
+  c->P2_host = std::move(p2);
   c->r = r;
   return KID_OK;
 }
@@ -461,7 +465,8 @@ int kid_recon_error_dev(kid_ctx* c, double h, uint32_t flags, double* d_out) {
   if (!c || !d_out) return KID_E_ERROR;
   if (c->r == 0 && c->skel_h.empty() && c->nonskel.empty())
     return fail(c, KID_E_ERROR, "kid_recon_error_dev: call kid_recon_prepare first");
-  return gram_dev(c, h, c->r, flags, d_out);
+  (void)flags;
+  return gram_dev(c, h, c->r, d_out);
 }
 
 int kid_recon_error(kid_ctx* c, double h, const int64_t* skel, int64_t r, const double* P, uint32_t flags,
@@ -473,7 +478,7 @@ int kid_recon_error(kid_ctx* c, double h, const int64_t* skel, int64_t r, const 
   if (!d_out) return KID_E_OOM;
   if (meff == 0) {
     // full-rank skeleton: D == 0; ||K||_F^2 still needed
-    if (int rc = gram_dev(c, h, 0, 0, d_out + 2)) return rc;
+    if (int rc = gram_dev(c, h, 0, d_out + 2)) return rc;
     std::vector<double> t(2);
     KID_CK(c, cudaMemcpyAsync(t.data(), d_out + 2, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
     if (KtK) KID_CK(c, cudaMemcpyAsync(KtK, d_out + 4, sizeof(double) * m * m, cudaMemcpyDeviceToHost, c->stream));
@@ -483,12 +488,12 @@ int kid_recon_error(kid_ctx* c, double h, const int64_t* skel, int64_t r, const 
     if (DtD) std::fill(DtD, DtD + m * m, 0.0);
     return KID_OK;
   }
-  if (int rc = gram_dev(c, h, r, flags, d_out)) return rc;
+  if (int rc = gram_dev(c, h, r, d_out)) return rc;
   std::vector<double> g(2 + meff * meff);
   KID_CK(c, cudaMemcpyAsync(g.data(), d_out, sizeof(double) * g.size(), cudaMemcpyDeviceToHost, c->stream));
   double* k_out = d_out + 2 + meff * meff;
   if (flags & KID_RECON_KTK) {
-    if (int rc = gram_dev(c, h, 0, 0, k_out)) return rc;
+    if (int rc = gram_dev(c, h, 0, k_out)) return rc;
     if (KtK) KID_CK(c, cudaMemcpyAsync(KtK, k_out + 2, sizeof(double) * m * m, cudaMemcpyDeviceToHost, c->stream));
   }
   KID_CK(c, cudaStreamSynchronize(c->stream));

@@ -9,24 +9,35 @@
 namespace kid {
 namespace {
 
-__device__ double c_exp2_tab[kExpTab];  // 2^(j/64); each CTA stages it in shared memory, replicated per lane
+// 2^(j/64), correctly rounded (generated from a 60-digit decimal evaluation; identical to
+// exp2l(j/64) rounded to double). A static initializer: no upload, so no ordering question between
+// a legacy-stream copy and the non-blocking stream the passes launch on.
+__device__ const double c_exp2_tab[kExpTab] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
+};
 
 // shared table [j][lane] (kExpTabWords doubles) for exp_neg_fast(q, tab + lane)
 __device__ __forceinline__ void stage_exp_table(double* tabr, int tid, int nthr) {
   for (int e = tid; e < kExpTabWords; e += nthr) tabr[e] = c_exp2_tab[e / kExpRep];
 }
 
-int init_device_tables() {
-  static thread_local int done_dev = -1;
-  int dev = -1;
-  if (cudaGetDevice(&dev) != cudaSuccess) return KID_E_CUDA;
-  if (done_dev == dev) return KID_OK;
-  double tab[kExpTab];
-  for (int j = 0; j < kExpTab; ++j) tab[j] = (double)exp2l((long double)j / (long double)kExpTab);
-  if (cudaMemcpyToSymbol(c_exp2_tab, tab, sizeof(tab)) != cudaSuccess) return KID_E_CUDA;
-  done_dev = dev;
-  return KID_OK;
-}
+// kept for the call sites: the table needs no device-side initialisation any more
+inline int init_device_tables() { return KID_OK; }
 
 constexpr int kTM = 32;        // targets per tile (SYRK k-depth: 8 DMMA k-steps)
 constexpr int kNT = 256;       // threads per CTA

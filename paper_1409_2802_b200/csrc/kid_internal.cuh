@@ -10,7 +10,6 @@
 // K itself is never stored: every FP64 pass re-evaluates its target tile in registers
 // / shared memory (SURVEY.md 8a A5 "never materialised on GPU").
 #pragma once
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -80,7 +79,9 @@ __device__ __forceinline__ double exp_neg_fast(double q, const double* __restric
 // applied to all N before the next) so the N dependency chains stay interleaved in the SASS --
 // ptxas otherwise tends to serialise them under a tight register budget. Same arithmetic, same
 // results as N calls of exp_neg_fast.
-template <int N>
+// REP: table replicas (row stride of the [j][replica] table): 32 (one per lane), or 16 -- a 64-bit
+// shared load is served per half-warp, so lanes l and l + 16 may share a replica conflict-free.
+template <int N, int REP = kExpRep>
 __device__ __forceinline__ void exp_neg_fast_n(double (&q)[N], const double* __restrict__ tabl) {
   const double shifter = 6755399441055744.0;
   double kd[N], r[N], p[N], t[N];
@@ -92,7 +93,7 @@ __device__ __forceinline__ void exp_neg_fast_n(double (&q)[N], const double* __r
 #pragma unroll
   for (int u = 0; u < N; ++u) {
     n[u] = __double2loint(kd[u]);
-    t[u] = tabl[(n[u] & (kExpTab - 1)) * kExpRep];
+    t[u] = tabl[(n[u] & (kExpTab - 1)) * REP];
   }
 #pragma unroll
   for (int u = 0; u < N; ++u) kd[u] -= shifter;
@@ -188,6 +189,7 @@ struct kid_ctx {
   std::vector<double> src_host;       // host copies (m x d col-major) of src / src_perm: the fused
   std::vector<double> src_perm_host;  // pass carries them in its kernel parameters
   double* P2 = nullptr;        // r x meff row-major, stride = r-major padded
+  std::vector<double> P2_host;  // host copy of P2 (the large-m fused pass builds its per-CTA images from it)
   size_t P2_cap = 0;
   std::vector<int64_t> nonskel;  // host: original column of each non-skeleton column
   std::vector<int64_t> skel_h;
@@ -200,9 +202,7 @@ struct kid_ctx {
   double* hbuf = nullptr;  // pinned host staging
   size_t hbuf_cap = 0;
   int64_t* counter = nullptr;  // device counters [8]
-  cublasHandle_t blas = nullptr;  // large-m fallback of the Gram passes
-  cudaStream_t aux_stream = nullptr;  // large-m path: K-batch evaluation overlapping the DGEMMs
-  cudaEvent_t aux_ev[5] = {};
+  int path = KID_PATH_AUTO;  // kid_set_path: which kernel family serves the Gram / leverage passes
   void* sort_tmp = nullptr;       // CUB radix-sort temporary storage (pass 1)
   size_t sort_tmp_cap = 0;
 
@@ -241,23 +241,20 @@ int split_finish(kid_ctx* c, const int64_t* src_idx_h, int64_t n, const double* 
 int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64_t* src_idx_out, double* rho_out,
                  int64_t* n_targets_out);
 int row_norms_dev(kid_ctx* c, double h, double* d_w);
-int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out);
+int gram_dev(kid_ctx* c, double h, int64_t r, double* d_out);
 int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores);
 int tsqr_dev(kid_ctx* c, double h, const double* d_Rin, int64_t nR, int64_t m, double* d_R);
 int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n, double* d_out);
-// large-m building blocks (kid_passes.cu), shared with kid_next.cu
-constexpr int kSyrkParts = 297;  // row chunks of the batched Gram (+1 remainder)
-int tall_syrk(kid_ctx* c, const double* D, int rows, int ld, int n, double* G, bool accumulate, double* part,
-              int max_parts);
+// launch wrapper shared with kid_next.cu (no relocatable device code)
 int launch_gram_reduce(kid_ctx* c, const double* partial, int nchunks, int LG, int n, const double* partial_sk,
                        int nparts, double* out);
-int launch_eval_batch(kid_ctx* c, cudaStream_t st, const double* src, double cscale, int64_t t0, int rows, int ev_rows,
-                      int ev_cols, bool staged, double* Kb, double* skp);
-int launch_large_finish(kid_ctx* c, double* G, int n, const double* skp, int nsk, double* out);
 int eval_rows_dev(kid_ctx* c, double h, const int64_t* d_rows, int64_t count, double* d_Ks);
 int apply_skeleton_dev(kid_ctx* c, double h, const int64_t* skel, int64_t r, const double* q_skel, double* d_u);
 int select_rows(kid_ctx* c, const int64_t* rows, int64_t n);
 int exp_check_dev(kid_ctx* c, const double* d_x, int64_t n, double* d_y);
+// large-m fused passes on a 2-CTA cluster (kid_fused.cu): D = K_B + K_A M, then D^T D or row sums of D^2
+enum : int { FX_RESID = 0, FX_GRAM = 1, FX_PROJ = 2, FX_LEV = 3 };
+int fused_dev(kid_ctx* c, double h, int mode, const double* M_host, int64_t n, double* d_out);
 // event pair bracketing the dominant kernel of a pass (no-op unless profiling)
 void prof_begin(kid_ctx* c);
 void prof_end(kid_ctx* c);

@@ -9,7 +9,6 @@
 #include <cstring>
 #include <vector>
 
-#include <cublas_v2.h>
 
 #include "kid_device.cuh"
 
@@ -72,7 +71,7 @@ __global__ void __launch_bounds__(kPT, 1) k_proj_gram(const ProjArgs A) {
   }
   for (int e = tid; e < d * m4; e += kPT) {
     const int k = e / m4, j = e - k * m4;
-    s_src[e] = j < m ? A.src[j + (size_t)k * m] * A.cscale : 1.0e4;
+    s_src[e] = j < m ? A.src[j + (size_t)k * m] * A.cscale : 1.0e150;
   }
   for (int b = tid; b < nblk; b += kPT) {  // upper-triangular block list, row-major
     int a = 0, rem = b;
@@ -272,7 +271,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
   if (EVAL)
     for (int e = tid; e < d * m4; e += kQThreads) {
       const int k = e / m4, j = e - k * m4;
-      s_src[e] = j < m ? A.src[j + (size_t)k * m] * A.cscale : 1.0e4;
+      s_src[e] = j < m ? A.src[j + (size_t)k * m] * A.cscale : 1.0e150;
     }
   const int64_t t_lo = A.ntiles * blockIdx.x / gridDim.x, t_hi = A.ntiles * (blockIdx.x + 1) / gridDim.x;
   const double* tabl = s_tab + lane;
@@ -478,7 +477,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_tsqr(const TsqrArgs A) {
 
 // G = (K C)^T (K C) for a device m x n coefficient matrix C (col-major); d_out = [||K C||_F^2,
 // ||K||_F^2, G (n x n col-major)]. Fused k_proj_gram when its shared-memory footprint fits, else
-// the batched path (K batch in HBM, D = K C by DGEMM, G += D^T D by DSYRK).
+// the cluster kernel of kid_fused.cu (K never leaves the SMs in either).
 int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n64, double* d_out) {
   if (int rc = check_block(c, h)) return rc;
   const int m = (int)c->m, d = c->d, n = (int)n64;
@@ -487,7 +486,7 @@ int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n64, double* 
   const double cscale = std::sqrt(1.0 / (2.0 * h * h));
   const int LG = ceil_to(n, 8);
   const size_t smem = proj_smem_bytes(m, n, d);
-  if (LG <= 128 && smem <= 200 * 1024 && !getenv("KID_FORCE_LARGE")) {
+  if (LG <= 128 && smem <= 200 * 1024 && c->path != KID_PATH_CLUSTER) {
     const int64_t ntiles = (c->nt + kTM - 1) / kTM;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms, (ntiles + kPG - 1) / kPG));
     const int nworkers = blocks * kPG;
@@ -520,49 +519,11 @@ int proj_gram_dev(kid_ctx* c, double h, const double* d_C, int64_t n64, double* 
     if (int rc = launch_gram_reduce(c, A.partial, nworkers, LG, n, A.partial_sk, 1, d_out)) return rc;
     return KID_OK;
   }
-  // batched path
-  if (!c->blas) {
-    if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return fail(c, KID_E_CUDA, "cublasCreate failed");
-  }
-  cublasSetStream(c->blas, c->stream);
-  cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
-  const int64_t nt = c->nt;
-  const int B = (int)std::max<int64_t>(1024, std::min<int64_t>(nt, (int64_t)(1ll << 30) / (8ll * (m + n))));
-  const int64_t nbatch = std::max<int64_t>(1, (nt + B - 1) / B);
-  const int ev_rows = (B + 255) / 256;
-  const int ev_cols = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_to(m, 4) / 4, (4ll * c->sms + ev_rows - 1) / ev_rows));
-  const int ev_blocks = ev_rows * ev_cols;
-  const bool ev_staged = sizeof(double) * (size_t)d * ceil_to(m, 4) <= 160 * 1024;
-  const size_t ev_smem = ev_staged ? sizeof(double) * (size_t)d * ceil_to(m, 4) : 0;
-  char* base = (char*)scratch(c, sizeof(double) * ((size_t)B * (m + n) + (size_t)n * n + (size_t)nbatch * ev_blocks +
-                                                  (size_t)kSyrkParts * n * n + 64));
-  if (!base) return KID_E_OOM;
-  double* Kb = (double*)base;
-  double* Db = Kb + (size_t)B * m;
-  double* G = Db + (size_t)B * n;
-  double* skp = G + (size_t)n * n;
-  double* gpart = skp + (size_t)nbatch * ev_blocks;
-  const double one = 1.0, zero = 0.0;
-  if (nt == 0) {
-    KID_CK(c, cudaMemsetAsync(G, 0, sizeof(double) * n * n, c->stream));
-    KID_CK(c, cudaMemsetAsync(skp, 0, sizeof(double) * ev_blocks, c->stream));
-  }
-  prof_begin(c);
-  for (int64_t b = 0; b < nbatch && nt > 0; ++b) {
-    const int64_t t0 = b * (int64_t)B;
-    const int rows = (int)std::min<int64_t>(B, nt - t0);
-if (int rc = launch_eval_batch(c, c->stream, c->src, cscale, t0, rows, ev_rows, ev_cols, ev_staged, Kb,
-                                  skp + b * ev_blocks)) return rc;
-    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, n, m, &one, Kb, rows, d_C, m, &zero, Db, rows) !=
-        CUBLAS_STATUS_SUCCESS)
-      return fail(c, KID_E_CUDA, "cublasDgemm failed");
-    c->launches++;
-    if (int rc = tall_syrk(c, Db, rows, rows, n, G, b > 0, gpart, kSyrkParts)) return rc;
-  }
-  prof_end(c);
-  const int nsk = nt == 0 ? ev_blocks : (int)(nbatch * ev_blocks);
-  if (int rc = launch_large_finish(c, G, n, skp, nsk, d_out)) return rc;
-  return KID_OK;
+  // beyond one SM's shared memory (c4 / c5): the 2-CTA cluster kernel (kid_fused.cu) with M = C
+  std::vector<double> Ch((size_t)m * n);
+  KID_CK(c, cudaMemcpyAsync(Ch.data(), d_C, sizeof(double) * Ch.size(), cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  return fused_dev(c, h, FX_PROJ, Ch.data(), n, d_out);
 }
 
 // Upper-triangular R (m x m col-major, device) with R^T R = K^T K, by TSQR over all targets
@@ -641,59 +602,14 @@ int tsqr_dev(kid_ctx* c, double h, const double* d_Rin, int64_t nR, int64_t m64,
   return KID_OK;
 }
 
-// scores[t0 + i] = sum_j KW[i + j * rows]^2 (KW rows x r column-major, coalesced over i)
-__global__ void k_rowsq(const double* __restrict__ KW, int rows, int r, double* __restrict__ scores) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int j = 0; j < r; ++j) {
-      const double v = KW[i + (size_t)j * rows];
-      s = fma(v, v, s);
-    }
-    scores[i] = s;
-  }
-}
-
-// Leverage for W that does not fit shared memory (c4 m = 256, c5 m = 512): a 1 GB batch of K
-// rows (k_eval_batch), KW = K_b W by DGEMM (W read once per batch instead of once per tile),
-// row sums of squares.
+// Leverage for W beyond one SM's shared memory (c4 m = 256, c5 m = 512): the cluster kernel of
+// kid_fused.cu in leverage mode (K W on DMMA across the CTA pair, row sums of squares).
 int leverage_dev_large(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores) {
-  const int m = (int)c->m, d = c->d, rr = (int)r;
-  if (!c->blas) {
-    if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return fail(c, KID_E_CUDA, "cublasCreate failed");
-  }
-  cublasSetStream(c->blas, c->stream);
-  cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
-  const int64_t nt = c->nt;
-  const int B = (int)std::max<int64_t>(1024, std::min<int64_t>(nt, (int64_t)(1ll << 30) / (8ll * (m + rr))));
-  const int64_t nbatch = (nt + B - 1) / B;
-  const int ev_rows = (B + 255) / 256;
-  const int ev_cols = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_to(m, 4) / 4, (4ll * c->sms + ev_rows - 1) / ev_rows));
-  const int ev_blocks = ev_rows * ev_cols;
-  const bool ev_staged = sizeof(double) * (size_t)d * ceil_to(m, 4) <= 160 * 1024;
-  const size_t ev_smem = ev_staged ? sizeof(double) * (size_t)d * ceil_to(m, 4) : 0;
-  char* base = (char*)scratch(c, sizeof(double) * ((size_t)B * (m + rr) + (size_t)ev_blocks + 64));
-  if (!base) return KID_E_OOM;
-  double* Kb = (double*)base;
-  double* KW = Kb + (size_t)B * m;
-  double* skp = KW + (size_t)B * rr;  // ||K||^2 partials (unused here)
-  const double cscale = std::sqrt(1.0 / (2.0 * h * h));
-  const double one = 1.0, zero = 0.0;
-  prof_begin(c);
-  for (int64_t b = 0; b < nbatch; ++b) {
-    const int64_t t0 = b * (int64_t)B;
-    const int rows = (int)std::min<int64_t>(B, nt - t0);
-if (int rc = launch_eval_batch(c, c->stream, c->src, cscale, t0, rows, ev_rows, ev_cols, ev_staged, Kb, skp))
-      return rc;
-    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, rr, m, &one, Kb, rows, d_W, m, &zero, KW, rows) !=
-        CUBLAS_STATUS_SUCCESS)
-      return fail(c, KID_E_CUDA, "cublasDgemm failed");
-    c->launches++;
-    k_rowsq<<<(unsigned)std::min<int64_t>((rows + 255) / 256, (int64_t)c->sms * 8), 256, 0, c->stream>>>(KW, rows, rr,
-                                                                                                      d_scores + t0);
-    KID_LAUNCHED(c);
-  }
-  prof_end(c);
-  return KID_OK;
+  const int64_t m = c->m;
+  std::vector<double> Wh((size_t)m * r);
+  KID_CK(c, cudaMemcpyAsync(Wh.data(), d_W, sizeof(double) * Wh.size(), cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  return fused_dev(c, h, FX_LEV, Wh.data(), r, d_scores);
 }
 
 int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_scores) {
@@ -703,7 +619,7 @@ int leverage_dev(kid_ctx* c, double h, const double* d_W, int64_t r, double* d_s
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   const int m = (int)c->m, d = c->d, rr = (int)r;
   const size_t smem = proj_smem_bytes(m, rr, d);
-  if (ceil_to(rr, 8) > 128 || smem > 200 * 1024 || getenv("KID_FORCE_LARGE"))
+  if (ceil_to(rr, 8) > 128 || smem > 200 * 1024 || c->path == KID_PATH_CLUSTER)
     return leverage_dev_large(c, h, d_W, r, d_scores);
   // the projected-Gram kernel in leverage mode: K tile by exp, K W on DMMA, row sums of squares
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;

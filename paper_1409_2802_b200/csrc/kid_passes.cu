@@ -20,8 +20,6 @@
 #include <cstring>
 #include <vector>
 
-#include <cublas_v2.h>
-
 #include "kid_device.cuh"
 
 namespace kid {
@@ -85,9 +83,7 @@ struct GramArgs {
   double* partial;     // [nchunks][LG][LG]
   int LG;              // padded Gram leading dimension = ceil8(meff)
   double* partial_sk;  // [nchunks] sum K^2 (part 0), then [nparts][nchunks] partial traces of D^T D
-  int dbg;             // profiling aid (KID_GRAM_DEBUG): 1 skip eval math, 2 skip the K_S P2 FMAs, 4 skip SYRK,
-                       // 16 no coordinate copies (ring slots keep tile 0's targets)
-  long long* trace;    // profiling aid (KID_GRAM_TRACE): [warp][tile][4] clock64 stamps of CTA 0
+  long long* trace;    // profiling build only (KID_GRAM_TRACE_BUILD): [warp][tile][4] clock64 stamps of CTA 0
   // scaled source coordinates in the kernel-parameter (constant) bank: the eval warps read them
   // at warp-uniform indices, so they cost constant-cache broadcasts instead of shared-memory
   // wavefronts. [d][rS] skeleton columns, then [d][mN] non-skeleton columns (padding: far away)
@@ -217,7 +213,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArg
     const short* itA = el + 2;
     const short* itB = el + 2 + nA;
     double sk = 0.0;
-    const bool copier = ew < d && !(A.dbg & 16);  // warp ew copies coordinate dims ew, ew + kEW, ...
+    const bool copier = ew < d;  // warp ew copies coordinate dims ew, ew + kEW, ...
     const int64_t nt = A.tv.nt;
     auto trow = [&](int tl) -> int64_t {  // target row of lane in local tile tl, -1 past the end
       const int64_t i = (tile_lo + tl) * kTM + lane;
@@ -261,7 +257,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArg
     };
     // A items: K_S columns of local tile tl into KS slot (tl & 1); two columns per pass
     auto eval_A = [&](int tl) {
-      if (tl >= ntile || nA == 0 || (A.dbg & 1)) return;
+      if (tl >= ntile || nA == 0) return;
       load_coords(tl);
       const bool valid = trow(tl) >= 0;
       double* KS = KSb + (size_t)(tl & 1) * TS;
@@ -303,7 +299,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArg
       if (it >= kStages) nbar_sync(kBarEmpty + s, kGT);  // the MMA warps released stage s
       KID_TRACE(1);
       eval_A(it + 1);
-      if (!(A.dbg & 1) && nB > 0) {
+      if (nB > 0) {
         load_coords(it);
         const bool valid = trow(it) >= 0;
         const double* KS = KSb + (size_t)(it & 1) * TS;
@@ -337,7 +333,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArg
           }
           // ... then D = K_N - K_S P2 on DMMA over the block's four 8-target row blocks:
           // C(rb) = K_N fragment, C += K_S(rb, k-step) x (-P2)(k-step, block), back to KN
-          if (r > 0 && !(A.dbg & 2)) {
+          if (r > 0) {
             __syncwarp();
             double c[4][2];
 #pragma unroll
@@ -405,7 +401,7 @@ __global__ void __launch_bounds__(kGT, 1) k_gram(const __grid_constant__ GramArg
       // unpredicated DMMAs: a per-DMMA predicate makes ptxas wrap every DMMA in a warp-sync and
       // branch (tools/syrk_probe.cu); the tile count is instead dispatched once per stage
       const double* col = KNb + (size_t)s * TN + fr * kST + fk;
-      if (!(A.dbg & 4)) {
+      {
         if (ntl == TPW) syrk_stage<TPW, TPW, WA>(acc, fa0, fb0, col);
         else if constexpr (TPW > 1) {
           if (ntl == TPW - 1) syrk_stage<TPW - 1, TPW, WA>(acc, fa0, fb0, col);
@@ -612,266 +608,6 @@ int row_norms_dev(kid_ctx* c, double h, double* d_w) {
   return KID_OK;
 }
 
-// Gram of T = K (r == 0) or T = K_N - K_S P2 (r > 0, operands from kid_recon_prepare).
-// d_out = [sumsq_T, sumsq_K, G (meff x meff)].
-// ------------------------------------------------------------------ large-m path
-// For m - r > 128 (BASELINE c4 m=256, c5 m=512) the fused kernel's shared-memory stages do not
-// fit; this path evaluates a batch of B target rows of K (columns [skel | non-skel]) into a
-// transient column-major HBM buffer with the same arithmetic, then D = K_N - K_S P2 is one DGEMM
-// and G += D^T D one DSYRK (cuBLAS, DMMA). ROUND-1 FALLBACK: it materialises K batch-wise,
-// which the fused kernel avoids; DESIGN.md section 8 plans its replacement.
-// One thread per target row (coordinates in registers, pre-scaled by 1/(sqrt2 h)), a block of
-// 256 rows x a contiguous range of the m4/4 four-column groups (blockIdx.y); sources staged in
-// shared memory [k][j] (scaled, padding far away -> exactly 0), four exp chains per step; the
-// column-major stores Kb[i + j*B] are coalesced across the warp. ||K||_F^2 partial per block.
-template <int D>
-__global__ void __launch_bounds__(256) k_eval_batch(TargetView tv, int d_rt, const double* __restrict__ src, int m,
-                                                    double cscale, int64_t t0, int B, double* __restrict__ Kb,
-                                                    double* __restrict__ sk_part, bool staged) {
-  const int d = D ? D : d_rt;
-  const int m4 = ceil_to(m, 4);
-  extern __shared__ __align__(16) double sm_eb[];  // d x m4 scaled sources (when staged)
-  __shared__ double s_tab[kExpTabWords];
-  __shared__ double red[8];
-  stage_exp_table(s_tab, threadIdx.x, blockDim.x);
-  if (staged)
-    for (int e = threadIdx.x; e < d * m4; e += blockDim.x) {
-      const int k = e / m4, j = e - k * m4;
-      sm_eb[e] = j < m ? src[j + (int64_t)k * m] * cscale : 1.0e4;
-    }
-  __syncthreads();
-  const double* tabl = s_tab + (threadIdx.x & 31);
-  const int ng = m4 / 4;
-  const int g_lo = (int)((int64_t)ng * blockIdx.y / gridDim.y), g_hi = (int)((int64_t)ng * (blockIdx.y + 1) / gridDim.y);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  double sk = 0.0;
-  if (i < B) {
-    const bool live = t0 + i < tv.nt;
-    constexpr int DR = D ? D : 1;
-    double t[DR];
-    if constexpr (D > 0) {
-#pragma unroll
-      for (int k = 0; k < D; ++k) t[k] = live ? tcoord(tv, t0 + i, k) * cscale : 0.0;
-    }
-    for (int g = g_lo; g < g_hi; ++g) {
-      const int j = 4 * g;
-      double kv[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int k = 0; k < d; ++k) {
-        const double tk = D ? t[D ? k : 0] : (live ? tcoord(tv, t0 + i, k) * cscale : 0.0);
-        double x[4];
-        if (staged) {
-          const double* xk = sm_eb + (size_t)k * m4 + j;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) x[u] = xk[u];
-        } else {  // m * d too large for shared memory: warp-uniform L1 broadcasts
-#pragma unroll
-          for (int u = 0; u < 4; ++u) x[u] = j + u < m ? __ldg(src + j + u + (int64_t)k * m) * cscale : 1.0e4;
-        }
-        const double a0 = tk - x[0], a1 = tk - x[1], a2 = tk - x[2], a3 = tk - x[3];
-        kv[0] = fma(a0, a0, kv[0]);
-        kv[1] = fma(a1, a1, kv[1]);
-        kv[2] = fma(a2, a2, kv[2]);
-        kv[3] = fma(a3, a3, kv[3]);
-      }
-      exp_neg_fast_n<4>(kv, tabl);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double v = live ? kv[u] : 0.0;
-        if (j + u < m) {
-          Kb[i + (int64_t)(j + u) * B] = v;
-          sk = fma(v, v, sk);
-        }
-      }
-    }
-  }
-  sk = warp_sum(sk);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sk;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tt = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tt += red[w];
-    sk_part[blockIdx.y * gridDim.x + blockIdx.x] = tt;
-  }
-}
-
-// out = [tr(G), sum_K2, G] with G symmetrised from the upper triangle. Block 0 also folds the
-// ||K||^2 partials: lane-strided sums, then a fixed shuffle / warp order (deterministic).
-__global__ void __launch_bounds__(256) k_large_finish(double* __restrict__ G, int n, const double* __restrict__ sk_part,
-                                                      int nsk, double* __restrict__ out) {
-  const int64_t total = (int64_t)n * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(e % n), y = (int)(e / n);
-    out[2 + e] = x <= y ? G[x + (int64_t)y * n] : G[y + (int64_t)x * n];
-  }
-  if (blockIdx.x == 0) {
-    __shared__ double red[8];
-    double sk = 0.0;
-    for (int b = threadIdx.x; b < nsk; b += blockDim.x) sk += sk_part[b];
-    sk = warp_sum(sk);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sk;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tr = 0.0, t = 0.0;
-      for (int x = 0; x < n; ++x) tr += G[x + (int64_t)x * n];
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-      out[0] = tr;
-      out[1] = t;
-    }
-  }
-}
-
-// G (n x n, full) = D^T D (+ G when accumulate) for a tall D (rows x n, col-major, ld): cuBLAS'
-// SYRK parallelises over output tiles only, which for n << rows leaves most SMs idle (one 3.5 ms
-// call per 262k x 47 batch at c5); here the rows are split into nch chunks, one strided-batched
-// DGEMM computes the per-chunk D_c^T D_c, and a fixed-order sum folds them (bitwise reproducible):
-// 32 elements x 8 part groups per block, groups combined in order.
-__global__ void __launch_bounds__(256) k_sum_partials(const double* __restrict__ part, int nparts, int64_t len,
-                                                      double* __restrict__ G, bool accumulate, int rows_c, int ldG) {
-  __shared__ double red[8][33];
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  for (int64_t base = (int64_t)blockIdx.x * 32; base < len; base += (int64_t)gridDim.x * 32) {
-    const int64_t e = base + lane;
-    double s = 0.0;
-    if (e < len)
-      for (int p = g; p < nparts; p += 8) s += part[(size_t)p * len + e];
-    red[g][lane] = s;
-    __syncthreads();
-    if (g == 0 && e < len) {
-      double t = 0.0;
-      for (int q = 0; q < 8; ++q) t += red[q][lane];
-      const int64_t ge = e % rows_c + (e / rows_c) * ldG;  // (rows_c x ...) block of G, leading dim ldG
-      G[ge] = (accumulate ? G[ge] : 0.0) + t;
-    }
-    __syncthreads();
-  }
-}
-
-// P2 row-major (r x SP) -> column-major (r x meff) for the DGEMM
-__global__ void k_p2_colmajor(const double* __restrict__ P2, int r, int SP, int meff, double* __restrict__ out) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)r * meff;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(e % r), nn = (int)(e / r);
-    out[e] = P2[(size_t)k * SP + nn];
-  }
-}
-
-int tall_syrk(kid_ctx* c, const double* D, int rows, int ld, int n, double* G, bool accumulate, double* part,
-              int max_parts) {
-  const double one = 1.0, zero = 0.0;
-  const int nch = std::max(1, std::min(max_parts - 1, rows / 2048));
-  const int chunk = rows / nch, rem = rows - nch * chunk;
-  // n > 128: only the upper block triangle of 128-column blocks (the full Gram by GEMM would
-  // double the flops: 10 of 16 block pairs at n = 512, 3 of 4 at n = 256)
-  const int bs = n > 128 ? 128 : n;
-  for (int i0 = 0; i0 < n; i0 += bs)
-    for (int j0 = i0; j0 < n; j0 += bs) {
-      const int ni = std::min(bs, n - i0), nj = std::min(bs, n - j0);
-      const int64_t nn = (int64_t)ni * nj;
-      const double* Di = D + (size_t)i0 * ld;
-      const double* Dj = D + (size_t)j0 * ld;
-      if (chunk > 0 &&
-          cublasDgemmStridedBatched(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ni, nj, chunk, &one, Di, ld, chunk, Dj, ld, chunk,
-                                    &zero, part, ni, nn, nch) != CUBLAS_STATUS_SUCCESS)
-        return fail(c, KID_E_CUDA, "cublasDgemmStridedBatched failed");
-      c->launches++;
-      if (rem > 0) {
-        if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ni, nj, rem, &one, Di + (size_t)nch * chunk, ld,
-                        Dj + (size_t)nch * chunk, ld, &zero, part + nch * nn, ni) != CUBLAS_STATUS_SUCCESS)
-          return fail(c, KID_E_CUDA, "cublasDgemm failed");
-        c->launches++;
-      }
-      k_sum_partials<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nn + 31) / 32, c->sms * 8)), 256, 0,
-                       c->stream>>>(part, nch + (rem > 0 ? 1 : 0), nn, G + i0 + (size_t)j0 * n, accumulate, ni, n);
-      KID_LAUNCHED(c);
-    }
-  return KID_OK;
-}
-
-int gram_dev_large(kid_ctx* c, double h, int64_t r, double* d_out) {
-  const int m = (int)c->m, d = c->d, meff = (int)(m - r);
-  if (!c->blas) {
-    if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return fail(c, KID_E_CUDA, "cublasCreate failed");
-  }
-  if (!c->aux_stream) {
-    KID_CK(c, cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
-    for (int i = 0; i < 5; ++i) KID_CK(c, cudaEventCreateWithFlags(&c->aux_ev[i], cudaEventDisableTiming));
-  }
-  cublasSetStream(c->blas, c->stream);
-  cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
-  const int64_t nt = c->nt;
-  // batches of B target rows through two 1 GB K buffers: the eval of batch b + 1 (aux stream, FP64
-  // exp) overlaps the DGEMM / Gram of batch b (launching stream, DMMA)
-  const int B = (int)std::max<int64_t>(1024, std::min<int64_t>(nt, (int64_t)(1ll << 30) / (8ll * m)));
-  const int64_t nbatch = (nt + B - 1) / B;
-  const int ev_rows = (B + 255) / 256;
-  const int ev_cols = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_to(m, 4) / 4, (4ll * c->sms + ev_rows - 1) / ev_rows));
-  const int ev_blocks = ev_rows * ev_cols;
-  const bool ev_staged = sizeof(double) * (size_t)d * ceil_to(m, 4) <= 160 * 1024;
-  const size_t ev_smem = ev_staged ? sizeof(double) * (size_t)d * ceil_to(m, 4) : 0;
-  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
-  // scratch: 2 K batches (B x m) | G (meff x meff) | P2 col-major (r x meff) | sk partials | Gram parts
-  const size_t kb = (size_t)B * m, gb = (size_t)meff * meff, pb = (size_t)std::max<int64_t>(r, 1) * meff;
-  char* base = (char*)scratch(c, sizeof(double) * (2 * kb + gb + pb + (size_t)nbatch * ev_blocks + (size_t)kSyrkParts * gb + 64));
-  if (!base) return KID_E_OOM;
-  double* Kbuf[2] = {(double*)base, (double*)base + kb};
-  double* G = Kbuf[1] + kb;
-  double* P2c = G + gb;
-  double* skp = P2c + pb;
-  double* gpart = skp + (size_t)nbatch * ev_blocks;
-  if (r > 0) {
-    k_p2_colmajor<<<(unsigned)std::min<int64_t>(((int64_t)r * meff + 255) / 256, 1024), 256, 0, c->stream>>>(
-        c->P2, (int)r, frag_stride(meff), meff, P2c);
-    KID_LAUNCHED(c);
-  }
-  const double* src = r > 0 ? c->src_perm : c->src;
-  const double cscale = std::sqrt(1.0 / (2.0 * h * h));
-  const double one = 1.0, mone = -1.0;
-  cudaEvent_t ev_start = c->aux_ev[0], ev_eval[2] = {c->aux_ev[1], c->aux_ev[2]}, ev_free[2] = {c->aux_ev[3], c->aux_ev[4]};
-  prof_begin(c);
-  KID_CK(c, cudaEventRecord(ev_start, c->stream));
-  KID_CK(c, cudaStreamWaitEvent(c->aux_stream, ev_start, 0));
-  auto eval = [&](int64_t b) -> int {
-    const int64_t t0 = b * (int64_t)B;
-    const int rows = (int)std::min<int64_t>(B, nt - t0);
-    if (b >= 2) KID_CK(c, cudaStreamWaitEvent(c->aux_stream, ev_free[b & 1], 0));
-#define LAUNCH(DD)                                                                                         \
-  {                                                                                                        \
-    cudaFuncSetAttribute(k_eval_batch<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ev_smem);      \
-    k_eval_batch<DD><<<dim3(ev_rows, ev_cols), 256, ev_smem, c->aux_stream>>>(view(c), d, src, m, cscale, t0, rows, \
-                                                                             Kbuf[b & 1], skp + b * ev_blocks, ev_staged); \
-  }
-    KID_DISPATCH_D(d, LAUNCH)
-#undef LAUNCH
-    KID_LAUNCHED(c);
-    KID_CK(c, cudaEventRecord(ev_eval[b & 1], c->aux_stream));
-    return KID_OK;
-  };
-  if (nbatch > 0)
-    if (int rc = eval(0)) return rc;
-  for (int64_t b = 0; b < nbatch; ++b) {
-    if (b + 1 < nbatch)
-      if (int rc = eval(b + 1)) return rc;
-    const int64_t t0 = b * (int64_t)B;
-    const int rows = (int)std::min<int64_t>(B, nt - t0);
-    double* Kb = Kbuf[b & 1];
-    KID_CK(c, cudaStreamWaitEvent(c->stream, ev_eval[b & 1], 0));
-    double* KN = Kb + (size_t)r * rows;  // non-skeleton columns follow the r skeleton columns
-    if (r > 0) {
-      if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, meff, (int)r, &mone, Kb, rows, P2c, (int)r, &one, KN,
-                      rows) != CUBLAS_STATUS_SUCCESS)
-        return fail(c, KID_E_CUDA, "cublasDgemm failed");
-      c->launches++;
-    }
-    if (int rc = tall_syrk(c, KN, rows, rows, meff, G, b > 0, gpart, kSyrkParts)) return rc;
-    KID_CK(c, cudaEventRecord(ev_free[b & 1], c->stream));
-  }
-  prof_end(c);
-  k_large_finish<<<std::max(1, std::min(c->sms * 4, (meff * meff + 255) / 256)), 256, 0, c->stream>>>(
-      G, meff, skp, (int)(nbatch * ev_blocks), d_out);
-  KID_LAUNCHED(c);
-  return KID_OK;
-}
-
 // ||K||_F^2 alone (the full-rank skeleton of the residual pass: D == 0): one thread per target,
 // four exp chains, per-block partials folded in a fixed order. d_out = [0, ||K||_F^2].
 template <int D>
@@ -885,7 +621,7 @@ __global__ void __launch_bounds__(256) k_sumsq(TargetView tv, int d_rt, const do
   stage_exp_table(s_tab, threadIdx.x, blockDim.x);
   for (int e = threadIdx.x; e < d * m4; e += blockDim.x) {
     const int k = e / m4, j = e - k * m4;
-    sm_sq[e] = j < m ? src[j + (int64_t)k * m] * cscale : 1.0e4;
+    sm_sq[e] = j < m ? src[j + (int64_t)k * m] * cscale : 1.0e150;
   }
   __syncthreads();
   const double* tabl = s_tab + (threadIdx.x & 31);
@@ -957,8 +693,7 @@ int sumsq_dev(kid_ctx* c, double h, double* d_out) {
   return KID_OK;
 }
 
-int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
-  (void)flags;
+int gram_dev(kid_ctx* c, double h, int64_t r, double* d_out) {
   if (int rc = check_block(c, h)) return rc;
   const int m = (int)c->m, d = c->d;
   const int meff = (int)(m - r);
@@ -1028,7 +763,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
       else la[best].push_back((short)(-itx.second - 1));
     }
     for (int w = 0; w < kEW; ++w) {
-      if (2 + la[w].size() + lb[w].size() > (size_t)kEItems) return gram_dev_large(c, h, r, d_out);
+      if (2 + la[w].size() + lb[w].size() > (size_t)kEItems) return fused_dev(c, h, r > 0 ? FX_RESID : FX_GRAM, nullptr, 0, d_out);
       std::sort(la[w].begin(), la[w].end());
       std::sort(lb[w].begin(), lb[w].end());
       short* e = &elist[(size_t)w * kEItems];
@@ -1043,8 +778,8 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   const int TS = (r4 > 0 ? r4 : 4) * kST, TN = ceil_to(NBN + 1, 2) * 8 * kST;
   const size_t smem = sizeof(double) * ((size_t)r4 * frag_stride(meff) + 2 * (size_t)TS + (size_t)kStages * TN +
                                         (size_t)kRing * d * kTM);
-  if ((size_t)d * (rS + mN) > (size_t)kCSrc) return gram_dev_large(c, h, r, d_out);
-  if (smem > 190 * 1024 || NBN > 16 || getenv("KID_FORCE_LARGE")) return gram_dev_large(c, h, r, d_out);
+  if ((size_t)d * (rS + mN) > (size_t)kCSrc || smem > 190 * 1024 || NBN > 16 || c->path == KID_PATH_CLUSTER)
+    return fused_dev(c, h, r > 0 ? FX_RESID : FX_GRAM, nullptr, 0, d_out);
   const int64_t ntiles = (c->nt + kTM - 1) / kTM;
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
   int per_sm = 1;
@@ -1084,9 +819,9 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
     if (sh.size() != (size_t)m * d) return fail(c, KID_E_ERROR, "gram: host copy of the sources is stale");
     const double cs = std::sqrt(1.0 / (2.0 * h * h));
     for (int k = 0; k < d; ++k) {
-      for (int j = 0; j < rS; ++j) A.csrc[k * rS + j] = j < rr ? sh[(size_t)k * m + j] * cs : 1.0e4;
+      for (int j = 0; j < rS; ++j) A.csrc[k * rS + j] = j < rr ? sh[(size_t)k * m + j] * cs : 1.0e150;
       for (int j = 0; j < mN; ++j)
-        A.csrc[d * rS + k * mN + j] = j < meff ? sh[(size_t)k * m + rr + j] * cs : 1.0e4;  // far away: K == 0
+        A.csrc[d * rS + k * mN + j] = j < meff ? sh[(size_t)k * m + rr + j] * cs : 1.0e150;  // far away: K == 0
     }
   }
   A.m = m;
@@ -1102,9 +837,12 @@ int gram_dev(kid_ctx* c, double h, int64_t r, uint32_t flags, double* d_out) {
   A.partial = partial;
   A.LG = LG;
   A.partial_sk = partial_sk;
-  A.dbg = getenv("KID_GRAM_DEBUG") ? atoi(getenv("KID_GRAM_DEBUG")) : 0;
   A.trace = nullptr;
-  const bool tracing = getenv("KID_GRAM_TRACE") != nullptr;
+#ifdef KID_GRAM_TRACE_BUILD  // profiling build only (tools/gram_probe.py): per-phase clock64 stamps of CTA 0
+  const bool tracing = true;
+#else
+  const bool tracing = false;
+#endif
   const size_t trace_n = (size_t)(kMW + kEW) * kTraceTiles * 4;
   if (tracing) {
     KID_CK(c, cudaMalloc(&A.trace, sizeof(long long) * trace_n));
@@ -1201,7 +939,7 @@ int apply_skeleton_dev(kid_ctx* c, double h, const int64_t* skel, int64_t r, con
   const double cs = std::sqrt(1.0 / (2.0 * h * h));
   std::vector<double> hx((size_t)d * r4 + r4);
   for (int k = 0; k < d; ++k)
-    for (int j = 0; j < r4; ++j) hx[(size_t)k * r4 + j] = j < r ? c->src_host[(size_t)k * m + skel[j]] * cs : 1.0e4;
+    for (int j = 0; j < r4; ++j) hx[(size_t)k * r4 + j] = j < r ? c->src_host[(size_t)k * m + skel[j]] * cs : 1.0e150;
   for (int j = 0; j < r4; ++j) hx[(size_t)d * r4 + j] = j < r ? q_skel[j] : 0.0;
   const size_t bytes = sizeof(double) * hx.size();
   if (bytes > 160 * 1024) return fail(c, KID_E_DIM, "apply_skeleton: skeleton too large for shared memory");
@@ -1265,29 +1003,6 @@ int launch_gram_reduce(kid_ctx* c, const double* partial, int nchunks, int LG, i
                        int nparts, double* out) {
   k_gram_reduce<<<std::max(1, std::min(c->sms * 2, (n * n + 31) / 32)), 1024, 0, c->stream>>>(partial, nchunks, LG, n,
                                                                                             partial_sk, nparts, out);
-  KID_LAUNCHED(c);
-  return KID_OK;
-}
-
-int launch_eval_batch(kid_ctx* c, cudaStream_t st, const double* src, double cscale, int64_t t0, int rows, int ev_rows,
-                      int ev_cols, bool staged, double* Kb, double* skp) {
-  if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
-  const int d = c->d, m = (int)c->m;
-  const size_t ev_smem = staged ? sizeof(double) * (size_t)d * ceil_to(m, 4) : 0;
-#define LAUNCH(DD)                                                                                          \
-  {                                                                                                         \
-    cudaFuncSetAttribute(k_eval_batch<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ev_smem);       \
-    k_eval_batch<DD><<<dim3(ev_rows, ev_cols), 256, ev_smem, st>>>(view(c), d, src, m, cscale, t0, rows, Kb, skp, \
-                                                                   staged);                                 \
-  }
-  KID_DISPATCH_D(d, LAUNCH)
-#undef LAUNCH
-  KID_LAUNCHED(c);
-  return KID_OK;
-}
-
-int launch_large_finish(kid_ctx* c, double* G, int n, const double* skp, int nsk, double* out) {
-  k_large_finish<<<std::max(1, std::min(c->sms * 4, (n * n + 255) / 256)), 256, 0, c->stream>>>(G, n, skp, nsk, out);
   KID_LAUNCHED(c);
   return KID_OK;
 }

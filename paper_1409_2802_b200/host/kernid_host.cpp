@@ -162,11 +162,7 @@ Matrix KernelBlock::gram(double* sumsq) const {
   return G;
 }
 
-double KernelBlock::spectral_norm() const {
-  std::vector<double> ev;
-  sym_eig(gram(), ev, nullptr);
-  return ev.empty() ? 0.0 : std::sqrt(std::max(ev[0], 0.0));
-}
+double KernelBlock::spectral_norm() const { return std::sqrt(lambda_max(gram())); }
 
 // ------------------------------------------------------------------ lowrank (host)
 namespace {
@@ -629,6 +625,66 @@ std::vector<double> sym_eigvals(const Matrix& A) {
   return d;
 }
 
+// Largest eigenvalue of a symmetric PSD matrix (the spectral norms sqrt(lambda_max(D^T D)) and
+// sqrt(lambda_max(K^T K)) of compress_id). n <= 128: all eigenvalues by Jacobi. Larger n (c4 / c5:
+// m = 256 / 512): Lanczos from the constant vector with full reorthogonalisation, stopped when the
+// Ritz residual |beta_k s_k| of the top Ritz pair is below 1e-14 of it (|theta - lambda| <= residual),
+// or at k = n (exact); the k x k tridiagonal is solved by Jacobi. ~n^2 flops per step instead of the
+// O(n^3) of a full tridiagonalisation.
+double lambda_max(const Matrix& G) {
+  const int64_t n = G.rows;
+  if (n == 0) return 0.0;
+  if (n <= 128) {
+    std::vector<double> ev;
+    sym_eig(G, ev, nullptr);
+    return ev.empty() ? 0.0 : std::max(ev[0], 0.0);
+  }
+  const size_t N = static_cast<size_t>(n);
+  std::vector<std::vector<double>> Q;
+  std::vector<double> alpha, beta;
+  std::vector<double> v(N, 1.0 / std::sqrt(static_cast<double>(n))), w(N);
+  double theta = 0.0;
+  for (int64_t k = 0; k < n; ++k) {
+    Q.push_back(v);
+    for (size_t i = 0; i < N; ++i) {  // w = G v (column-major, symmetric)
+      double acc = 0.0;
+      const double* gi = G.data() + i * N;
+      for (size_t j = 0; j < N; ++j) acc += gi[j] * v[j];
+      w[i] = acc;
+    }
+    double a = 0.0;
+    for (size_t i = 0; i < N; ++i) a += v[i] * w[i];
+    alpha.push_back(a);
+    for (int pass = 0; pass < 2; ++pass)  // full reorthogonalisation, twice
+      for (const auto& q : Q) {
+        double c = 0.0;
+        for (size_t i = 0; i < N; ++i) c += q[i] * w[i];
+        for (size_t i = 0; i < N; ++i) w[i] -= c * q[i];
+      }
+    double b = 0.0;
+    for (size_t i = 0; i < N; ++i) b += w[i] * w[i];
+    b = std::sqrt(b);
+    const int64_t kk = k + 1;
+    const bool last = kk == n || b <= 1e-300;
+    if (last || kk % 8 == 0) {
+      Matrix T(kk, kk);
+      for (int64_t i = 0; i < kk; ++i) {
+        T(i, i) = alpha[static_cast<size_t>(i)];
+        if (i + 1 < kk) T(i, i + 1) = T(i + 1, i) = beta[static_cast<size_t>(i)];
+      }
+      std::vector<double> ev;
+      Matrix V;
+      sym_eig(T, ev, &V);
+      theta = ev[0];
+      const double res = std::abs(b * V(kk - 1, 0));
+      if (last || res <= 1e-14 * std::abs(theta)) return std::max(theta, 0.0);
+    }
+    beta.push_back(b);
+    for (size_t i = 0; i < N; ++i) v[i] = w[i] / b;
+  }
+  return std::max(theta, 0.0);
+}
+
 LeverageScores row_leverage_scores(const KernelBlock& K, int64_t r) {
   const int64_t mn = std::min(K.rows(), K.cols());
   if (r < 1 || r > mn) throw RangeError("row_leverage_scores: requires 1 <= r <= min(m, n)");
@@ -854,6 +910,22 @@ double now_ms() {
 }
 }  // namespace
 
+// D^T D is zero on the skeleton rows / columns (P[:, skel] = I): its spectrum is that of the
+// (m - r) x (m - r) non-skeleton block.
+static Matrix nonskeleton_block(const Matrix& DtD, const std::vector<int64_t>& skel) {
+  const int64_t m = DtD.rows;
+  std::vector<char> in(static_cast<size_t>(m), 0);
+  for (int64_t j : skel) in[static_cast<size_t>(j)] = 1;
+  std::vector<int64_t> b;
+  for (int64_t i = 0; i < m; ++i)
+    if (!in[static_cast<size_t>(i)]) b.push_back(i);
+  const int64_t n = static_cast<int64_t>(b.size());
+  Matrix S(n, n);
+  for (int64_t y = 0; y < n; ++y)
+    for (int64_t x = 0; x < n; ++x) S(x, y) = DtD(b[static_cast<size_t>(x)], b[static_cast<size_t>(y)]);
+  return S;
+}
+
 // compress.hpp:168-215 with the error pass on the device.
 std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, const RowSample& sample,
                                                           const RankRule& rule, const CompressOptions& opts) {
@@ -886,9 +958,7 @@ std::pair<IDFactorization, CompressionReport> compress_id(const KernelBlock& K, 
     double sd = 0.0, sk = 0.0;
     K.device().check(kid_recon_error(K.device().ctx(), K.spec().h, id.skeleton.data(), r, id.projection.data(),
                                      KID_RECON_DTD, &sd, &sk, DtD.data(), nullptr));
-    std::vector<double> ev;
-    sym_eig(DtD, ev, nullptr);
-    const double num = std::sqrt(std::max(ev.empty() ? 0.0 : ev[0], 0.0));
+    const double num = std::sqrt(lambda_max(nonskeleton_block(DtD, id.skeleton)));
     const double den = opts.k_norm ? *opts.k_norm : K.spectral_norm();
     rep.rel_error = (den > 0.0) ? num / den : 0.0;
     rep.rel_error_fro = (sk > 0.0) ? std::sqrt(sd / sk) : 0.0;
@@ -1320,16 +1390,6 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
 }
 
 // ------------------------------------------------------------------ interaction fractions
-namespace {
-// largest eigenvalue of a symmetric PSD matrix
-double lambda_max(const Matrix& G) {
-  std::vector<double> ev;
-  if (G.rows <= 128) sym_eig(G, ev, nullptr);  // Jacobi
-  else ev = sym_eigvals(G);                     // tridiagonal + QL
-  return ev.empty() ? 0.0 : std::max(ev[0], 0.0);
-}
-}  // namespace
-
 InteractionFractions interaction_fractions(Device& dev, const PointSet& ps, const KernelSpec& spec,
                                            const std::vector<double>& x_c, int64_t n) {
   spec.validate();
@@ -1580,6 +1640,37 @@ int kidh_kernel_rows(const double* pts, int64_t N, int32_t d, const int64_t* tgt
     for (int64_t i = 0; i < count; ++i)
       for (int64_t j = 0; j < m; ++j)
         out[i + j * count] = eval_kernel(spec, pts + tgt_idx[rows[i]], N, pts + src_idx[j], N, d);
+  });
+}
+
+// The error pass of compress_id (compress.hpp:178-206) on a caller-owned kid_ctx holding the block
+// K(T, S): num = sqrt(lambda_max(D^T D)) from kid_recon_error, den = ||K||_2 = sqrt(lambda_max(K^T K))
+// from kid_gram unless k_norm > 0 is given (harness.hpp:237 caches it per trial). Host buffers in
+// and out: the end-to-end path of bench.py.
+int kidh_error_pass(void* ctx, double h, const int64_t* skel, int64_t r, const double* P, double k_norm,
+                    double* rel_error, double* rel_error_fro, double* k_norm_out) {
+  return guard([&] {
+    kid_ctx* c = static_cast<kid_ctx*>(ctx);
+    auto ck = [&](int rc) {
+      if (rc != KID_OK) throw Error(std::string("kid: ") + kid_last_error(c));
+    };
+    int64_t nt = 0, m = 0;
+    int32_t d = 0;
+    ck(kid_block_shape(c, &nt, &m, &d));
+    Matrix DtD(m, m);
+    double sd = 0.0, sk = 0.0;
+    ck(kid_recon_error(c, h, skel, r, P, KID_RECON_DTD, &sd, &sk, DtD.data(), nullptr));
+    const std::vector<int64_t> sv(skel, skel + r);
+    const double num = std::sqrt(lambda_max(nonskeleton_block(DtD, sv)));
+    double den = k_norm;
+    if (!(den > 0.0)) {
+      Matrix G(m, m);
+      ck(kid_gram(c, h, G.data(), nullptr));
+      den = std::sqrt(lambda_max(G));
+    }
+    *rel_error = den > 0.0 ? num / den : 0.0;
+    *rel_error_fro = sk > 0.0 ? std::sqrt(sd / sk) : 0.0;
+    if (k_norm_out) *k_norm_out = den;
   });
 }
 

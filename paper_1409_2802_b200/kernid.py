@@ -44,6 +44,7 @@ def host_lib():
         L.kidh_sym_eigvals.argtypes = [_dp, i64, _dp]
         L.kidh_draw.argtypes = [i32, i32, i64, C.c_void_p, dbl, u64, _ip, P(i64)]
         L.kidh_kernel_rows.argtypes = [_dp, i64, i32, _ip, _ip, i64, _ip, i64, dbl, _dp]
+        L.kidh_error_pass.argtypes = [C.c_void_p, dbl, _ip, i64, _dp, dbl, P(dbl), P(dbl), P(dbl)]
         L.kidh_trial_next_rows.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, dbl, i32, u64, _dp,
                                            P(i64), P(i64), _ip, _dp, _dp, _dp, i64]
         L.kidh_compress_trial.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, i32, i64, dbl, u64, dbl, P(i64), P(i64),
@@ -148,6 +149,17 @@ def kernel_rows(points_colmajor: np.ndarray, N: int, d: int, tgt_idx, rows, src_
     _ck(host_lib().kidh_kernel_rows(points_colmajor, N, d, tgt_idx, rows, rows.size, src_idx, src_idx.size, h, out),
         "kernel_rows")
     return _uncm(out[: rows.size * src_idx.size], rows.size, src_idx.size)
+
+
+def error_pass(dev, h: float, skel, P, k_norm: float = 0.0):
+    """compress_id's error pass (compress.hpp:178-206) through the host mirror on the block held by
+    the C-ABI Device `dev`: (rel_error, rel_error_fro, ||K||_2). k_norm > 0 skips the K^T K pass."""
+    skel = np.ascontiguousarray(skel, dtype=np.int64)
+    Pc = _cm(np.asarray(P, dtype=np.float64))
+    rel, fro, kn = C.c_double(), C.c_double(), C.c_double()
+    _ck(host_lib().kidh_error_pass(dev.h, h, skel, skel.size, Pc, k_norm, C.byref(rel), C.byref(fro), C.byref(kn)),
+        "error_pass")
+    return rel.value, fro.value, kn.value
 
 
 @dataclass

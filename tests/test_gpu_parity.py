@@ -128,9 +128,9 @@ def test_recon_error_vs_oracle(oracle, dev, d, eps, n):
 
 
 @pytest.mark.parametrize("d,n,rs", [(16, 256, (8, 64)), (8, 200, (30,))])
-def test_leverage_large(oracle, dev, monkeypatch, d, n, rs):
-    """W beyond shared memory (c4-like m = 256, d = 16): the batched path (K batch, DGEMM K W,
-    row sums of squares); the same bar as test_leverage."""
+def test_leverage_large(oracle, dev, d, n, rs):
+    """W beyond shared memory (c4-like m = 256, d = 16): the 2-CTA cluster kernel (K W on DMMA across
+    the CTA pair, row sums of squares); the same bar as test_leverage."""
     t, K = _block(oracle, d=d, N=30_000, n=n)
     dev.set_points(t.points)
     dev.split(t.center, n, 2.0)
@@ -140,14 +140,17 @@ def test_leverage_large(oracle, dev, monkeypatch, d, n, rs):
         ref, _ = oracle.row_leverage_scores(K, r)
         got = dev.leverage(t.h, W)
         assert np.max(np.abs(got - ref)) <= 1e-10 * max(1.0, ref.max())
-    monkeypatch.setenv("KID_FORCE_LARGE", "1")  # small m through the batched path too
-    t, K = _block(oracle, d=3)
-    dev.set_points(t.points)
-    dev.split(t.center, 100, 2.0)
-    sv, V = oracle.right_factor(K)
-    W = V[:, :20] / sv[:20]
-    ref, _ = oracle.row_leverage_scores(K, 20)
-    assert np.max(np.abs(dev.leverage(t.h, W) - ref)) <= 1e-10 * max(1.0, ref.max())
+    dev.set_path(1)  # small m through the cluster kernel too
+    try:
+        t, K = _block(oracle, d=3)
+        dev.set_points(t.points)
+        dev.split(t.center, 100, 2.0)
+        sv, V = oracle.right_factor(K)
+        W = V[:, :20] / sv[:20]
+        ref, _ = oracle.row_leverage_scores(K, 20)
+        assert np.max(np.abs(dev.leverage(t.h, W) - ref)) <= 1e-10 * max(1.0, ref.max())
+    finally:
+        dev.set_path(0)
 
 
 def test_leverage(oracle, dev):
@@ -192,11 +195,10 @@ def test_fast_exp_accuracy(dev):
 
 
 @pytest.mark.parametrize("d,n,eps,force", [(16, 256, 1e-2, False), (8, 512, 1e-2, False), (3, 100, 1e-4, True)])
-def test_recon_error_large_m_path(oracle, dev, monkeypatch, d, n, eps, force):
-    """m - r > 128 runs the batched large-m path (k_eval_batch + DGEMM + DSYRK); KID_FORCE_LARGE
-    routes a small case through it too so both Gram paths are checked against the oracle."""
-    if force:
-        monkeypatch.setenv("KID_FORCE_LARGE", "1")
+def test_recon_error_large_m_path(oracle, dev, d, n, eps, force):
+    """m - r > 128 runs the 2-CTA cluster kernel (kid_fused.cu); kid_set_path routes a small case
+    through it too so both kernel families are checked against the oracle."""
+    dev.set_path(1 if force else 0)
     t, K = _block(oracle, d=d, N=12_000, n=n)
     rows = oracle.sample_rows(oracle.SCHEME_UNIFORM, K.shape[0], 0.2, 5)
     res = oracle.compress_id(K, rows, eps=eps)
@@ -213,6 +215,7 @@ def test_recon_error_large_m_path(oracle, dev, monkeypatch, d, n, eps, force):
     bound = 1e-10 * np.outer(dg, dg) + np.outer(noise, dg) + np.outer(dg, noise) + np.outer(noise, noise)
     assert np.all(np.abs(DtD - r_DtD) <= bound + 1e-300)
     G, gsk = dev.gram(t.h)
+    dev.set_path(0)
     assert _gram_ok(G, r_KtK)
 
 

@@ -57,14 +57,16 @@ def _check(O, dev, t, K, V, r, n):
 @pytest.mark.parametrize("d,n,eps", [(3, 100, 1e-2), (2, 100, 1e-8), (1, 100, 1e-14), (5, 64, 1e-4), (8, 37, 1e-2),
                                      (3, 128, 1e-2), (4, 100, 1e-2)])
 @pytest.mark.parametrize("large", [False, True])
-def test_proj_gram_svd_error_vs_oracle(oracle, dev, monkeypatch, d, n, eps, large):
-    if large:
-        monkeypatch.setenv("KID_FORCE_LARGE", "1")  # the batched (DGEMM + DSYRK) path
+def test_proj_gram_svd_error_vs_oracle(oracle, dev, d, n, eps, large):
     t, K, rows, V, r = _svd_case(oracle, d, 20_000, n, eps)
     assert 0 < r < n
     dev.set_points(t.points)
     dev.split(t.center, n, 2.0)
-    _check(oracle, dev, t, K, V, r, n)
+    dev.set_path(1 if large else 0)  # large: the 2-CTA cluster kernel (kid_fused.cu)
+    try:
+        _check(oracle, dev, t, K, V, r, n)
+    finally:
+        dev.set_path(0)
 
 
 def test_proj_gram_edges(oracle, dev):
