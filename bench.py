@@ -1,29 +1,32 @@
 #!/usr/bin/env python
 """bench.py -- headline benchmark of the B200 far-field path (arXiv 1409.2802, kernid).
 
-Metric (BASELINE.json): kernel entries/s (targets x sources) of the FP64 fused
-eval + reconstruction-error pass, and its fraction of the FP64 roofline.
+Metric (BASELINE.json): kernel entries/s (targets x sources) of the FP64 fused eval + reconstruction-
+error pass, and its fraction of the FP64 roofline.
 
-Workload (N=1): BASELINE.json configs[1] at its largest dimension -- d=3, 1e6 N(0,I_3)
-points (seed 1, trial 0), RandomPoint center, m=100 nearest sources, D_WS=2, Silverman h,
-EuclideanNorm sampling of 2% of the rows, ID to eps=1e-2 (r=17) -> one fused pass over all
-N_T ~ 1e6 targets x 100 sources = ~1e8 entries. Synthetic data (no dataset exists).
+Workload (N=1): the largest single-GPU configuration, BASELINE configs[4] (c5) -- d=8,
+N=1.0012e8 N(0,I_8) points (seed 1, trial 0: the harness seed streams), RandomPoint center, m=512
+nearest sources, D_WS=2, Silverman h; EuclideanNorm sampling of ~4000 rows, ID to eps=1e-2 -> one
+fused pass over all N_T ~ 1e8 targets x 512 sources = 5.1e10 entries. Synthetic data (no dataset exists).
+A second measurement on configs[1] (c2-d3: d=3, 1e6 points, m=100) rides along under "also".
 
   value   device-resident pass (kid_recon_error_dev on the timed stream), CUDA events,
           L2 flushed (256 MB write) between timed steps, max over ranks;
-  e2e     the same metric through the C-ABI with HOST buffers every step: points H2D
-          from pinned memory, kid_split, target indices D2H, kid_recon_error (skeleton /
-          P H2D, Grams D2H);
-  roofline  the dominant kernel (k_gram in residual mode) timed by the library's own
-          CUDA events on the launching stream (kid_profile), algorithmic FP64 flops per
-          entry / its average duration vs the measured FP64 peak;
-  cpu_baseline  the oracle restatement of the reference pipeline (threaded K assembly,
-          exact QR+SVD norms) on a bounded slice of the same targets, rank 0, N=1.
+  e2e     compress_id's error pass through the public API with HOST buffers every step: points H2D
+          from pinned memory, kid_split, then the host mirror's error pass (kernid.error_pass:
+          kid_recon_error -> lambda_max(D^T D), kid_gram -> ||K||_2 = sqrt(lambda_max(K^T K)));
+  roofline  the dominant kernel (the one the library reports it launched) timed by the library's own
+          CUDA events on the launching stream; achieved = the work it must do (strict count, DESIGN.md
+          section 5) / its average duration, against the sustained FP64 peak (tools/fp64_peaks.cu);
+  cpu_baseline  the oracle restatement of the reference pipeline (threaded K assembly, exact QR+SVD
+          norms) on a bounded slice of the same targets, rank 0, N=1; per-entry rate and the
+          extrapolated full-pass time.
 
-Multi-GPU (torchrun): weak scaling, each rank holds its own 1e6-point shard; the split
-exchanges the local top-m candidates (all_gather) and the pass all-reduces its Grams.
-`--impl reference` times the reference's CPU path (oracle port; the reference itself
-cannot be built here: no Eigen) on the same config / metric.
+Multi-GPU (torchrun, or --gpus N which re-launches itself under torch.distributed.run): the same c5
+dataset sharded by contiguous index ranges (strong scaling); sharded split (all_gather of the local
+top-m candidates), the fused pass on each shard, NCCL all_reduce of [||D||^2, ||K||^2, D^T D].
+`--impl reference` times the reference's CPU path (oracle port; the reference itself cannot be built
+here: no Eigen) on the same config / metric.
 """
 from __future__ import annotations
 
@@ -48,41 +51,50 @@ F_EXP = 32  # flops charged per exp (SURVEY.md 8d convention: CUDA 12.9 exp(doub
 
 WORKLOADS = {
     # configs[1] (quoted config of the metric): d in {1,2,3}, 1e6 targets, m=100, D_WS=2
-    "c2-d3": dict(d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-2),
-    "c2-d2": dict(d=2, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-8),
-    "c2-d3-e4": dict(d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-4),
-    "c2-d3-e6": dict(d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-6),
-    "c2-d3-e8": dict(d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-8),
-    "c1": dict(d=2, N=100_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-8),
-    "c3-d5": dict(d=5, N=1_000_000, m=100, xi=3.0, h_value=1.0, s=0.02, eps=1e-8),
-    "c4-d16": dict(d=16, N=12_000_000, m=256, xi=2.0, h_value=1.0, s=0.002, eps=1e-2),
-    "c5-d8-shard": dict(d=8, N=12_515_000, m=512, xi=2.0, h_value=1.0, s=0.002, eps=1e-2),
-    # configs[4] at N=1 GPU: the largest single-GPU configuration (1.0012e8 points, 6.4 GB)
-    "c5": dict(d=8, N=100_120_000, m=512, xi=2.0, h_value=1.0, s=4e-5, eps=1e-2),
+    "c2-d3": dict(cfg="configs[1]", d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-2),
+    "c2-d2": dict(cfg="configs[1]", d=2, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-8),
+    "c2-d3-e4": dict(cfg="configs[1]", d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-4),
+    "c2-d3-e6": dict(cfg="configs[1]", d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-6),
+    "c2-d3-e8": dict(cfg="configs[1]", d=3, N=1_000_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-8),
+    "c1": dict(cfg="configs[0]", d=2, N=100_000, m=100, xi=2.0, h_value=1.0, s=0.02, eps=1e-8),
+    "c3-d5": dict(cfg="configs[2]", d=5, N=1_000_000, m=100, xi=3.0, h_value=1.0, s=0.02, eps=1e-8),
+    "c4-d16": dict(cfg="configs[3]", d=16, N=12_000_000, m=256, xi=2.0, h_value=1.0, s=4e-4, eps=1e-2),
+    "c4-d16-e8": dict(cfg="configs[3]", d=16, N=12_000_000, m=256, xi=2.0, h_value=1.0, s=4e-4, eps=1e-8),
+    # configs[4] at N=1 GPU: the largest single-GPU configuration (1.0012e8 points, 6.4 GB); sharded
+    # over the ranks of a torchrun job for the scaling runs
+    "c5": dict(cfg="configs[4]", d=8, N=100_120_000, m=512, xi=2.0, h_value=1.0, s=4e-5, eps=1e-2),
+    "c5-e8": dict(cfg="configs[4]", d=8, N=100_120_000, m=512, xi=2.0, h_value=1.0, s=4e-5, eps=1e-8),
 }
 
 
-def flops_per_entry(d: int, m: int, r: int) -> float:
-    """SURVEY.md 8(d) per-entry flop figure of the fused pass (K5 mode S, spectral error with the
-    D^T D Gram): eval 3d + 1 + F_EXP, skel.P 2r, SYRK m + 1 -> 3d + 2r + m + 34. This is the
-    figure the roofline contract prescribes (`roofline.achieved`)."""
+def flops_per_entry_literal(d: int, m: int, r: int) -> float:
+    """SURVEY.md 8(d)'s literal K5 mode-S figure 3d + 2r + m + 34. It charges skel.P to every column
+    and the SYRK to all m columns, work the pass never does (the skeleton columns of D are exactly
+    zero), so it is reported for reference only -- never as `frac`."""
     return 3 * d + 2 * r + m + 34
 
 
 def flops_per_entry_strict(d: int, m: int, r: int) -> float:
-    """Stricter count of the work the kernel actually needs: eval 3d + 1 + F_EXP,
-    sum K^2 (2), skel.P and the SYRK only over the m - r non-skeleton columns (the skeleton
-    columns of D are exactly zero): 2 r (m - r) / m + (m - r)(m - r + 1) / m."""
+    """The work the residual pass must do per (target, source) entry: eval 3d + 1 +
+    F_EXP, sum K^2 (2), D = K_N - K_S P2 over the m - r non-skeleton columns (2 r (m - r) / m) and
+    the upper triangle of D^T D ((m - r)(m - r + 1) / m). r = m: ||K||_F^2 alone (3d + 35)."""
     me = m - r
+    if me <= 0:
+        return 3 * d + 1 + F_EXP + 2
     return 3 * d + 1 + F_EXP + 2 + 2.0 * r * me / m + me * (me + 1) / m
 
 
 def load_peaks():
+    """FP64 roofline denominator: the SUSTAINED DMMA rate of tools/fp64_peaks.cu (seconds-long
+    back-to-back launches, the regime of a 0.1-1 s pass); the burst figure is kept beside it."""
     p = os.path.join(ROOT, "profiles", "fp64_peaks.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f)
-    return {"fp64_tflops": 37.0, "source": "fallback: tools/fp64_peaks.cu DMMA m8n8k4 loop, round-1 measurement"}
+            pk = json.load(f)
+        pk.setdefault("fp64_tflops_sustained", pk["fp64_tflops"])
+        return pk
+    return {"fp64_tflops": 37.0, "fp64_tflops_sustained": 37.0,
+            "source": "fallback: tools/fp64_peaks.cu DMMA m8n8k4 loop, round-1 burst measurement"}
 
 
 # ----------------------------------------------------------------- clocks
@@ -135,37 +147,40 @@ def dist_env():
 
 # ----------------------------------------------------------------- workload setup (product path)
 class Problem:
-    """One rank's shard: points, the split, and the skeleton / P from the product host path."""
+    """One rank's shard of the workload's dataset: points [rank N / ws, (rank + 1) N / ws) of the
+    same seeded point set on every rank, the (sharded) split, and the skeleton / P from the product
+    host path (drawn by rank 0 over ALL targets, broadcast)."""
 
-    def __init__(self, wl, dev, torch, ws, rank, seed=1):
+    def __init__(self, wl, dev, torch, ws, rank, local, seed=1):
         from paper_1409_2802_b200 import kernid as H
-        self.wl, self.dev, self.torch, self.ws, self.rank = wl, dev, torch, ws, rank
-        d, N, m, xi = wl["d"], wl["N"], wl["m"], wl["xi"]
+        self.wl, self.dev, self.torch, self.ws, self.rank, self.local = wl, dev, torch, ws, rank, local
+        d, N = wl["d"], wl["N"]
         data_seed = H.derive_seed(seed, 0, 0)  # trial 0, scheme 0 (harness.hpp:160-161)
-        pseed = H.derive_seed(data_seed, 0xDA7A) if rank == 0 else H.derive_seed(data_seed, 0xDA7A, rank)
-        self.points = H.gen_normal(d, N, pseed)  # (N, d), rank 0 == the reference trial's data
+        full = H.gen_normal(d, N, H.derive_seed(data_seed, 0xDA7A))  # (N, d): the reference trial's data
+        lo, hi = N * rank // ws, N * (rank + 1) // ws
+        self.full = full if (ws > 1 and rank == 0) else None
+        self.points = np.ascontiguousarray(full[lo:hi]) if ws > 1 else full
+        del full
         self.pts_cm = np.ascontiguousarray(self.points.T).ravel()
-        self.offset = rank * N
+        self.offset = lo
         dev.set_points(self.points, self.offset)
-        from paper_1409_2802_b200 import _lib
-        # RandomPoint center (harness.hpp:95-100) from rank 0's shard
-        ci = H.center_index(N, data_seed)
-        center = self.points[ci].copy()
-        self.center = self._bcast(center)
-        self.h = wl["h_value"] * self._silverman(d, N * ws)
+        ci = H.center_index(N, data_seed)  # RandomPoint center (harness.hpp:95-100)
+        owner = next(g for g in range(ws) if N * g // ws <= ci < N * (g + 1) // ws)
+        self.center = self._bcast(self.points[ci - lo].copy() if lo <= ci < hi else np.zeros(d), owner)
+        self.h = wl["h_value"] * self._silverman(d, N)
         self.data_seed = data_seed
-        self.H, self._lib = H, _lib
+        self.H = H
 
     @staticmethod
     def _silverman(d, N):
         e = 1.0 / (d + 4.0)
         return (4.0 / (2.0 * d + 1.0)) ** e * float(N) ** (-e)
 
-    def _bcast(self, arr):
+    def _bcast(self, arr, owner=0):
         if self.ws == 1:
             return arr
         t = self.torch.tensor(arr, dtype=self.torch.float64, device="cuda")
-        self.torch.distributed.broadcast(t, 0)
+        self.torch.distributed.broadcast(t, owner)
         return t.cpu().numpy()
 
     def split(self):
@@ -180,22 +195,29 @@ class Problem:
         self.src, self.rho, self.nt, self._src_pts = src, rho, nt, src_pts
 
     def skeleton(self):
-        """EuclideanNorm sampling + host ID on rank 0 (product host path), broadcast."""
-        H, dev, wl = self.H, self.dev, self.wl
-        m = wl["m"]
+        """EuclideanNorm sampling over all targets + host ID (product host path) on rank 0, broadcast.
+        Multi-GPU: rank 0 holds the whole point set for this untimed setup step."""
+        H, wl = self.H, self.wl
+        d, m = wl["d"], wl["m"]
         if self.rank == 0:
-            w = dev.row_norms(self.h)
-            tgt_local = dev.targets() - self.offset
+            from paper_1409_2802_b200._lib import Device
+            pts = self.points if self.ws == 1 else self.full
+            dv = self.dev if self.ws == 1 else Device(self.local)
+            src = self.src
+            if self.ws > 1:
+                dv.set_points(pts, 0)
+                src, _, _ = dv.split(self.center, m, wl["xi"])
+            w = dv.row_norms(self.h)
+            tgt = dv.targets()
             sample = H.draw(H.EUCLIDEAN_NORM, w.size, wl["s"], H.derive_seed(self.data_seed, 0, 1), w)
-            src_local = self.src - self.offset if self.ws == 1 else None
-            if self.ws == 1:
-                Ks = H.kernel_rows(self.pts_cm, self.points.shape[0], wl["d"], tgt_local, sample, src_local, self.h)
-            else:
-                Ks = self._rows_global(tgt_local, sample)
-            sv = H.singular_values(Ks)
-            r = H.epsilon_rank(sv, wl["eps"])
+            pcm = self.pts_cm if self.ws == 1 else np.ascontiguousarray(pts.T).ravel()
+            Ks = H.kernel_rows(pcm, pts.shape[0], d, tgt, sample, src, self.h)
+            r = H.epsilon_rank(H.singular_values(Ks), wl["eps"])
             skel, P = H.interpolative_decomposition(Ks, r)
             self.sample_rows = sample.size
+            if self.ws > 1:
+                dv.close()
+                self.full = None
         else:
             r = 0
         if self.ws > 1:
@@ -211,19 +233,6 @@ class Problem:
             skel, P = ts.cpu().numpy(), tp.cpu().numpy()
         self.skel, self.P, self.r = skel, P, r
 
-    def _rows_global(self, tgt_local, sample):
-        # sources may live on other ranks: evaluate with the gathered source coordinates
-        from paper_1409_2802_b200 import kernid as H
-        d = self.wl["d"]
-        src_pts = self._src_points_global()
-        pts = np.concatenate([self.points, src_pts])
-        pts_cm = np.ascontiguousarray(pts.T).ravel()
-        src_idx = np.arange(self.points.shape[0], pts.shape[0], dtype=np.int64)
-        return H.kernel_rows(pts_cm, pts.shape[0], d, tgt_local, sample, src_idx, self.h)
-
-    def _src_points_global(self):
-        return self._src_pts  # gathered with the split's candidates (dist.sharded_split)
-
     def entries(self):
         return self.nt * self.wl["m"]
 
@@ -231,7 +240,7 @@ class Problem:
 def setup(wl, ws, rank, local, torch):
     from paper_1409_2802_b200._lib import Device
     dev = Device(local)
-    prob = Problem(wl, dev, torch, ws, rank)
+    prob = Problem(wl, dev, torch, ws, rank, local)
     prob.split()
     prob.skeleton()
     dev.recon_prepare(prob.skel, prob.P)
@@ -239,15 +248,9 @@ def setup(wl, ws, rank, local, torch):
 
 
 # ----------------------------------------------------------------- our arm
-def run_ours(args):
-    import torch
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = WORKLOADS[args.config]
-    # a dedicated (non-default) stream: the library launches on it, the CUDA events time it
-    torch.cuda.set_stream(torch.cuda.Stream())
+def measure_pass(wl_name, args, torch, ws, rank, local, steps, warmup, e2e_steps):
+    """Set up one workload, time the device-resident fused pass, optionally the e2e path."""
+    wl = WORKLOADS[wl_name]
     dev, prob = setup(wl, ws, rank, local, torch)
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
@@ -261,7 +264,7 @@ def run_ours(args):
         if ws > 1:
             torch.distributed.all_reduce(out)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize()
@@ -270,11 +273,11 @@ def run_ours(args):
     clocks = ClockSampler(local)
     dev.profile(True)
     l0 = dev.launches
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    for i in range(args.steps):
+    for i in range(steps):
         flush.zero_()
         evs[i][0].record(stream)
         step()
@@ -284,6 +287,7 @@ def run_ours(args):
         torch.distributed.barrier()
     launches = dev.launches - l0
     kern_ms = dev.profile_read()
+    kernel = dev.last_kernel()
     dev.profile(False)
     clk = clocks.stop()
     ms = sum(a.elapsed_time(b) for a, b in evs)
@@ -294,49 +298,76 @@ def run_ours(args):
         torch.distributed.all_reduce(ent)
     ms_max = float(t.item())
     total_entries = float(ent.item())
-    value = total_entries * args.steps / (ms_max / 1e3)
-
-    # roofline of the dominant kernel (k_gram, residual mode)
+    value = total_entries * steps / (ms_max / 1e3)
+    # roofline of the dominant kernel: the work it must do (strict count) / its measured duration
     peaks = load_peaks()
+    peak = peaks["fp64_tflops_sustained"]
     kavg = float(np.mean(kern_ms)) if len(kern_ms) else float("nan")
-    fpe = flops_per_entry(wl["d"], m, r)
-    kernel_name = "k_gram (residual mode)"
-    if r >= m:  # full-rank skeleton: D == 0, the pass is ||K||_F^2 alone (k_sumsq): eval + square-sum
-        fpe, kernel_name = 3 * wl["d"] + 1 + F_EXP + 2, "k_sumsq (full-rank skeleton: D == 0)"
+    fpe = flops_per_entry_strict(wl["d"], m, r)
     achieved = prob.entries() * fpe / (kavg / 1e3) / 1e12
-    fpe_strict = flops_per_entry_strict(wl["d"], m, r)
-    achieved_strict = prob.entries() * fpe_strict / (kavg / 1e3) / 1e12
+    frac = achieved / peak
+    assert frac <= 1.0, f"roofline fraction {frac} > 1: flop count or timing is wrong"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(args.config)
+            traffic = json.load(f).get(wl_name)
+    res = {"value": value, "ms_per_step": ms_max / steps, "entries_per_step": total_entries, "rank_r": r,
+           "nt": prob.nt, "h": prob.h, "kernel": kernel, "kernel_ms": kavg, "fpe": fpe, "achieved": achieved,
+           "peak": peak, "frac": frac, "traffic": traffic, "launches": launches, "clocks": clk,
+           "fpe_literal": flops_per_entry_literal(wl["d"], m, r), "peaks": peaks}
+    if e2e_steps:
+        res["e2e"] = run_e2e(dev, prob, torch, ws, rank, e2e_steps)
+    res["_prob"] = prob
+    return res
 
-    # e2e through the C-ABI with host buffers
-    e2e = run_e2e(args, dev, prob, torch, ws, rank)
 
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # a dedicated (non-default) stream: the library launches on it, the CUDA events time it
+    torch.cuda.set_stream(torch.cuda.Stream())
+    wl = WORKLOADS[args.config]
+    R = measure_pass(args.config, args, torch, ws, rank, local, args.steps, args.warmup, max(2, min(args.steps, 5)))
+    prob = R.pop("_prob")
+    m, r = wl["m"], R["rank_r"]
+    sharded = ws > 1
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic: seeded N(0,I_d) points (harness seed streams), no dataset",
-        "config": {"workload": f"BASELINE configs[1] {args.config}: d={wl['d']}, N={wl['N']} points/rank, "
-                               f"N_T={prob.nt}/rank, m={m}, D_WS={wl['xi']}, h=silverman({prob.h:.6g}), "
-                               f"euclidean_norm s={wl['s']}, eps={wl['eps']}, rank r={r}",
-                   "global_targets": int(total_entries // m), "sources": m, "skeleton_rank": r,
-                   "parallelism": f"target shards x{ws}, NCCL all_reduce of D^T D" if ws > 1 else "1 GPU",
+        "metric": METRIC, "value": R["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": R["ms_per_step"], "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded N(0,I_d) points (harness seed streams), no dataset",
+        "config": {"workload": f"BASELINE {wl['cfg']} {args.config}: d={wl['d']}, N={wl['N']} points, "
+                               f"N_T={int(R['entries_per_step'] // m)}, m={m}, D_WS={wl['xi']}, h=silverman({R['h']:.6g}), "
+                               f"euclidean_norm s={wl['s']}, eps={wl['eps']}, skeleton rank r={r}",
+                   "global_targets": int(R["entries_per_step"] // m), "sources": m, "skeleton_rank": r,
+                   "parallelism": (f"the same dataset sharded over {ws} GPUs by index range, NCCL all_reduce of "
+                                   f"[||D||^2, ||K||^2, D^T D]") if sharded else "1 GPU",
                    "l2": "flushed (256 MB write) between timed steps"},
-        "roofline": {"bound": "tensor", "pipe": "FP64 (DMMA + DFMA)", "achieved": achieved,
-                     "peak": peaks["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"],
-                     "traffic": traffic, "kernel": kernel_name, "kernel_ms": kavg,
-                     "flops_per_entry": fpe, "flops_convention": "SURVEY.md 8(d) K5 mode S: 3d + 2r + m + 34",
-                     "frac_strict": achieved_strict / peaks["fp64_tflops"], "flops_per_entry_strict": fpe_strict,
-                     "peak_source": peaks["source"]},
-        "gpu_launches": int(launches),
-        "clocks": clk,
-        "e2e": e2e,
+        "roofline": {"bound": "tensor", "pipe": "FP64 (DMMA + DFMA share one datapath)", "achieved": R["achieved"],
+                     "peak": R["peak"], "unit": "TFLOP/s", "frac": R["frac"], "traffic": R["traffic"],
+                     "kernel": R["kernel"], "kernel_ms": R["kernel_ms"], "flops_per_entry": R["fpe"],
+                     "flops_convention": "strict: 3d + 35 + 2r(m-r)/m + (m-r)(m-r+1)/m per (target, source) entry "
+                                         "(F_EXP = 32, SURVEY.md 8(d)); the work the pass must do",
+                     "flops_per_entry_survey_literal": R["fpe_literal"],
+                     "peak_kind": "sustained (tools/fp64_peaks.cu, back-to-back DMMA launches for 5 s)",
+                     "peak_burst": R["peaks"]["fp64_tflops"], "peak_source": R["peaks"]["source"]},
+        "gpu_launches": int(R["launches"]),
+        "clocks": R["clocks"],
+        "e2e": R["e2e"],
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(prob, budget_s=args.cpu_seconds)
+    if ws == 1 and args.config == "c5" and not args.no_also:
+        A = measure_pass("c2-d3", args, torch, ws, rank, local, 20, 3, 5)
+        A.pop("_prob")
+        line["also"] = {"c2-d3": {"workload": "BASELINE configs[1] c2-d3: d=3, 1e6 points, m=100, eps=1e-2",
+                                  "value": A["value"], "unit": UNIT, "ms_per_step": A["ms_per_step"],
+                                  "skeleton_rank": A["rank_r"], "kernel": A["kernel"], "kernel_ms": A["kernel_ms"],
+                                  "roofline_frac": A["frac"], "flops_per_entry": A["fpe"],
+                                  "e2e": A["e2e"]["value"], "gpu_launches": A["launches"]}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -353,7 +384,7 @@ def run_split(args):
     wl = WORKLOADS[args.config]
     from paper_1409_2802_b200._lib import Device
     dev = Device(local)
-    prob = Problem(wl, dev, torch, 1, 0)
+    prob = Problem(wl, dev, torch, 1, 0, local)
     dev.set_stream(torch.cuda.current_stream().cuda_stream)
     N, d, m = wl["N"], wl["d"], wl["m"]
     for _ in range(args.warmup):
@@ -537,29 +568,41 @@ def run_next_pass(args):
     print(json.dumps(line), flush=True)
 
 
-def run_e2e(args, dev, prob, torch, ws, rank):
-    """Same metric through the C-ABI with host buffers (pinned points H2D every step)."""
+def run_e2e(dev, prob, torch, ws, rank, steps):
+    """The same metric end to end through the public API with HOST buffers every step: the point
+    set H2D from pinned memory (kid_set_points), kid_split (the target list stays on the device),
+    then compress_id's error pass through the host mirror (kernid.error_pass: kid_recon_error ->
+    lambda_max(D^T D); kid_gram -> ||K||_2 = sqrt(lambda_max(K^T K)); rel_error back on the host).
+    Multi-GPU: each rank its shard, the residual Grams all-reduced (NCCL) before lambda_max."""
+    from paper_1409_2802_b200 import kernid as H
     wl = prob.wl
-    N, d, m = wl["N"], wl["d"], wl["m"]
+    N_loc, d, m = prob.points.shape[0], wl["d"], wl["m"]
     host = torch.from_numpy(prob.pts_cm).pin_memory()
     stream = torch.cuda.current_stream()
-    steps = max(3, min(args.steps, 20))
-    times = []
-    for i in range(steps + 2):
+    times, rel = [], None
+    for i in range(steps + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if ws > 1:
             torch.distributed.barrier()
         e0.record(stream)
-        dev.set_points_colmajor_ptr(host.data_ptr(), N, d, prob.offset)
-        prob.split()  # kid_split: the target list stays on the device (SURVEY.md 8b)
-        sd, sk, DtD, _ = dev.recon_error(prob.h, prob.skel, prob.P)
-        if ws > 1:
-            g = torch.tensor(DtD, device="cuda")
+        dev.set_points_colmajor_ptr(host.data_ptr(), N_loc, d, prob.offset)
+        prob.split()
+        if ws == 1:
+            rel, fro, knorm = H.error_pass(dev, prob.h, prob.skel, prob.P)
+        else:
+            sd, sk, DtD, _ = dev.recon_error(prob.h, prob.skel, prob.P)
+            G, _ = dev.gram(prob.h)
+            g = torch.tensor(np.concatenate([[sd, sk], DtD.ravel(), G.ravel()]), device="cuda")
             torch.distributed.all_reduce(g)
-            DtD = g.cpu().numpy()
+            g = g.cpu().numpy()
+            nz = np.setdiff1d(np.arange(m), prob.skel)
+            D2 = g[2:2 + m * m].reshape(m, m)[np.ix_(nz, nz)]
+            num = H.lambda_max(D2) if nz.size else 0.0
+            den = H.lambda_max(g[2 + m * m:].reshape(m, m))
+            rel = math.sqrt(num / den) if den > 0 else 0.0
         e1.record(stream)
         torch.cuda.synchronize()
-        if i >= 2:
+        if i >= 1:
             times.append(e0.elapsed_time(e1))
     ms = float(np.median(times))  # host-side jitter (page-locked copies, syncs) -> median of the steps
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -567,11 +610,12 @@ def run_e2e(args, dev, prob, torch, ws, rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())
     r = prob.r
-    h2d = N * d * 8 + d * 8 + r * 8 + r * m * 8 + m * d * 8
-    d2h = m * 8 + 8 + 8 + (2 + m * m) * 8 + m * d * 8
+    h2d = N_loc * d * 8 + d * 8 + r * 8 + r * m * 8
+    d2h = m * 8 + 8 + 8 + 2 * (2 + m * m) * 8
     return {"value": prob.entries() * ws / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "ms_mean": float(np.mean(times)),
-            "path": "kid_set_points(pinned) -> kid_split (targets stay on the device) -> kid_recon_error"}
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "ms_mean": float(np.mean(times)), "rel_error": rel,
+            "path": "kid_set_points(pinned) -> kid_split -> kernid.error_pass (kid_recon_error + lambda_max(D^T D), "
+                    "kid_gram + lambda_max(K^T K))"}
 
 
 # ----------------------------------------------------------------- CPU baseline (oracle port)
@@ -587,46 +631,64 @@ def reference_pipeline_sample(prob, rows: int, threads: int):
     return K.shape[0] * K.shape[1], num / den if den > 0 else 0.0
 
 
-def _prep_cpu(prob):
-    tgt = prob.dev.targets() - prob.offset
+def _prep_cpu(prob, rows):
+    tgt = prob.dev.targets()[:rows] - prob.offset
     prob.targets_sample = np.ascontiguousarray(prob.points[tgt])
     prob.sources = np.ascontiguousarray(prob.points[prob.src - prob.offset])
 
 
+def default_ref_rows(m: int) -> int:
+    """Rows per reference step: the exact QR of an R x m difference costs ~2 R m^2 single-threaded
+    flops, so R scales as 1/m (50k rows at m = 100, ~10k at m = 512): a few seconds per step."""
+    return max(2000, int(5_000_000 / m))
+
+
 def cpu_baseline(prob, budget_s=15.0):
+    """The oracle port of the reference's error path on a bounded slice of this run's targets (rank 0,
+    N=1): per-entry rate, and the full pass extrapolated from it (c4 / c5 cannot hold the dense K the
+    reference materialises: 20 / 410 GB)."""
     threads = os.cpu_count() or 1
-    _prep_cpu(prob)
-    rows = 20000
+    m = prob.wl["m"]
+    cap = min(prob.nt, 200_000)
+    rows = min(cap, default_ref_rows(m) // 4)
+    _prep_cpu(prob, cap)
     t0 = time.perf_counter()
     reference_pipeline_sample(prob, rows, threads)
     dt = time.perf_counter() - t0
-    rows = int(min(prob.targets_sample.shape[0], max(rows, rows * budget_s / max(dt, 1e-3))))
+    rows = int(min(cap, max(rows, rows * budget_s / max(dt, 1e-3))))
     t0 = time.perf_counter()
     ent, _ = reference_pipeline_sample(prob, rows, threads)
     dt = time.perf_counter() - t0
-    return {"value": ent / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {rows} of {prob.nt} targets x {prob.wl['m']} sources through the oracle's compress_id "
-                      f"error path (K assembly on {threads} threads; QR+SVD exact norms single-threaded as the "
-                      f"reference's Eigen build), {dt:.1f} s"}
+    rate = ent / dt
+    full_s = prob.nt * m / rate
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {rows} of {prob.nt} targets x {m} sources through the oracle's compress_id error path "
+                      f"(K assembly on {threads} threads; QR+SVD exact norms single-threaded as the reference's Eigen "
+                      f"build), {dt:.1f} s; extrapolated full pass over all {prob.nt} targets: {full_s:.0f} s "
+                      f"(an extrapolation: the dense K of the full block does not fit host memory)"}
 
 
 class OracleProblem:
-    """The same trial as our arm (harness seed streams), set up on the host by the oracle alone:
-    points, RandomPoint center, split, EuclideanNorm sample, host ID -- no device code."""
+    """The same trial as our arm (harness seed streams), set up on the host by the oracle alone: points,
+    RandomPoint center, split -- no device code. The ID comes from an EuclideanNorm sample of the
+    first `setup_rows` targets (row norms over all 1e8 targets of c5 would take the CPU minutes);
+    the timed error path is the reference's compress_id error pass on a slice of that block."""
 
-    def __init__(self, wl, threads, seed=1):
+    def __init__(self, wl, threads, setup_rows, seed=1):
         from oracle import oracle as O
         d, N, m, xi = wl["d"], wl["N"], wl["m"], wl["xi"]
         data_seed = O.derive_seed(seed, 0, 0)
         t = O.prepare_trial(d, N, m, xi, data_seed, h_value=wl["h_value"])
         self.wl, self.h, self.nt = wl, t.h, t.targets.shape[0]
         self.targets_sample, self.sources = t.targets, t.sources
-        w = np.concatenate([O.row_norms(O.kernel_matrix(t.targets[i:i + 100_000], t.sources, t.h, threads=threads))
-                            for i in range(0, self.nt, 100_000)])
-        rows = O.sample_rows(O.SCHEME_EUCLIDEAN, self.nt, wl["s"], O.derive_seed(data_seed, 0, 1), w)
+        ns = min(self.nt, setup_rows)
+        w = O.row_norms(O.kernel_matrix(t.targets[:ns], t.sources, t.h, threads=threads))
+        s = min(1.0, max(wl["s"], 4000.0 / ns))
+        rows = O.sample_rows(O.SCHEME_EUCLIDEAN, ns, s, O.derive_seed(data_seed, 0, 1), w)
         Ks = O.kernel_matrix(t.targets[rows], t.sources, t.h, threads=threads)
         r = O.epsilon_rank(O.singular_values(Ks), wl["eps"])
         self.skel, self.P = O.interpolative_decomposition(Ks, r)
+        self.sample_desc = f"ID from an EuclideanNorm sample of {rows.size} of the first {ns} targets"
 
 
 def run_reference(args):
@@ -638,8 +700,8 @@ def run_reference(args):
         return
     wl = WORKLOADS[args.config]
     threads = os.cpu_count() or 1
-    prob = OracleProblem(wl, threads)
-    rows = args.ref_rows
+    rows = args.ref_rows or default_ref_rows(wl["m"])
+    prob = OracleProblem(wl, threads, setup_rows=max(rows, 100_000))
     for _ in range(args.warmup):
         reference_pipeline_sample(prob, rows, threads)
     times, ent = [], 0
@@ -649,31 +711,50 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     v = ent / float(np.mean(times))
     sample = (f"{rows} of {prob.nt} targets x {wl['m']} sources per step through the oracle port of compress_id's "
-              f"error path (K assembly on {threads} threads, exact QR+SVD norms single-threaded)")
+              f"error path (K assembly on {threads} threads, exact QR+SVD norms single-threaded); "
+              f"{prob.sample_desc}")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"BASELINE configs[1] {args.config}", "skeleton_rank": int(len(prob.skel))},
+            "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"BASELINE {wl['cfg']} {args.config}", "skeleton_rank": int(len(prob.skel))},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args):
+    """--gpus N outside torchrun: re-run this script under torch.distributed.run with N ranks."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2-d3", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-also", action="store_true", help="skip the c2-d3 measurement that rides along with c5")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-rows", type=int, default=50000)
+    ap.add_argument("--ref-rows", type=int, default=0, help="reference rows per step (0: 5e6 / m)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--svd-proj", action="store_true", help="--pass svd through kid_proj_gram (C = V_perp) instead of the ID route")
     ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms", "gram", "leverage"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        self_launch(args)
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}: launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args)
     elif args.pass_ == "split":

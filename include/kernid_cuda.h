@@ -66,6 +66,9 @@ int kid_synchronize(kid_ctx* ctx);
 #define KID_PATH_AUTO 0
 #define KID_PATH_CLUSTER 1
 int kid_set_path(kid_ctx* ctx, int32_t path);
+/* Name of the dominant kernel the last pass launched ("k_gram", "k_fused", "k_sumsq", ...): the
+   bench labels its roofline line with the kernel that actually ran. */
+const char* kid_last_kernel(const kid_ctx* ctx);
 
 /* ---- point set (PointSet, kernel.hpp:14): N x d column-major ----
  * index_offset: global index of local row 0 when the point set is sharded across ranks. */

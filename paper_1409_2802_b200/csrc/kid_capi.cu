@@ -152,6 +152,8 @@ int kid_set_stream(kid_ctx* c, void* s) {
   return KID_OK;
 }
 
+const char* kid_last_kernel(const kid_ctx* c) { return c ? c->last_kernel : ""; }
+
 int kid_set_path(kid_ctx* c, int32_t path) {
   if (!c) return KID_E_ERROR;
   if (path != KID_PATH_AUTO && path != KID_PATH_CLUSTER) return fail(c, KID_E_RANGE, "kid_set_path: unknown path");

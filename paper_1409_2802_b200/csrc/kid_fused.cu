@@ -1008,6 +1008,7 @@ int fused_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, dou
     case 4: FX_LAUNCH_T(DD, 4) break;    \
     default: FX_LAUNCH_T(DD, 5) break;   \
   }
+  c->last_kernel = "k_fused";
   prof_begin(c);
   switch (d) {
     case 8: FX_LAUNCH_D(8) break;

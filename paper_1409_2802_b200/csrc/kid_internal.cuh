@@ -202,7 +202,8 @@ struct kid_ctx {
   double* hbuf = nullptr;  // pinned host staging
   size_t hbuf_cap = 0;
   int64_t* counter = nullptr;  // device counters [8]
-  int path = KID_PATH_AUTO;  // kid_set_path: which kernel family serves the Gram / leverage passes
+  int path = KID_PATH_AUTO;
+  const char* last_kernel = "";  // dominant kernel of the last pass (kid_last_kernel)  // kid_set_path: which kernel family serves the Gram / leverage passes
   void* sort_tmp = nullptr;       // CUB radix-sort temporary storage (pass 1)
   size_t sort_tmp_cap = 0;
 

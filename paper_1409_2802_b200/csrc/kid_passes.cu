@@ -678,6 +678,7 @@ int sumsq_dev(kid_ctx* c, double h, double* d_out) {
   double* part = (double*)scratch(c, sizeof(double) * (blocks + 8));
   if (!part) return KID_E_OOM;
   const double cscale = std::sqrt(1.0 / (2.0 * h * h));
+  c->last_kernel = "k_sumsq";
 #define LAUNCH(DD)                                                                                  \
   {                                                                                                 \
     cudaFuncSetAttribute(k_sumsq<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
@@ -849,6 +850,7 @@ int gram_dev(kid_ctx* c, double h, int64_t r, double* d_out) {
     KID_CK(c, cudaMemsetAsync(A.trace, 0, sizeof(long long) * trace_n, c->stream));
   }
   dim3 grid(nchunks, nparts);
+  c->last_kernel = "k_gram";
 #define LAUNCH_B(DD, BB, WW)                                                                           \
   {                                                                                                    \
     cudaFuncSetAttribute(k_gram<DD, BB, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \

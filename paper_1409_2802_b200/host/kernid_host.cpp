@@ -1601,6 +1601,10 @@ int kidh_sym_eig(const double* A, int64_t n, double* evals, double* evecs) {
   });
 }
 
+int kidh_lambda_max(const double* A, int64_t n, double* lmax) {
+  return guard([&] { *lmax = lambda_max(wrap(A, n, n)); });
+}
+
 int kidh_sym_eigvals(const double* A, int64_t n, double* evals) {
   return guard([&] {
     const std::vector<double> ev = sym_eigvals(wrap(A, n, n));

@@ -42,6 +42,7 @@ def host_lib():
         L.kidh_interpolative_decomposition.argtypes = [_dp, i64, i64, i64, _ip, _dp]
         L.kidh_sym_eig.argtypes = [_dp, i64, _dp, C.c_void_p]
         L.kidh_sym_eigvals.argtypes = [_dp, i64, _dp]
+        L.kidh_lambda_max.argtypes = [_dp, i64, P(dbl)]
         L.kidh_draw.argtypes = [i32, i32, i64, C.c_void_p, dbl, u64, _ip, P(i64)]
         L.kidh_kernel_rows.argtypes = [_dp, i64, i32, _ip, _ip, i64, _ip, i64, dbl, _dp]
         L.kidh_error_pass.argtypes = [C.c_void_p, dbl, _ip, i64, _dp, dbl, P(dbl), P(dbl), P(dbl)]
@@ -117,6 +118,17 @@ def sym_eigvals(A):
     ev = np.zeros(n)
     _ck(host_lib().kidh_sym_eigvals(_cm(A), n, ev), "sym_eigvals")
     return ev
+
+
+def lambda_max(A) -> float:
+    """Largest eigenvalue of a symmetric PSD matrix (Jacobi for n <= 128, Lanczos above)."""
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    if n == 0:
+        return 0.0
+    v = C.c_double()
+    _ck(host_lib().kidh_lambda_max(_cm(A), n, C.byref(v)), "lambda_max")
+    return v.value
 
 
 def sym_eig(A):

@@ -153,3 +153,31 @@ def test_sym_eig_vectors_large():
     assert np.max(np.abs(ev - ref)) <= 1e-13 * ref[0]
     assert np.max(np.abs(A @ V - V * ev)) <= 1e-13 * ref[0]
     assert np.max(np.abs(V.T @ V - np.eye(n))) <= 1e-12
+
+
+@pytest.mark.parametrize("n,kind", [(50, "rand"), (200, "rand"), (512, "rand"), (300, "cluster"), (256, "lowrank"),
+                                    (129, "gram")])
+def test_host_lambda_max(n, kind):
+    """lambda_max (Jacobi for n <= 128, Lanczos with full reorthogonalisation above) against LAPACK:
+    the spectral norms of compress_id at c4 / c5 (m = 256 / 512) come from it."""
+    from paper_1409_2802_b200 import kernid as H
+    rng = np.random.default_rng(n)
+    if kind == "rand":
+        X = rng.standard_normal((n + 7, n))
+        A = X.T @ X
+    elif kind == "cluster":  # top eigenvalues nearly equal: slow Lanczos convergence, exact at k = n
+        Q = np.linalg.qr(rng.standard_normal((n, n)))[0]
+        ev = np.concatenate([[1.0, 1.0 - 1e-9, 1.0 - 2e-9], rng.random(n - 3) * 0.5])
+        A = (Q * ev) @ Q.T
+    elif kind == "lowrank":  # rank 5 PSD, the numerically rank-deficient Gram of a far-field block
+        X = rng.standard_normal((5, n)) * np.array([1e-3, 1e-7, 1e-11, 1e-15, 1e-20])[:, None]
+        A = X.T @ X
+    else:
+        t = rng.standard_normal((4000, 3))
+        s = rng.standard_normal((n, 3)) * 0.3
+        K = np.exp(-((t[:, None, :] - s[None, :, :]) ** 2).sum(-1))
+        A = K.T @ K
+    A = 0.5 * (A + A.T)
+    ref = np.linalg.eigvalsh(A)[-1]
+    got = H.lambda_max(A)
+    assert abs(got - ref) <= 1e-12 * ref, (got, ref)

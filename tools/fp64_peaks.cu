@@ -110,6 +110,27 @@ int main() {
     double ne = 8.0 * iters * (double)blocks * threads;
     printf("{\"kernel\": \"exp_f64\", \"gexp_per_s\": %.2f, \"ms\": %.3f}\n", ne / ms / 1e6, ms);
   }
+  // sustained: back-to-back launches for ~5 s each (the clocks a seconds-long FP64 pass runs at)
+  for (int kind = 0; kind < 2; ++kind) {
+    const int iters = kind == 0 ? 40000 : 80000;  // ~0.1-0.2 s per launch
+    double flops = 0.0, tot_ms = 0.0;
+    cudaEventRecord(e0);
+    int launches = 0;
+    while (tot_ms < 5000.0) {
+      for (int k = 0; k < 4; ++k, ++launches) {
+        if (kind == 0) dmma884_loop<<<blocks, threads>>>(out, iters);
+        else dfma_loop<<<blocks, threads>>>(out, iters, 0.999, 1e-3);
+        flops += kind == 0 ? 2.0 * 8 * 8 * 4 * 8 * iters * (double)blocks * (threads / 32)
+                           : 2.0 * 64 * iters * (double)blocks * threads;
+      }
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      cudaEventElapsedTime(&ms, e0, e1);
+      tot_ms = ms;
+    }
+    printf("{\"kernel\": \"%s_sustained\", \"tflops\": %.2f, \"seconds\": %.2f, \"launches\": %d}\n",
+           kind == 0 ? "dmma_m8n8k4" : "dfma", flops / tot_ms / 1e9, tot_ms / 1e3, launches);
+  }
   size_t n = (size_t)1 << 27;  // 4 GiB per buffer in double4? no: 2^27 * 32 B = 4 GiB
   double4 *a, *b; CK(cudaMalloc(&a, n * sizeof(double4))); CK(cudaMalloc(&b, n * sizeof(double4)));
   cudaMemset(a, 0, n * sizeof(double4));
