@@ -134,7 +134,7 @@ void kid_destroy(kid_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  void* bufs[] = {c->pts_own, c->dist, c->tgt_idx, c->blk_tgt, c->src, c->src_perm, c->P2,
+  void* bufs[] = {c->pts_own, c->dist, c->flag, c->tgt_idx, c->blk_tgt, c->src, c->src_perm, c->P2,
                   c->scratch, c->partial, c->counter, c->sort_tmp, c->sub_idx};
   for (void* p : bufs)
     if (p) cudaFree(p);

@@ -176,9 +176,9 @@ __device__ __forceinline__ void fx_syrk(double (&acc)[TPW][2][2][2], const int (
   }
 }
 
-// GEMM1 column blocks per MMA warp: 4, or 3 for the widest SYRK layouts (register budget)
+// GEMM1 column blocks per MMA warp: 4, or 3 for the widest SYRK layout (register budget)
 template <int TPW>
-__host__ __device__ constexpr int fx_cbm() { return TPW >= 4 ? 3 : kFCB; }
+__host__ __device__ constexpr int fx_cbm() { return TPW >= 5 ? 3 : kFCB; }
 
 template <int D, int TPW>
 __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs A) {
@@ -245,9 +245,11 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
       mbar_init(smem_u32(&bars[2 * S + s]), kFM);  // free: the peer's MMA warps released my stage s
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // zero-byte exchanges (a CTA that owns no D block, or whose peer owns none) use no barrier at all:
+    // re-arming one would complete its next phase at once and flip the parity under a slow waiter
     for (int s = 0; s < S; ++s) {
-      mbar_expect(smem_u32(&bars[s]), xbytes);
-      mbar_expect(smem_u32(&bars[S + s]), dbytes);
+      if (xbytes) mbar_expect(smem_u32(&bars[s]), xbytes);
+      if (dbytes) mbar_expect(smem_u32(&bars[S + s]), dbytes);
     }
   }
   __syncthreads();
@@ -452,8 +454,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
               }
           }
         }
-        mbar_wait(xfull0 + 8 * s, use & 1);
-        if (mw == 0 && lane == 0 && it + S < ntile) mbar_expect(xfull0 + 8 * s, xbytes);
+        if (xbytes) {
+          mbar_wait(xfull0 + 8 * s, use & 1);
+          if (mw == 0 && lane == 0 && it + S < ntile) mbar_expect(xfull0 + 8 * s, xbytes);
+        }
         const double* xb = Xb + (size_t)s * A.own_max * kST;
 #pragma unroll
         for (int i = 0; i < CBM; ++i) {
@@ -531,8 +535,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
         }
       }
       nbar_sync(kBMma, kFM * 32);           // my half of Db[s] is complete
-      mbar_wait(dfull0 + 8 * s, use & 1);   // ... and the peer's half has landed
-      if (mw == 0 && lane == 0 && it + S < ntile) mbar_expect(dfull0 + 8 * s, dbytes);
+      if (dbytes) {                         // ... and the peer's half has landed
+        mbar_wait(dfull0 + 8 * s, use & 1);
+        if (mw == 0 && lane == 0 && it + S < ntile) mbar_expect(dfull0 + 8 * s, dbytes);
+      }
       const double* col = db + fr * kST + fk;
       switch (ntl) {
         case 1: fx_syrk<1, TPW>(g, fa0, fb0, col); break;
@@ -761,7 +767,7 @@ int fused_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, dou
   int TPW = 1;
   for (auto& p : parts) TPW = std::max(TPW, (int)((p.tiles.size() + 2 * kFM - 1) / (2 * kFM)));
   if (TPW > kFTPW) return fail(c, KID_E_DIM, "fused pass: Gram part exceeds the register budget");
-  const int CBM = TPW >= 4 ? 3 : kFCB;
+  const int CBM = TPW >= 5 ? 3 : kFCB;
   // ---- k-split of the A columns over the two CTAs (chunks of 32)
   const int a0 = has_A ? std::min(a, ceil_to((a + 1) / 2, 4)) : 0;
   const int a_lo[2] = {0, a0}, a_cnt[2] = {a0, a - a0};

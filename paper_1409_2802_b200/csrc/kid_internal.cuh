@@ -161,6 +161,8 @@ struct kid_ctx {
   // split state
   double* dist = nullptr;
   size_t dist_cap = 0;
+  unsigned char* flag = nullptr;  // pass 1 fast path: 1 = surely a target, 0 = near (exact dist kept)
+  size_t flag_cap = 0;
   int64_t* tgt_idx = nullptr;
   size_t tgt_cap = 0;
   int64_t n_split_targets = 0;

@@ -256,6 +256,174 @@ __global__ void __launch_bounds__(kCT) k_compact(const double* __restrict__ dist
   }
 }
 
+// ---- fast path (kid_split on one rank): one byte per point instead of the 8-byte distance.
+// T (>= rho, the sample bound) is known before the distance pass, so a point with dist > T and
+// dist >= xi T is a target whatever rho turns out to be (rho <= T; xi * x rounds monotonically):
+// flag 1. Every other point is "near": its exact distance is kept (a sparse 8-byte store; ~0.3% of
+// the points at c5) and resolved against rho in the compaction. Traffic: 8 d N + N + 8 N_T (+ the
+// near points), against the algorithmic 8 d N + 8 N_T.
+__global__ void __launch_bounds__(256) k_dist_flag(const double* __restrict__ pts, int64_t N, int d,
+                                                   const double* __restrict__ center,
+                                                   const unsigned int* __restrict__ T32, double xi,
+                                                   unsigned char* __restrict__ flag, double* __restrict__ dist,
+                                                   unsigned long long* __restrict__ cand_key,
+                                                   unsigned long long* __restrict__ cand_idx,
+                                                   unsigned long long* __restrict__ cand_count, int64_t cap) {
+  __shared__ double c_s[64];
+  if (threadIdx.x < d) c_s[threadIdx.x] = center[threadIdx.x];
+  __syncthreads();
+  const double Td = (double)__int_as_float((int)*T32);
+  const unsigned long long T = (unsigned long long)__double_as_longlong(Td);
+  const double cut = xi * Td;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < N; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool cand = false;
+    unsigned long long key = 0;
+    if (i < N) {
+      double diff = __dsub_rn(__ldcs(pts + i), c_s[0]);
+      double acc = __dmul_rn(diff, diff);
+      for (int k = 1; k < d; ++k) {
+        diff = __dsub_rn(__ldcs(pts + i + k * N), c_s[k]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+      }
+      const double v = __dsqrt_rn(acc);
+      const bool sure = v > Td && v >= cut;
+      flag[i] = sure ? 1 : 0;
+      if (!sure) dist[i] = v;
+      key = (unsigned long long)__double_as_longlong(v);
+      cand = key <= T;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, cand);
+    if (mask) {
+      unsigned long long pos0 = 0;
+      if (lane == 0) pos0 = atomicAdd(cand_count, (unsigned long long)__popc(mask));
+      pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+      if (cand) {
+        const unsigned long long pos = pos0 + __popc(mask & ((1u << lane) - 1u));
+        if ((int64_t)pos < cap) {
+          cand_key[pos] = key;
+          cand_idx[pos] = (unsigned long long)i;
+        }
+      }
+    }
+  }
+}
+
+// Stable compaction of the flagged points (ascending index): 256 threads x 16 consecutive points
+// per tile (one 16-byte flag load per thread), block scan, decoupled look-back over tiles, output
+// staged in shared memory and written coalesced.
+__global__ void __launch_bounds__(kCT) k_compact_flag(const unsigned char* __restrict__ flag,
+                                                      const double* __restrict__ dist, int64_t N,
+                                                      const int64_t* __restrict__ src_local, int64_t n_src,
+                                                      int64_t* __restrict__ out,
+                                                      unsigned long long* __restrict__ tile_status,
+                                                      unsigned int* __restrict__ tile_counter,
+                                                      int64_t* __restrict__ total_out, int64_t ntiles,
+                                                      const double* __restrict__ rho_dev, double xi) {
+  const double rho = *rho_dev, cutoff = xi * rho;  // geometry.hpp:57
+  __shared__ unsigned int tile_s;
+  __shared__ long long wsum[kCT / 32];
+  __shared__ long long excl_s, total_s;
+  __shared__ int64_t stage[kTile];
+  if (threadIdx.x == 0) tile_s = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const int64_t tile = tile_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t first = tile * kTile + (int64_t)threadIdx.x * kIPT;
+  unsigned bits = 0;
+  if (first + kIPT <= N) {
+    const uint4 f4 = *reinterpret_cast<const uint4*>(flag + first);
+    const unsigned w4[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+    for (int j = 0; j < kIPT; ++j) bits |= ((w4[j >> 2] >> (8 * (j & 3))) & 1u) << j;
+  } else {
+    for (int j = 0; j < kIPT; ++j)
+      if (first + j < N) bits |= (unsigned)(flag[first + j] & 1) << j;
+  }
+  // near points: the exact distance against rho, the source list where dist <= rho
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    const int64_t i = first + j;
+    if (i < N && !((bits >> j) & 1u)) {
+      const double v = dist[i];
+      bool f = v >= cutoff;
+      if (f && v <= rho) f = !is_source(src_local, n_src, i);
+      bits |= (unsigned)f << j;
+    }
+  }
+  // block exclusive scan of the per-thread counts
+  const int cnt = __popc(bits);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long run = 0;
+    for (int w = 0; w < kCT / 32; ++w) {
+      const long long t = wsum[w];
+      wsum[w] = run;
+      run += t;
+    }
+    total_s = run;
+  }
+  __syncthreads();
+  const long long total = total_s;
+  const int my_off = (int)(wsum[warp] + incl - cnt);
+  if (warp == 0) {
+    long long excl = 0;
+    if (tile == 0) {
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&tile_status[0], kStInc | (unsigned long long)total);
+      }
+    } else {
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&tile_status[tile], kStAgg | (unsigned long long)total);
+      }
+      int64_t p = tile - 1;
+      for (;;) {
+        const int64_t q = p - lane;
+        unsigned long long sv = kStInc;
+        if (q >= 0) {
+          do {
+            sv = *((volatile unsigned long long*)&tile_status[q]);
+          } while ((sv & ~kValMask) == 0);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, (sv & ~kValMask) == kStInc);
+        const int firstinc = inc ? __ffs(inc) - 1 : 31;
+        long long v = lane <= firstinc ? (long long)(sv & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (inc) break;
+        p -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&tile_status[tile], kStInc | (unsigned long long)(excl + total));
+      }
+    }
+    if (lane == 0) {
+      excl_s = excl;
+      if (tile == ntiles - 1) *total_out = excl + total;
+    }
+  }
+  // stage this tile's targets in index order, then one coalesced store
+  int k = my_off;
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j)
+    if ((bits >> j) & 1u) stage[k++] = first + j;
+  __syncthreads();
+  const long long excl = excl_s;
+  for (int e = threadIdx.x; e < (int)total; e += kCT) __stcs(out + excl + e, stage[e]);
+}
+
 // Device-side selection of the n sources (single CTA; the candidate count is read on the device):
 // each candidate's rank under (dist, idx) -- nth_element's comparator (geometry.hpp:40-47) -- by
 // counting over the <= kSelMax candidates in shared memory (warp-uniform broadcast reads, no
@@ -368,9 +536,11 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   if (ensure(c, &c->sort_tmp, &c->sort_tmp_cap, tmpb)) return KID_E_OOM;
   KID_CK(c, cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmpb, skeys, skeys2, (int)S, 0, 32, c->stream));
   c->launches += 4;
+  if (ensure(c, (void**)&c->flag, &c->flag_cap, (size_t)ntiles * kTile)) return KID_E_OOM;
+  unsigned char* flag = c->flag;
   prof_begin(c);
-  k_dist_cand<<<c->sms * 8, 256, 0, c->stream>>>(c->pts, N, d, center, nullptr, c->dist, ck, ci, count, cap,
-                                                 skeys2 + (ks - 1));
+  k_dist_flag<<<c->sms * 8, 256, 0, c->stream>>>(c->pts, N, d, center, skeys2 + (ks - 1), xi, flag, c->dist, ck, ci,
+                                                 count, cap);
   prof_end(c);
   KID_LAUNCHED(c);
   const size_t sel_smem = sizeof(unsigned long long) * 2 * (kSelMax + kSelT);
@@ -378,8 +548,8 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   k_split_select<<<1, kSelT, sel_smem, c->stream>>>(ck, ci, count, cap, (int)nl, c->pts, N, d, src_local, c->src, ctrl);
   KID_LAUNCHED(c);
   prof_begin(c);
-  k_compact<<<(unsigned)ntiles, kCT, 0, c->stream>>>(c->dist, N, 0.0, 0.0, src_local, nl, c->tgt_idx, status,
-                                                     (unsigned int*)c->counter, c->counter + 1, ntiles, ctrl, xi);
+  k_compact_flag<<<(unsigned)ntiles, kCT, 0, c->stream>>>(flag, c->dist, N, src_local, nl, c->tgt_idx, status,
+                                                          (unsigned int*)c->counter, c->counter + 1, ntiles, ctrl, xi);
   prof_end(c);
   KID_LAUNCHED(c);
   // one D2H of [rho, overflow | nt | source indices | source coordinates] and one synchronisation
