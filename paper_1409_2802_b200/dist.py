@@ -85,3 +85,83 @@ def sharded_tsqr(dev, h: float, group=None, device=None) -> np.ndarray:
     m = R.shape[0]
     allR = all_gather_np(R.reshape(1, -1), group, device)
     return dev.tsqr_combine([row.reshape(m, m) for row in allR])
+
+
+def all_gather_ragged(arr: np.ndarray, group=None, device=None) -> np.ndarray:
+    """all_gather of 1-D float64 arrays of different lengths, concatenated in rank order."""
+    import torch.distributed as dist
+    ws = dist.get_world_size(group)
+    n = np.array([float(arr.size)])
+    sizes = all_gather_np(n, group, device).astype(np.int64)
+    width = int(max(1, sizes.max()))
+    pad = np.zeros(width)
+    pad[: arr.size] = arr
+    allp = all_gather_np(pad.reshape(1, -1), group, device)
+    return np.concatenate([allp[g, : sizes[g]] for g in range(ws)])
+
+
+def sharded_sample_rows(dev, points_local: np.ndarray, offset: int, src_pts: np.ndarray, h: float, s: float,
+                        seed: int, scheme: int, group=None, device=None, weights_fn=None):
+    """sample_rows (sampling.hpp:156-243) over the targets of ALL shards, then the sampled kernel rows.
+
+    Each rank computes the weights of its own targets (EuclideanNorm: kid_row_norms, sampling.hpp:189-196;
+    or weights_fn() -- e.g. leverage scores, sampling.hpp:212-221); the weight vectors are gathered in
+    rank order -- the global target order, shards being contiguous index ranges -- and every rank draws
+    the identical sample with the reference seed stream (the host draw, sampling.hpp:78-149). The
+    sampled rows K(T[sample], S) are evaluated with the reference arithmetic by the rank that holds the
+    target and gathered, so every rank then runs the identical host ID.
+    Returns (sample positions in the global target list, K_s (count x m), global target count)."""
+    from . import kernid as H
+    d = points_local.shape[1]
+    if scheme == H.UNIFORM:
+        w_local = np.zeros(0)
+        nt_local = dev.nt
+        counts = all_gather_np(np.array([float(nt_local)]), group, device).astype(np.int64)
+        NT = int(counts.sum())
+        sample = H.draw(H.UNIFORM, NT, s, seed)
+    else:
+        w_local = weights_fn() if weights_fn is not None else dev.row_norms(h)
+        counts = all_gather_np(np.array([float(w_local.size)]), group, device).astype(np.int64)
+        w = all_gather_ragged(np.asarray(w_local, dtype=np.float64), group, device)
+        NT = w.size
+        sample = H.draw(scheme, NT, s, seed, w)
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    lo = int(counts[:rank].sum())
+    hi = lo + int(counts[rank])
+    mine = np.nonzero((sample >= lo) & (sample < hi))[0]  # positions in the sample held by this rank
+    m = src_pts.shape[0]
+    rows = np.zeros((sample.size, m))
+    if mine.size:
+        tgt_local = dev.targets() - offset
+        pts = np.concatenate([points_local, src_pts])  # sources may live on other shards
+        pcm = np.ascontiguousarray(pts.T).ravel()
+        src_idx = np.arange(points_local.shape[0], pts.shape[0], dtype=np.int64)
+        rows[mine] = H.kernel_rows(pcm, pts.shape[0], d, tgt_local, sample[mine] - lo, src_idx, h)
+    # each sampled row is held by exactly one rank: the ordered sum over ranks assembles K_s exactly
+    Ks = ordered_sum(rows, group, device)
+    return sample, Ks, NT
+
+
+def sharded_compress_id(dev, points_local: np.ndarray, offset: int, src_pts: np.ndarray, skel_rule_eps: float,
+                        h: float, s: float, seed: int, scheme: int, group=None, device=None):
+    """compress_id (compress.hpp:168-215) on the sharded block: the sample and K_s over all shards
+    (sharded_sample_rows), the host ID (identical on every rank), the fused error pass on each shard,
+    [||D||^2, ||K||^2, D^T D, K^T K] summed in rank order, rel_error = sqrt(lmax(D^T D) / lmax(K^T K)).
+    Returns (skeleton, P, rel_error, rel_error_fro, sample)."""
+    from . import kernid as H
+    sample, Ks, _ = sharded_sample_rows(dev, points_local, offset, src_pts, h, s, seed, scheme, group, device)
+    r = H.epsilon_rank(H.singular_values(Ks), skel_rule_eps)
+    m = Ks.shape[1]
+    if r == 0:
+        return np.zeros(0, np.int64), np.zeros((0, m)), 1.0, 1.0, sample
+    skel, P = H.interpolative_decomposition(Ks, r)
+    sd, sk, DtD, KtK = dev.recon_error(h, skel, P, flags=3)
+    red = ordered_sum(np.concatenate([[sd, sk], DtD.ravel(), KtK.ravel()]), group, device)
+    nz = np.setdiff1d(np.arange(m), skel)
+    D2 = red[2:2 + m * m].reshape(m, m)[np.ix_(nz, nz)]
+    num = H.lambda_max(D2) if nz.size else 0.0
+    den = H.lambda_max(red[2 + m * m:].reshape(m, m))
+    rel = float(np.sqrt(num / den)) if den > 0 else 0.0
+    fro = float(np.sqrt(red[0] / red[1])) if red[1] > 0 else 0.0
+    return skel, P, rel, fro, sample

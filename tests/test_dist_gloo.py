@@ -19,7 +19,7 @@ class CpuShard:
     def __init__(self, pts, offset):
         self.pts, self.offset = pts, offset
         self.dist = None
-        self.targets = None
+        self.tgt = None
 
     def split_candidates(self, center, n):
         p = self.pts
@@ -33,17 +33,34 @@ class CpuShard:
 
     def tsqr_r(self, h):  # stand-in for kid_tsqr_r on this shard's block
         from oracle import oracle as O
-        return np.linalg.qr(O.kernel_matrix(self.pts[self.targets - self.offset], self.src_pts, h), mode="r")
+        return np.linalg.qr(O.kernel_matrix(self.pts[self.tgt - self.offset], self.src_pts, h), mode="r")
 
     def tsqr_combine(self, Rs):  # stand-in for kid_tsqr_combine
         return np.linalg.qr(np.concatenate(Rs), mode="r")
+
+    def targets(self):
+        return self.tgt
 
     def split_finish(self, src_idx, rho, xi, src_points=None):
         self.src_pts = src_points
         local = np.arange(self.pts.shape[0]) + self.offset
         keep = (self.dist >= xi * rho) & ~np.isin(local, src_idx)
-        self.targets = local[keep]
-        return int(keep.sum())
+        self.tgt = local[keep]
+        self.nt = int(keep.sum())
+        return self.nt
+
+    # the device passes on this shard's block, with the oracle's arithmetic
+    def _K(self, h):
+        from oracle import oracle as O
+        return O.kernel_matrix(self.pts[self.tgt - self.offset], self.src_pts, h)
+
+    def row_norms(self, h):
+        from oracle import oracle as O
+        return O.row_norms(self._K(h))
+
+    def recon_error(self, h, skel, P, flags=1):
+        from oracle import oracle as O
+        return O.residual_stats(self._K(h), skel, P)
 
 
 def _free_port():
@@ -67,14 +84,14 @@ def _worker(rank, ws, port, d, N, n, xi, q):
     src, rho, src_pts, nt = D.sharded_split(shard, allpts[lo:hi], lo, center, n, xi)
     # per-shard fused-pass partials (oracle arithmetic), reduced in rank order
     t = O.split_sources_targets(allpts, center, n, xi)
-    K_local = O.kernel_matrix(allpts[shard.targets], src_pts, 0.3)
+    K_local = O.kernel_matrix(allpts[shard.tgt], src_pts, 0.3)
     skel = np.array([0, 5, 9])
     P = np.random.default_rng(0).standard_normal((3, n))
     P[:, skel] = np.eye(3)
     sd, sk, DtD, KtK = O.residual_stats(K_local, skel, P)
     red = D.ordered_sum(np.concatenate([[sd, sk], DtD.ravel()]))
     R = D.sharded_tsqr(shard, 0.3)
-    q.put((rank, src, rho, shard.targets, red, R))
+    q.put((rank, src, rho, shard.tgt, red, R))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -112,6 +129,55 @@ def test_sharded_split_and_reduction_match_single_process(oracle, d, N, n, xi):
     R = res[0][5]
     assert np.array_equal(R, res[1][5])
     assert np.allclose(R.T @ R, K.T @ K, rtol=0, atol=1e-12 * np.abs(K.T @ K).max())
+
+
+def _compress_worker(rank, ws, port, d, N, n, xi, h, s, eps, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from oracle import oracle as O
+    from paper_1409_2802_b200 import dist as D
+    from paper_1409_2802_b200 import kernid as H
+    allpts = O.gen_normal(d, N, 4242)
+    lo, hi = N * rank // ws, N * (rank + 1) // ws
+    shard = CpuShard(allpts[lo:hi], lo)
+    src, rho, src_pts, nt = D.sharded_split(shard, allpts[lo:hi], lo, allpts[11], n, xi)
+    skel, P, rel, fro, sample = D.sharded_compress_id(shard, allpts[lo:hi], lo, src_pts, eps, h, s, 99,
+                                                      H.EUCLIDEAN_NORM)
+    q.put((rank, skel, P, rel, fro, sample))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_sharded_compress_id_matches_single_process(oracle, ws):
+    """compress_id on a block sharded over ws ranks (gloo): the EuclideanNorm weights gathered in rank
+    order give the single-process sample, the host ID the same skeleton and P (bitwise), and the rank-
+    ordered sum of the per-shard residual Grams the single-process rel_error (sampling.hpp:189-196,
+    compress.hpp:168-215)."""
+    d, N, n, xi, h, s, eps = 3, 6000, 60, 2.0, 0.35, 0.05, 1e-6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_compress_worker, args=(r, ws, port, d, N, n, xi, h, s, eps, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=180) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    allpts = oracle.gen_normal(d, N, 4242)
+    t = oracle.split_sources_targets(allpts, allpts[11], n, xi)
+    K = oracle.kernel_matrix(allpts[t.target_indices], allpts[t.source_indices], h)
+    w = oracle.row_norms(K)
+    sample = oracle.sample_rows(oracle.SCHEME_EUCLIDEAN, K.shape[0], s, 99, w)
+    ref = oracle.compress_id(K, sample, eps=eps)
+    for _, skel, P, rel, fro, smp in res:
+        assert np.array_equal(smp, sample)
+        assert np.array_equal(skel, ref.skeleton)
+        assert np.array_equal(P, ref.P)
+        assert rel == pytest.approx(ref.rel_error, rel=1e-9)
+    assert all(r[3] == res[0][3] for r in res)  # identical on every rank
 
 
 def test_merge_candidates_tie_break():
