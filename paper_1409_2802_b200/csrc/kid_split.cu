@@ -23,6 +23,8 @@ namespace kid {
 namespace {
 
 constexpr int kSampleMax = 65536;
+constexpr int64_t kSampleBig = 1 << 20;
+inline int64_t ceil_to64(int64_t x) { return (x + 255) / 256 * 256; }
 
 __device__ __forceinline__ double point_dist(const double* __restrict__ pts, int64_t N, int d,
                                              int64_t i, const double* __restrict__ c) {
@@ -38,11 +40,16 @@ __device__ __forceinline__ double point_dist(const double* __restrict__ pts, int
 // 32-bit sample keys: the distance rounded UP to float (monotone), so the n-th smallest of them,
 // widened back to double, still bounds the n-th smallest sample distance from above -- half the
 // radix passes of the 64-bit keys.
+// The sample is S / kRun runs of kRun consecutive points spread evenly over [0, N) (coalesced reads);
+// any subset gives a valid bound, the spread only keeps the candidate count near its expectation.
+constexpr int kRun = 256;
 __global__ void k_sample_keys32(const double* __restrict__ pts, int64_t N, int d, const double* __restrict__ center,
                                 int64_t S, unsigned int* __restrict__ keys) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= S) return;
-  const int64_t i = (S == N) ? j : (int64_t)(((__int128)j * N) / S);
+  const int64_t runs = S / kRun;
+  const long long r0 = (long long)(((__int128)(j / kRun) * N) / runs);
+  const int64_t i = (S == N) ? j : (int64_t)min(r0, (long long)(N - kRun)) + j % kRun;
   keys[j] = (unsigned int)__float_as_int(__double2float_ru(point_dist(pts, N, d, i, center)));
 }
 
@@ -310,9 +317,10 @@ __global__ void __launch_bounds__(256) k_dist_flag(const double* __restrict__ pt
   }
 }
 
-// Stable compaction of the flagged points (ascending index): 256 threads x 16 consecutive points
-// per tile (one 16-byte flag load per thread), block scan, decoupled look-back over tiles, output
-// staged in shared memory and written coalesced.
+// Stable compaction of the flagged points (ascending index): 256 threads x 32 consecutive points per
+// tile (two 16-byte flag loads per thread), block scan, decoupled look-back over tiles, output staged
+// in shared memory (64 KB) and written coalesced.
+constexpr int kFIPT = 32, kFTile = kCT * kFIPT;
 __global__ void __launch_bounds__(kCT) k_compact_flag(const unsigned char* __restrict__ flag,
                                                       const double* __restrict__ dist, int64_t N,
                                                       const int64_t* __restrict__ src_local, int64_t n_src,
@@ -322,35 +330,37 @@ __global__ void __launch_bounds__(kCT) k_compact_flag(const unsigned char* __res
                                                       int64_t* __restrict__ total_out, int64_t ntiles,
                                                       const double* __restrict__ rho_dev, double xi) {
   const double rho = *rho_dev, cutoff = xi * rho;  // geometry.hpp:57
+  extern __shared__ int64_t stage[];  // kFTile
   __shared__ unsigned int tile_s;
   __shared__ long long wsum[kCT / 32];
   __shared__ long long excl_s, total_s;
-  __shared__ int64_t stage[kTile];
   if (threadIdx.x == 0) tile_s = atomicAdd(tile_counter, 1u);
   __syncthreads();
   const int64_t tile = tile_s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t first = tile * kTile + (int64_t)threadIdx.x * kIPT;
+  const int64_t first = tile * kFTile + (int64_t)threadIdx.x * kFIPT;
   unsigned bits = 0;
-  if (first + kIPT <= N) {
-    const uint4 f4 = *reinterpret_cast<const uint4*>(flag + first);
-    const unsigned w4[4] = {f4.x, f4.y, f4.z, f4.w};
+  if (first + kFIPT <= N) {
+    const uint4* f = reinterpret_cast<const uint4*>(flag + first);
+    const uint4 a = __ldcs(f), b = __ldcs(f + 1);
+    const unsigned w8[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int j = 0; j < kIPT; ++j) bits |= ((w4[j >> 2] >> (8 * (j & 3))) & 1u) << j;
+    for (int j = 0; j < kFIPT; ++j) bits |= ((w8[j >> 2] >> (8 * (j & 3))) & 1u) << j;
   } else {
-    for (int j = 0; j < kIPT; ++j)
+    for (int j = 0; j < kFIPT; ++j)
       if (first + j < N) bits |= (unsigned)(flag[first + j] & 1) << j;
   }
   // near points: the exact distance against rho, the source list where dist <= rho
-#pragma unroll
-  for (int j = 0; j < kIPT; ++j) {
+  const int64_t lim = N - first;
+  unsigned near = ~bits & (lim >= kFIPT ? 0xffffffffu : ((1u << (lim > 0 ? lim : 0)) - 1u));
+  while (near) {
+    const int j = __ffs(near) - 1;
+    near &= near - 1;
     const int64_t i = first + j;
-    if (i < N && !((bits >> j) & 1u)) {
-      const double v = dist[i];
-      bool f = v >= cutoff;
-      if (f && v <= rho) f = !is_source(src_local, n_src, i);
-      bits |= (unsigned)f << j;
-    }
+    const double v = dist[i];
+    bool f = v >= cutoff;
+    if (f && v <= rho) f = !is_source(src_local, n_src, i);
+    bits |= (unsigned)f << j;
   }
   // block exclusive scan of the per-thread counts
   const int cnt = __popc(bits);
@@ -416,9 +426,12 @@ __global__ void __launch_bounds__(kCT) k_compact_flag(const unsigned char* __res
   }
   // stage this tile's targets in index order, then one coalesced store
   int k = my_off;
-#pragma unroll
-  for (int j = 0; j < kIPT; ++j)
-    if ((bits >> j) & 1u) stage[k++] = first + j;
+  unsigned bb = bits;
+  while (bb) {
+    const int j = __ffs(bb) - 1;
+    bb &= bb - 1;
+    stage[k++] = first + j;
+  }
   __syncthreads();
   const long long excl = excl_s;
   for (int e = threadIdx.x; e < (int)total; e += kCT) __stcs(out + excl + e, stage[e]);
@@ -505,7 +518,9 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   // sample size and the sample quantile used as the threshold: the k_s-th smallest of S strided
   // sample distances lets about k_s N / S points through (2.5 n + 4 N / S, a few hundred to a few
   // thousand candidates); fewer than n (rare) or more than kSelMax take the general path
-  const int64_t S = std::min<int64_t>(N, std::max<int64_t>(16384, std::min<int64_t>(kSampleMax, N / 64)));
+  // S ~ N / 64 up to 2^20 samples (kRun-point runs): about 2.5 n + 4 N / S candidates must stay
+  // below kSelMax for the one-CTA selection (at N = 1e8, m = 512: ~1700)
+  const int64_t S = N <= 16384 ? N : ceil_to64(std::min<int64_t>(N, std::max<int64_t>(16384, std::min<int64_t>(kSampleBig, N / 64))));
   const int64_t ks = S == N ? nl : std::min<int64_t>(S, (int64_t)std::ceil(2.5 * (double)nl * (double)S / (double)N) + 4);
   const int64_t cap = std::min<int64_t>(kSelMax, N);
   if (ensure(c, (void**)&c->dist, &c->dist_cap, sizeof(double) * N)) return KID_E_OOM;
@@ -536,7 +551,8 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   if (ensure(c, &c->sort_tmp, &c->sort_tmp_cap, tmpb)) return KID_E_OOM;
   KID_CK(c, cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmpb, skeys, skeys2, (int)S, 0, 32, c->stream));
   c->launches += 4;
-  if (ensure(c, (void**)&c->flag, &c->flag_cap, (size_t)ntiles * kTile)) return KID_E_OOM;
+  const int64_t ftiles = (N + kFTile - 1) / kFTile;
+  if (ensure(c, (void**)&c->flag, &c->flag_cap, (size_t)ftiles * kFTile)) return KID_E_OOM;
   unsigned char* flag = c->flag;
   prof_begin(c);
   k_dist_flag<<<c->sms * 8, 256, 0, c->stream>>>(c->pts, N, d, center, skeys2 + (ks - 1), xi, flag, c->dist, ck, ci,
@@ -548,8 +564,9 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   k_split_select<<<1, kSelT, sel_smem, c->stream>>>(ck, ci, count, cap, (int)nl, c->pts, N, d, src_local, c->src, ctrl);
   KID_LAUNCHED(c);
   prof_begin(c);
-  k_compact_flag<<<(unsigned)ntiles, kCT, 0, c->stream>>>(flag, c->dist, N, src_local, nl, c->tgt_idx, status,
-                                                          (unsigned int*)c->counter, c->counter + 1, ntiles, ctrl, xi);
+  cudaFuncSetAttribute(k_compact_flag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int64_t) * kFTile));
+  k_compact_flag<<<(unsigned)ftiles, kCT, sizeof(int64_t) * kFTile, c->stream>>>(
+      flag, c->dist, N, src_local, nl, c->tgt_idx, status, (unsigned int*)c->counter, c->counter + 1, ftiles, ctrl, xi);
   prof_end(c);
   KID_LAUNCHED(c);
   // one D2H of [rho, overflow | nt | source indices | source coordinates] and one synchronisation
