@@ -301,15 +301,16 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
         next_row = row_of(it + 4);
       }
       const double* slot = ring + (size_t)(it % kFRing) * d * kTM;
-      // rows past the end of the target list get the far sentinel: their K entries are exactly 0
+      // rows past the end of the target list sit at -far (padding sources at +far): every K entry of
+      // such a row is exactly 0, the padding source columns included ((2 far)^2 d stays finite)
       const bool valid = trow(it) >= 0;
       if constexpr (D > 0 && D <= 8) {
 #pragma unroll
-        for (int k = 0; k < DR; ++k) tc[k] = valid ? slot[k * kTM + lane] * A.cscale : kFar;
+        for (int k = 0; k < DR; ++k) tc[k] = valid ? slot[k * kTM + lane] * A.cscale : -kFar;
       }
       auto coord = [&](int k) -> double {
         if constexpr (D > 0 && D <= 8) return tc[k];
-        else return valid ? slot[k * kTM + lane] * A.cscale : kFar;
+        else return valid ? slot[k * kTM + lane] * A.cscale : -kFar;
       };
       // four source columns at s_src[jc ..] -> out[(col) * kST + lane]; ||K||^2 when counted
       auto eval4 = [&](int jc, double* out, bool count) {
