@@ -69,6 +69,10 @@ int kid_set_path(kid_ctx* ctx, int32_t path);
 /* Name of the dominant kernel the last pass launched ("k_gram", "k_fused", "k_sumsq", ...): the
    bench labels its roofline line with the kernel that actually ran. */
 const char* kid_last_kernel(const kid_ctx* ctx);
+/* Tuning options of the cluster kernel (no effect on results): KID_OPT_EVAL_WARPS = 0 (auto), 8 or 12
+   eval warps of 16 per CTA (the rest run the DMMA contractions). */
+#define KID_OPT_EVAL_WARPS 1
+int kid_set_option(kid_ctx* ctx, int32_t key, int64_t value);
 
 /* ---- point set (PointSet, kernel.hpp:14): N x d column-major ----
  * index_offset: global index of local row 0 when the point set is sharded across ranks. */

@@ -38,7 +38,7 @@ SYMBOLS = ["kid_abi_version", "kid_host_alloc", "kid_host_free", "kid_create", "
            "kid_get_targets", "kid_set_block", "kid_block_shape", "kid_row_norms", "kid_row_norms_dev", "kid_gram",
            "kid_gram_dev", "kid_leverage", "kid_leverage_dev", "kid_recon_error", "kid_recon_prepare",
            "kid_recon_error_dev", "kid_eval_rows", "kid_apply_skeleton", "kid_apply_skeleton_dev", "kid_select_rows",
-           "kid_launch_count", "kid_profile", "kid_profile_read", "kid_exp_check", "kid_set_path", "kid_last_kernel"]
+           "kid_launch_count", "kid_profile", "kid_profile_read", "kid_exp_check", "kid_set_path", "kid_last_kernel", "kid_set_option"]
 
 
 def cuda_lib():
@@ -64,6 +64,7 @@ def cuda_lib():
         L.kid_synchronize.argtypes = [vp]
         L.kid_set_path.argtypes = [vp, i32]
         L.kid_last_kernel.argtypes = [vp]
+        L.kid_set_option.argtypes = [vp, i32, i64]
         L.kid_last_kernel.restype = C.c_char_p
         L.kid_set_points.argtypes = [vp, vp, i64, i32, i64]
         L.kid_set_points_device.argtypes = [vp, vp, i64, i32, i64]
@@ -185,6 +186,10 @@ class Device:
     def set_path(self, path: int):
         """KID_PATH_AUTO (0) or KID_PATH_CLUSTER (1): force the 2-CTA cluster kernel (kid_set_path)."""
         self._ck(cuda_lib().kid_set_path(self.h, int(path)), "kid_set_path")
+
+    def set_option(self, key: int, value: int):
+        """kid_set_option: KID_OPT_EVAL_WARPS (1) = 0 (auto), 8 or 12."""
+        self._ck(cuda_lib().kid_set_option(self.h, int(key), int(value)), "kid_set_option")
 
     def last_kernel(self) -> str:
         return cuda_lib().kid_last_kernel(self.h).decode()

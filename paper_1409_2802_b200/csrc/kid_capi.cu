@@ -154,6 +154,16 @@ int kid_set_stream(kid_ctx* c, void* s) {
 
 const char* kid_last_kernel(const kid_ctx* c) { return c ? c->last_kernel : ""; }
 
+int kid_set_option(kid_ctx* c, int32_t key, int64_t value) {
+  if (!c) return KID_E_ERROR;
+  if (key == KID_OPT_EVAL_WARPS) {
+    if (value != 0 && value != 8 && value != 12) return fail(c, KID_E_RANGE, "kid_set_option: eval warps must be 0, 8 or 12");
+    c->eval_warps = (int)value;
+    return KID_OK;
+  }
+  return fail(c, KID_E_RANGE, "kid_set_option: unknown option");
+}
+
 int kid_set_path(kid_ctx* c, int32_t path) {
   if (!c) return KID_E_ERROR;
   if (path != KID_PATH_AUTO && path != KID_PATH_CLUSTER) return fail(c, KID_E_RANGE, "kid_set_path: unknown path");
