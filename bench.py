@@ -254,6 +254,8 @@ def measure_pass(wl_name, args, torch, ws, rank, local, steps, warmup, e2e_steps
     dev, prob = setup(wl, ws, rank, local, torch)
     if getattr(args, "eval_warps", 0):
         dev.set_option(1, args.eval_warps)
+    if getattr(args, "chunk_cols", 0):
+        dev.set_option(2, args.chunk_cols)
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
     m, r = wl["m"], prob.r
@@ -748,6 +750,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=0, help="reference rows per step (0: 5e6 / m)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eval-warps", type=int, default=0, help="cluster kernel eval warps (0 auto, 8, 12)")
+    ap.add_argument("--chunk-cols", type=int, default=0, help="cluster kernel K_A chunk width (0 auto, 32-96)")
     ap.add_argument("--svd-proj", action="store_true", help="--pass svd through kid_proj_gram (C = V_perp) instead of the ID route")
     ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms", "gram", "leverage"])
     args = ap.parse_args()

@@ -161,6 +161,12 @@ int kid_set_option(kid_ctx* c, int32_t key, int64_t value) {
     c->eval_warps = (int)value;
     return KID_OK;
   }
+  if (key == KID_OPT_CHUNK_COLS) {
+    if (value != 0 && value != 32 && value != 48 && value != 64 && value != 96)
+      return fail(c, KID_E_RANGE, "kid_set_option: chunk columns must be 0, 32, 48, 64 or 96");
+    c->chunk_cols = (int)value;
+    return KID_OK;
+  }
   return fail(c, KID_E_RANGE, "kid_set_option: unknown option");
 }
 

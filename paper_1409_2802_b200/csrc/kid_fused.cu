@@ -826,7 +826,8 @@ int fused_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, dou
   };
   const size_t kMaxSmem = 227 * 1024 - 6144;  // minus the static arrays
   // chunk width: CW / 4 four-column groups per chunk spread over the NE eval warps (two each when it fits)
-  const int cw_try[2] = {NE == 12 ? 96 : 64, NE == 12 ? 48 : 32};
+  int cw_try[2] = {NE == 12 ? 96 : 32, NE == 12 ? 48 : 32};
+  if (c->chunk_cols) cw_try[0] = c->chunk_cols;
   for (int msm = (has_A ? 1 : 0); msm >= 0 && !S; --msm)
     for (int cw : cw_try) {
       for (int st : {2, 1}) {

@@ -314,6 +314,9 @@ RightFactor right_factor(const Matrix& A) {
   return rf;
 }
 
+// relative singular values the Gram route (sqrt of the eigenvalues of K^T K) resolves: ~sqrt(u) plus margin
+constexpr double kGramResolvable = 1e-7;
+
 std::vector<double> KernelBlock::singular_values() const {
   const int64_t m = cols();
   if (m <= 128) return right_factor().singular_values;
@@ -695,6 +698,10 @@ LeverageScores row_leverage_scores(const KernelBlock& K, int64_t r) {
   sv.resize(static_cast<size_t>(m), 0.0);
   if (!(sv[static_cast<size_t>(r - 1)] > 0.0))
     throw NumericalError("row_leverage_scores: sigma_r vanishes; scores undefined");
+  if (m > 128 && sv[static_cast<size_t>(r - 1)] < kGramResolvable * sv[0])  // Gram-route V_r, Sigma_r
+    throw IllConditionedSkeletonError("row_leverage_scores: sigma_r / sigma_1 = " +
+                                      std::to_string(sv[static_cast<size_t>(r - 1)] / sv[0]) +
+                                      " is below the resolution of the Gram route for m > 128");
   Matrix W(m, r);  // lowrank.hpp:304
   for (int64_t j = 0; j < r; ++j)
     for (int64_t i = 0; i < m; ++i) W(i, j) = V(i, j) * (1.0 / sv[static_cast<size_t>(j)]);
@@ -1285,6 +1292,13 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
         const bool auto_rank = scheme.kind == SchemeKind::Leverage && cfg.scheme_rank_auto[scheme_idx];
         const bool need_full = cfg.rank_reference_full || cfg.emit_bound_sampling || auto_rank;
         if (need_full) full_sv = K->singular_values();  // harness.hpp:176-184 (device TSQR)
+        // m > 128 takes the spectrum from the Gram K^T K: sigma_i below ~sqrt(u) sigma_1 are rounding noise
+        // there, so an eps-rank of the full spectrum finer than kGramResolvable is refused rather than
+        // returned wrong (the reference resolves it by QR + BDCSVD, lowrank.hpp:56-77)
+        if (auto_rank && K->cols() > 128 && rule.eps && *rule.eps < kGramResolvable)
+          throw IllConditionedSkeletonError("auto-rank leverage: eps = " + std::to_string(*rule.eps) +
+                                            " is below the resolution of the Gram-route spectrum for m > 128 (" +
+                                            std::to_string(kGramResolvable) + ")");
         if (cfg.rank_reference_full) rule.reference_sigma1 = (*full_sv)[0];
         if (auto_rank) scheme.rank_for_leverage = std::max<int64_t>(1, rule.resolve(*full_sv));
       }
