@@ -167,6 +167,11 @@ int kid_set_option(kid_ctx* c, int32_t key, int64_t value) {
     c->chunk_cols = (int)value;
     return KID_OK;
   }
+  if (key == KID_OPT_KERNEL) {
+    if (value < 0 || value > 2) return fail(c, KID_E_RANGE, "kid_set_option: kernel must be 0, 1 or 2");
+    c->kernel_choice = (int)value;
+    return KID_OK;
+  }
   return fail(c, KID_E_RANGE, "kid_set_option: unknown option");
 }
 

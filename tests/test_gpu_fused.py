@@ -78,9 +78,43 @@ def test_cluster_gram(oracle, cluster, d, n):
 
 @pytest.mark.parametrize("d,n,eps", [(2, 100, 1e-2), (2, 100, 1e-8), (3, 100, 1e-4), (8, 64, 1e-2),
                                      (16, 48, 1e-6), (5, 90, 1e-12), (7, 30, 1e-3)])
-def test_cluster_residual(oracle, cluster, d, n, eps):
+@pytest.mark.parametrize("kern", [1, 2])
+def test_cluster_residual(oracle, cluster, d, n, eps, kern):
+    """kern 1: the warp-specialised k_fused; 2: the warp-tile k_fused_w where n - r <= 32 (else k_fused)."""
     t, K = _block(oracle, d, 20_000, n)
-    _check_resid(oracle, cluster, t, K, n, eps)
+    cluster.set_option(3, kern)
+    try:
+        _check_resid(oracle, cluster, t, K, n, eps)
+    finally:
+        cluster.set_option(3, 0)
+
+
+@pytest.mark.parametrize("d,n,r", [(8, 100, 80), (3, 64, 60), (16, 48, 17), (5, 40, 39), (2, 200, 190)])
+def test_warp_tile_kernel(oracle, dev, d, n, r):
+    """k_fused_w (n - r <= 32 D columns: 1 to 4 column blocks, ragged tiles) against the oracle, and the same
+    Grams from k_fused within the rounding ladder; bitwise reproducible run to run."""
+    t, K = _block(oracle, d, 15_000, n)
+    dev.set_points(t.points)
+    dev.split(t.center, n, 2.0)
+    res = oracle.compress_id(K, np.arange(0, K.shape[0], 7), fixed_r=r)
+    _, _, r_DtD, _ = oracle.residual_stats(K, res.skeleton, res.P)
+    bound, _, _ = _resid_bound(K, res, r_DtD)
+    out = {}
+    try:
+        for kern in (2, 1):
+            dev.set_path(1)
+            dev.set_option(3, kern)
+            out[kern] = dev.recon_error(t.h, res.skeleton, res.P)
+            if kern == 2:
+                assert dev.last_kernel() == "k_fused_w"
+                again = dev.recon_error(t.h, res.skeleton, res.P)
+                assert np.array_equal(again[2], out[2][2]) and again[0] == out[2][0]
+    finally:
+        dev.set_option(3, 0)
+        dev.set_path(0)
+    for kern in (1, 2):
+        assert np.all(np.abs(out[kern][2] - r_DtD) <= bound + 1e-300)
+        assert out[kern][1] == pytest.approx(float(np.sum(K * K)), rel=1e-12)
 
 
 def test_cluster_residual_rank_one_and_full(oracle, cluster):
