@@ -1332,7 +1332,7 @@ int fused_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, dou
   };
   const size_t kMaxSmem = 227 * 1024 - 6144;  // minus the static arrays
   // chunk width: CW / 4 four-column groups per chunk spread over the NE eval warps (two each when it fits)
-  int cw_try[2] = {NE == 12 ? 96 : 32, NE == 12 ? 48 : 32};
+  int cw_try[2] = {NE == 12 ? 64 : 48, 32};  // measured best: c5 (12 eval warps) 64, c4-d16 (8) 48
   if (c->chunk_cols) cw_try[0] = c->chunk_cols;
   for (int msm = (has_A ? 1 : 0); msm >= 0 && !S; --msm)
     for (int cw : cw_try) {
