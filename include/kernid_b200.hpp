@@ -14,6 +14,8 @@
 //     epsilon-rank, weighted draws.
 #pragma once
 #include <cstdint>
+#include <functional>
+#include <memory>
 #include <optional>
 #include <ostream>
 #include <random>
@@ -305,5 +307,60 @@ struct BandwidthResult {
 BandwidthResult bandwidth_search(Device& dev, const ExperimentConfig& cfg, const BandwidthSearchSpec& spec,
                                  std::uint64_t data_seed);
 std::string format_double(double v);
+
+
+// ------------------------------------------------------------- multi-GPU (kernid_multi.cpp)
+// One process, G GPUs: a context per GPU, a host thread per GPU for each pass, NCCL for the Gram
+// reductions (ncclCommInitAll; a group listing a device twice -- single-GPU tests -- sums on the host).
+class DeviceGroup {
+ public:
+  explicit DeviceGroup(const std::vector<int>& devices);
+  ~DeviceGroup();
+  DeviceGroup(const DeviceGroup&) = delete;
+  DeviceGroup& operator=(const DeviceGroup&) = delete;
+  int size() const { return static_cast<int>(devs_.size()); }
+  Device& dev(int g) const { return *devs_[static_cast<size_t>(g)]; }
+  bool uses_nccl() const { return !comms_.empty(); }
+  // sum of the per-GPU device buffers (count doubles each), read back to the host
+  std::vector<double> allreduce_to_host(const std::vector<double*>& dbufs, size_t count);
+
+ private:
+  std::vector<int> ids_;
+  std::vector<std::unique_ptr<Device>> devs_;
+  std::vector<struct ncclComm*> comms_;
+};
+
+struct ShardedSplit {
+  SourceTargetSplit global;      // identical to the single-GPU split
+  std::vector<int64_t> offsets;  // G + 1 point-index boundaries of the shards
+  std::vector<int64_t> nt;       // targets per shard (concatenated in GPU order = global order)
+};
+ShardedSplit split_sources_targets(DeviceGroup& grp, const PointSet& ps, const std::vector<double>& x_c, int64_t n,
+                                   double xi);
+
+// K(T, S) with the targets sharded over the group (the multi-GPU KernelBlock)
+class ShardedBlock {
+ public:
+  ShardedBlock(DeviceGroup& grp, KernelSpec spec, const PointSet& points, const ShardedSplit& split);
+  int64_t rows() const { return static_cast<int64_t>(split_->global.target_indices.size()); }
+  int64_t cols() const { return static_cast<int64_t>(split_->global.source_indices.size()); }
+  const KernelSpec& spec() const { return spec_; }
+  DeviceGroup& group() const { return *grp_; }
+  Matrix rows_exact(const std::vector<int64_t>& idx) const;
+  std::vector<double> row_norms() const;       // global target order
+  Matrix gram(double* sumsq = nullptr) const;  // K^T K, NCCL-reduced
+  double spectral_norm() const;
+  // [sum_0, sum_1, G (k x k)] of `pass` (writing 2 + k^2 doubles into a device buffer) over all shards
+  std::vector<double> reduced_pass(int64_t k, const std::function<void(int, double*)>& pass) const;
+
+ private:
+  DeviceGroup* grp_;
+  KernelSpec spec_;
+  const PointSet* points_;
+  const ShardedSplit* split_;
+};
+RowSample sample_rows_euclidean(const ShardedBlock& K, double s, std::uint64_t seed);
+std::pair<IDFactorization, CompressionReport> compress_id(const ShardedBlock& K, const RowSample& sample,
+                                                          const RankRule& rule, const CompressOptions& opts = {});
 
 }  // namespace kernid_b200

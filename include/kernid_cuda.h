@@ -75,6 +75,13 @@ const char* kid_last_kernel(const kid_ctx* ctx);
 #define KID_OPT_CHUNK_COLS 2 /* K_A chunk width: 0 (auto), 32, 48, 64, 96 */
 #define KID_OPT_KERNEL 3     /* 0 auto, 1 the warp-specialised k_fused, 2 the warp-tile k_fused_w (n <= 32) */
 int kid_set_option(kid_ctx* ctx, int32_t key, int64_t value);
+/* Plumbing for a multi-GPU host (kernid_b200::DeviceGroup): the context's device, its stream, device
+   buffers on it and a synchronous read-back. */
+int32_t kid_device_id(const kid_ctx* ctx);
+void* kid_stream(kid_ctx* ctx);
+void* kid_device_alloc(kid_ctx* ctx, size_t bytes);
+void kid_device_free(kid_ctx* ctx, void* p);
+int kid_memcpy_dtoh(kid_ctx* ctx, void* dst, const void* src, size_t bytes);
 
 /* ---- point set (PointSet, kernel.hpp:14): N x d column-major ----
  * index_offset: global index of local row 0 when the point set is sharded across ranks. */

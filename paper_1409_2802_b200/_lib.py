@@ -38,7 +38,8 @@ SYMBOLS = ["kid_abi_version", "kid_host_alloc", "kid_host_free", "kid_create", "
            "kid_get_targets", "kid_set_block", "kid_block_shape", "kid_row_norms", "kid_row_norms_dev", "kid_gram",
            "kid_gram_dev", "kid_leverage", "kid_leverage_dev", "kid_recon_error", "kid_recon_prepare",
            "kid_recon_error_dev", "kid_eval_rows", "kid_apply_skeleton", "kid_apply_skeleton_dev", "kid_select_rows",
-           "kid_launch_count", "kid_profile", "kid_profile_read", "kid_exp_check", "kid_set_path", "kid_last_kernel", "kid_set_option"]
+           "kid_launch_count", "kid_profile", "kid_profile_read", "kid_exp_check", "kid_set_path", "kid_last_kernel", "kid_set_option",
+           "kid_device_id", "kid_stream", "kid_device_alloc", "kid_device_free", "kid_memcpy_dtoh"]
 
 
 def cuda_lib():

@@ -17,7 +17,7 @@ HOST_SO = os.path.join(PKG, "libkernid_host.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SRCS = ["kid_capi.cu", "kid_split.cu", "kid_passes.cu", "kid_next.cu", "kid_fused.cu"]
-HOST_SRCS = ["kernid_host.cpp"]
+HOST_SRCS = ["kernid_host.cpp", "kernid_multi.cpp"]
 
 
 def _stale(target, deps):
@@ -48,7 +48,8 @@ def build_host(force=False, verbose=False):
         return HOST_SO
     cmd = ["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-ffp-contract=off", "-Wall",
            "-I", os.path.join(ROOT, "include"), "-o", HOST_SO] + [os.path.join(HOST, f) for f in HOST_SRCS] + \
-          ["-L", PKG, "-lkernid_cuda", "-Wl,-rpath,$ORIGIN", "-ldl", "-lpthread"]
+          ["-I", "/usr/local/cuda/include", "-L", PKG, "-lkernid_cuda", "-Wl,-rpath,$ORIGIN",
+           "-L/usr/lib/x86_64-linux-gnu", "-l:libnccl.so.2", "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

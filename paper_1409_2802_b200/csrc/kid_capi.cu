@@ -154,6 +154,34 @@ int kid_set_stream(kid_ctx* c, void* s) {
 
 const char* kid_last_kernel(const kid_ctx* c) { return c ? c->last_kernel : ""; }
 
+int32_t kid_device_id(const kid_ctx* c) { return c ? c->device : -1; }
+
+void* kid_stream(kid_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+void* kid_device_alloc(kid_ctx* c, size_t bytes) {
+  if (!c || set_device(c)) return nullptr;
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes ? bytes : 8) != cudaSuccess) {
+    cuda_fail(c, cudaGetLastError(), "kid_device_alloc");
+    return nullptr;
+  }
+  return p;
+}
+
+void kid_device_free(kid_ctx* c, void* p) {
+  if (!c || !p) return;
+  set_device(c);
+  cudaFree(p);
+}
+
+int kid_memcpy_dtoh(kid_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!c || (bytes && (!dst || !src))) return KID_E_ERROR;
+  if (int rc = set_device(c)) return rc;
+  KID_CK(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  KID_CK(c, cudaStreamSynchronize(c->stream));
+  return KID_OK;
+}
+
 int kid_set_option(kid_ctx* c, int32_t key, int64_t value) {
   if (!c) return KID_E_ERROR;
   if (key == KID_OPT_EVAL_WARPS) {

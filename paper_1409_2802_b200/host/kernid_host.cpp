@@ -1734,6 +1734,34 @@ int kidh_compress_trial(int32_t device, int32_t d, int64_t N, int64_t n, double 
   });
 }
 
+// kidh_compress_trial with the targets sharded over `G` devices (EuclideanNorm sampling): the
+// multi-GPU mirror (DeviceGroup, ShardedBlock; NCCL reductions when the devices are distinct).
+int kidh_sharded_compress_trial(const int32_t* devices, int32_t G, int32_t d, int64_t N, int64_t n, double xi,
+                                double h_value, uint64_t data_seed, double s, uint64_t sample_seed, double eps,
+                                int64_t* n_targets, int64_t* rank, double* rel_error, double* rel_error_fro,
+                                int64_t* skel_out, int64_t* sample_out, int64_t* sample_count_out, int32_t* used_nccl) {
+  return guard([&] {
+    DeviceGroup grp(std::vector<int>(devices, devices + G));
+    const PointSet points = gen_normal(d, N, derive_seed(data_seed, 0xDA7A));
+    Rng crng(derive_seed(data_seed, 0xCE));
+    const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(N)));
+    std::vector<double> center(static_cast<size_t>(d));
+    for (int k = 0; k < d; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+    const ShardedSplit split = split_sources_targets(grp, points, center, n, xi);
+    const ShardedBlock K(grp, KernelSpec::gaussian(h_value * silverman_bandwidth(d, N)), points, split);
+    *n_targets = K.rows();
+    const RowSample sample = sample_rows_euclidean(K, s, sample_seed);
+    std::memcpy(sample_out, sample.indices.data(), sizeof(int64_t) * sample.indices.size());
+    *sample_count_out = static_cast<int64_t>(sample.indices.size());
+    auto [id, rep] = compress_id(K, sample, RankRule::from_eps(eps));
+    *rank = rep.rank;
+    *rel_error = rep.rel_error;
+    *rel_error_fro = rep.rel_error_fro;
+    std::memcpy(skel_out, id.skeleton.data(), sizeof(int64_t) * id.skeleton.size());
+    *used_nccl = grp.uses_nccl() ? 1 : 0;
+  });
+}
+
 // One compress trial (as kidh_compress_trial, uniform sampling) followed by the 8(f) passes on
 // its ID: mc_error (n_mc estimates) and apply_skeleton with charges q (m) -> u (n_targets).
 int kidh_trial_next_rows(int32_t device, int32_t d, int64_t N, int64_t n, double xi, double h_value,

@@ -48,6 +48,8 @@ def host_lib():
         L.kidh_error_pass.argtypes = [C.c_void_p, dbl, _ip, i64, _dp, dbl, P(dbl), P(dbl), P(dbl)]
         L.kidh_trial_next_rows.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, dbl, i32, u64, _dp,
                                            P(i64), P(i64), _ip, _dp, _dp, _dp, i64]
+        L.kidh_sharded_compress_trial.argtypes = [C.c_void_p, i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl,
+                                                  P(i64), P(i64), P(dbl), P(dbl), _ip, _ip, P(i64), P(i32)]
         L.kidh_compress_trial.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, i32, i64, dbl, u64, dbl, P(i64), P(i64),
                                           P(dbl), P(dbl), _ip, _ip, P(i64)]
         L.kidh_trial_svd.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, P(i64), P(dbl), P(dbl), _dp]
@@ -194,6 +196,21 @@ def compress_trial(d, N, n, xi, data_seed, scheme, s, sample_seed, eps, h_value=
                                        C.byref(nt), C.byref(rank), C.byref(rel), C.byref(relf), skel, sample,
                                        C.byref(cnt)), "compress_trial")
     return TrialResult(nt.value, rank.value, rel.value, relf.value, skel[: rank.value].copy(), sample[: cnt.value].copy())
+
+
+def sharded_compress_trial(devices, d, N, n, xi, data_seed, s, sample_seed, eps, h_value=1.0):
+    """compress_trial (EuclideanNorm) with the targets sharded over `devices` by the C++ multi-GPU mirror
+    (DeviceGroup / ShardedBlock, NCCL reductions for distinct devices). Returns (TrialResult, used_nccl)."""
+    dv = np.ascontiguousarray(devices, dtype=np.int32)
+    nt, rank, cnt, nccl = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+    rel, fro = C.c_double(), C.c_double()
+    skel = np.zeros(n, np.int64)
+    smp = np.zeros(max(N, 1), np.int64)
+    _ck(host_lib().kidh_sharded_compress_trial(dv.ctypes.data, dv.size, d, N, n, xi, h_value, data_seed, s, sample_seed,
+                                               eps, C.byref(nt), C.byref(rank), C.byref(rel), C.byref(fro), skel, smp,
+                                               C.byref(cnt), C.byref(nccl)), "sharded_compress_trial")
+    return TrialResult(nt.value, rank.value, rel.value, fro.value, skel[: rank.value].copy(),
+                       smp[: cnt.value].copy()), bool(nccl.value)
 
 
 def trial_next_rows(d, N, n, xi, data_seed, s, sample_seed, eps, s_mc, n_mc, mc_seed, q, h_value=1.0, device=0):
