@@ -317,7 +317,8 @@ def measure_pass(wl_name, args, torch, ws, rank, local, steps, warmup, e2e_steps
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(wl_name)
+            t = json.load(f).get(wl_name)
+        traffic = t["dram_bytes_per_launch"] if isinstance(t, dict) else t
     res = {"value": value, "ms_per_step": ms_max / steps, "entries_per_step": total_entries, "rank_r": r,
            "nt": prob.nt, "h": prob.h, "kernel": kernel, "kernel_ms": kavg, "fpe": fpe, "achieved": achieved,
            "peak": peak, "frac": frac, "traffic": traffic, "launches": launches, "clocks": clk,
