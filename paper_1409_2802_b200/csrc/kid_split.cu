@@ -437,50 +437,57 @@ __global__ void __launch_bounds__(kCT) k_compact_flag(const unsigned char* __res
   for (int e = threadIdx.x; e < (int)total; e += kCT) __stcs(out + excl + e, stage[e]);
 }
 
-// Device-side selection of the n sources (single CTA; the candidate count is read on the device):
-// each candidate's rank under (dist, idx) -- nth_element's comparator (geometry.hpp:40-47) -- by
-// counting over the <= kSelMax candidates in shared memory (warp-uniform broadcast reads, no
-// sorting network, three barriers); the n of rank < n are placed by rank, rho = the largest
-// (geometry.hpp:52-53), then placed again by their rank in index order (geometry.hpp:50-51) and
-// the source coordinates gathered. ctrl = [rho, fallback flag (overflow or fewer than n)].
-constexpr int kSelMax = 4096, kSelT = 1024;
-__global__ void __launch_bounds__(kSelT) k_split_select(const unsigned long long* __restrict__ ck,
-                                                       const unsigned long long* __restrict__ ci,
-                                                       const unsigned long long* __restrict__ count, int64_t cap,
-                                                       int nl, const double* __restrict__ pts, int64_t N, int d,
-                                                       int64_t* __restrict__ src_local, double* __restrict__ src,
-                                                       double* __restrict__ ctrl) {
-  extern __shared__ unsigned long long sel_sm[];  // key | idx (kSelMax each) | sel_key | sel_idx (kSelT each)
-  unsigned long long* key = sel_sm;
+// Device-side selection of the n sources, in two launches (the candidate count is read on the
+// device): k_split_rank -- kSelCtas CTAs each stage all <= kSelMax candidates in shared memory and
+// rank their share under (dist, idx), nth_element's comparator (geometry.hpp:40-47), by counting
+// (warp-uniform broadcast reads, no sorting network); the n of rank < n land at sel[rank]. Then
+// k_split_place (one CTA): rho = the largest of the n (geometry.hpp:52-53), the n re-ranked by index
+// (geometry.hpp:50-51), the source coordinates gathered. ctrl = [rho, fallback flag (overflow or
+// fewer than n candidates)].
+constexpr int kSelMax = 4096, kSelT = 1024, kSelCtas = 16, kRankT = 256;
+__global__ void __launch_bounds__(kRankT) k_split_rank(const unsigned long long* __restrict__ ck,
+                                                      const unsigned long long* __restrict__ ci,
+                                                      const unsigned long long* __restrict__ count, int64_t cap,
+                                                      int nl, unsigned long long* __restrict__ sel,
+                                                      double* __restrict__ ctrl) {
+  extern __shared__ unsigned long long rk_sm[];  // key | idx (kSelMax each)
+  unsigned long long* key = rk_sm;
   unsigned long long* idx = key + kSelMax;
-  unsigned long long* sel_key = idx + kSelMax;
-  unsigned long long* sel_idx = sel_key + kSelT;
   const unsigned long long total = *count;
   const unsigned long long lim = (unsigned long long)(cap < kSelMax ? cap : kSelMax);
   const bool bad = total > lim || total < (unsigned long long)nl;
-  if (threadIdx.x == 0) ctrl[1] = bad ? 1.0 : 0.0;
-  if (bad) return;  // uniform over the CTA
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctrl[1] = bad ? 1.0 : 0.0;
+  if (bad) return;  // uniform over the grid
   const int cnt = (int)total;
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
     key[i] = ck[i];
     idx[i] = ci[i];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const unsigned long long ki = key[i], ii = idx[i];
     int rank = 0;
     for (int j = 0; j < cnt; ++j) rank += (key[j] < ki) || (key[j] == ki && idx[j] < ii);
     if (rank < nl) {
-      sel_key[rank] = ki;
-      sel_idx[rank] = ii;
+      sel[rank] = ki;
+      sel[kSelT + rank] = ii;
     }
   }
+}
+
+__global__ void __launch_bounds__(kSelT) k_split_place(const unsigned long long* __restrict__ sel, int nl,
+                                                      const double* __restrict__ pts, int64_t N, int d,
+                                                      int64_t* __restrict__ src_local, double* __restrict__ src,
+                                                      double* __restrict__ ctrl) {
+  __shared__ unsigned long long s_idx[kSelT];
+  if (ctrl[1] != 0.0) return;
+  for (int i = threadIdx.x; i < nl; i += blockDim.x) s_idx[i] = sel[kSelT + i];
   __syncthreads();
-  if (threadIdx.x == 0) ctrl[0] = __longlong_as_double((long long)sel_key[nl - 1]);  // rho: the largest of the n
+  if (threadIdx.x == 0) ctrl[0] = __longlong_as_double((long long)sel[nl - 1]);  // rho: the largest of the n
   for (int i = threadIdx.x; i < nl; i += blockDim.x) {
-    const unsigned long long ii = sel_idx[i];
+    const unsigned long long ii = s_idx[i];
     int rank = 0;
-    for (int j = 0; j < nl; ++j) rank += sel_idx[j] < ii;
+    for (int j = 0; j < nl; ++j) rank += s_idx[j] < ii;
     const int64_t li = (int64_t)ii;
     src_local[rank] = li;
     for (int k = 0; k < d; ++k) src[rank + (int64_t)k * nl] = pts[li + k * N];
@@ -506,7 +513,7 @@ int sort_candidates(kid_ctx* c, unsigned long long* key, unsigned long long* idx
 }  // namespace
 
 // Single-rank split with one host synchronisation (kid_split): sample threshold, distances and
-// candidates, device-side selection (k_split_select), compaction with rho read on the device.
+// candidates, device-side selection (k_split_rank + k_split_place), compaction with rho read on the device.
 // Returns 1 (not taken: fall back to split_candidates / split_finish) when the candidate buffer
 // would exceed one CTA's sort or overflowed.
 int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64_t* src_idx_out, double* rho_out,
@@ -529,7 +536,8 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   const int64_t ntiles = (N + kTile - 1) / kTile;
   // scratch: center | ctrl | count | tile status | sample keys (2x) | candidates | src_local
   const size_t bytes = 512 + 64 + 16 + sizeof(unsigned long long) * (ntiles + 8) + 2 * sizeof(unsigned long long) * S +
-                       2 * sizeof(unsigned long long) * cap + sizeof(int64_t) * (n + 8);
+                       2 * sizeof(unsigned long long) * cap + sizeof(int64_t) * (n + 8) +
+                       2 * sizeof(unsigned long long) * kSelT;
   char* base = (char*)scratch(c, bytes);
   if (!base) return KID_E_OOM;
   double* center = (double*)base;
@@ -541,6 +549,7 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
   unsigned long long* ck = (unsigned long long*)(skeys2 + S);  // 2S 32-bit keys: 8-byte aligned
   unsigned long long* ci = ck + cap;
   int64_t* src_local = (int64_t*)(ci + cap);
+  unsigned long long* sel = (unsigned long long*)(src_local + n + 8);  // [key | idx] of the n selected
   KID_CK(c, cudaMemcpyAsync(center, center_h, sizeof(double) * d, cudaMemcpyHostToDevice, c->stream));
   KID_CK(c, cudaMemsetAsync(count, 0, sizeof(unsigned long long) * (2 + ntiles + 8), c->stream));
   KID_CK(c, cudaMemsetAsync(c->counter, 0, sizeof(int64_t) * 2, c->stream));
@@ -559,9 +568,11 @@ int split_device(kid_ctx* c, const double* center_h, int64_t n, double xi, int64
                                                  count, cap);
   prof_end(c);
   KID_LAUNCHED(c);
-  const size_t sel_smem = sizeof(unsigned long long) * 2 * (kSelMax + kSelT);
-  cudaFuncSetAttribute(k_split_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
-  k_split_select<<<1, kSelT, sel_smem, c->stream>>>(ck, ci, count, cap, (int)nl, c->pts, N, d, src_local, c->src, ctrl);
+  const size_t rank_smem = sizeof(unsigned long long) * 2 * kSelMax;
+  cudaFuncSetAttribute(k_split_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem);
+  k_split_rank<<<kSelCtas, kRankT, rank_smem, c->stream>>>(ck, ci, count, cap, (int)nl, sel, ctrl);
+  KID_LAUNCHED(c);
+  k_split_place<<<1, kSelT, 0, c->stream>>>(sel, (int)nl, c->pts, N, d, src_local, c->src, ctrl);
   KID_LAUNCHED(c);
   prof_begin(c);
   cudaFuncSetAttribute(k_compact_flag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int64_t) * kFTile));
