@@ -55,7 +55,9 @@ def _ladder(K, skel, P, DtD_ref):
 
 def _device_vs(O, dev, K, skel, P, h, r_sd, r_sk, r_DtD, r_KtK):
     sd, sk, DtD, _ = dev.recon_error(h, skel, P)
-    assert sk == pytest.approx(r_sk, rel=1e-12)
+    # a sum of 1e7..5e10 positive terms: the oracle's own sequential sum carries ~sqrt(N) u ~ 1e-12, so
+    # the full-size bar for the Frobenius sums is the Gram bar
+    assert sk == pytest.approx(r_sk, rel=1e-10)
     bound, noise, dg = _ladder(K, skel, P, r_DtD)
     assert np.all(np.abs(DtD - r_DtD) <= bound + 1e-300)
     assert abs(sd - r_sd) <= 1e-10 * r_sd + 2 * np.sum(noise * dg) + np.sum(noise ** 2) + 1e-300
