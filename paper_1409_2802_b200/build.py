@@ -31,8 +31,22 @@ def build_cuda(force=False, verbose=False):
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "kernid_cuda.h")]
     if not force and not _stale(CUDA_SO, deps):
         return CUDA_SO
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-warn-spills", "-o", CUDA_SO] + [os.path.join(CSRC, f) for f in CU_SRCS]
+    # one nvcc per translation unit, in parallel (the cluster kernels' template instances dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, f[:-3] + ".o") for f in CU_SRCS]
+
+    def cc(i):
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-c",
+               "-Xptxas", "-warn-spills", "-o", objs[i], os.path.join(CSRC, CU_SRCS[i])]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+
+    with ThreadPoolExecutor(len(CU_SRCS)) as ex:
+        list(ex.map(cc, range(len(CU_SRCS))))
+    cmd = [NVCC, *ARCH, "-shared", "-o", CUDA_SO] + objs
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
