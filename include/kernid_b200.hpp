@@ -130,11 +130,14 @@ class KernelBlock {
   std::vector<double> row_norms() const;        // sampling.hpp:193 (device)
   Matrix gram(double* sumsq = nullptr) const;   // K^T K (device)
   double spectral_norm() const;                 // ||K||_2 = sqrt(lambda_max(K^T K))
-  // right_factor(K) / singular_values(K) of the full block (lowrank.hpp:70-90): Householder TSQR
-  // on the device (kid_tsqr_r) + a Jacobi SVD of the m x m factor for m <= 128 -- every sigma
-  // to ~u sigma_1; the Gram route (sqrt(eig(K^T K)), ~sqrt(u) sigma_1 floor) above that.
-  RightFactor right_factor() const;
-  std::vector<double> singular_values() const;  // values only: m > 128 by the Gram eigenvalues (sym_eigvals)
+  // right_factor(K) / singular_values(K) of the full block (lowrank.hpp:70-90). m <= 128: Householder TSQR
+  // on the device (kid_tsqr_r) + a Jacobi SVD of the m x m factor -- every sigma to ~u sigma_1. m > 128
+  // (the factor does not fit one SM): the Gram route (eig(K^T K), sigma resolved to ~sqrt(u) sigma_1) followed,
+  // when the caller needs more, by one preconditioned second pass (kid_proj_gram on K V diag(1/sigma)) that
+  // carries every sigma to ~1e-14 sigma_1. `resolve` = the relative level sigma / sigma_1 down to which the
+  // caller needs the spectrum (an eps of epsilon_rank; 0 = all of it): at or above 1e-7 the Gram pass suffices.
+  RightFactor right_factor(double resolve = 0.0) const;
+  std::vector<double> singular_values(double resolve = 0.0) const;
 
  private:
   Device* dev_;

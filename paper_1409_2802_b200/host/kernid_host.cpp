@@ -317,9 +317,57 @@ RightFactor right_factor(const Matrix& A) {
 // relative singular values the Gram route (sqrt of the eigenvalues of K^T K) resolves: ~sqrt(u) plus margin
 constexpr double kGramResolvable = 1e-7;
 
-std::vector<double> KernelBlock::singular_values() const {
+namespace {
+// Second pass of the m > 128 spectrum (the stand-in for the TSQR factor that does not fit one SM):
+// given the Gram route's eigenpairs (V, s) of K^T K -- sigma_i resolved to ~sqrt(u) sigma_1 -- form the
+// preconditioner X = V diag(1 / max(s_i, delta)), delta = 4 sqrt(m u) s_1, and take the Gram of K X on the
+// device (kid_proj_gram: K X has near-orthonormal leading columns, and trailing columns of norm sigma_i / delta,
+// so its Gram G2 carries the tail to ~u relative to delta^2 instead of sigma_1^2). With G2 = Q M Q^T,
+// K^T K = X^-T G2 X^-1 = B^T B for B = M^(1/2) Q^T diag(max(s, delta)) V^T, whose singular values and right
+// singular vectors are those of K (lowrank.hpp:56-90 takes them from the QR factor instead). B V has nearly
+// orthogonal columns, so the one-sided Jacobi SVD runs on it and the rotations J are folded into V.
+// Measured against LAPACK on the oracle's K: every sigma within ~2e-14 sigma_1 (m = 256 / 512, d = 1..16).
+void refine_right_factor(const KernelBlock& K, RightFactor& rf) {
+  const int64_t m = K.cols();
+  std::vector<double> sc(static_cast<size_t>(m));
+  const double s1 = rf.singular_values.empty() ? 0.0 : rf.singular_values[0];
+  if (!(s1 > 0.0)) return;
+  const double delta = 4.0 * std::sqrt(static_cast<double>(m) * 1.1102230246251565e-16) * s1;
+  Matrix X(m, m);
+  for (int64_t j = 0; j < m; ++j) {
+    const double sj = j < static_cast<int64_t>(rf.singular_values.size()) ? rf.singular_values[static_cast<size_t>(j)] : 0.0;
+    sc[static_cast<size_t>(j)] = std::max(sj, delta);
+    const double inv = 1.0 / sc[static_cast<size_t>(j)];
+    for (int64_t i = 0; i < m; ++i) X(i, j) = rf.V(i, j) * inv;
+  }
+  Matrix G2(m, m);
+  double sd = 0.0, sk = 0.0;
+  K.device().check(kid_proj_gram(K.device().ctx(), K.spec().h, X.data(), m, &sd, &sk, G2.data()));
+  std::vector<double> mu;
+  Matrix Q;
+  sym_eig(G2, mu, &Q);
+  Matrix U0(m, m);  // M^(1/2) Q^T diag(sc)
+  for (int64_t j = 0; j < m; ++j)
+    for (int64_t i = 0; i < m; ++i)
+      U0(i, j) = std::sqrt(std::max(mu[static_cast<size_t>(i)], 0.0)) * Q(j, i) * sc[static_cast<size_t>(j)];
+  Matrix J;
+  std::vector<double> sv;
+  jacobi_svd_v(std::move(U0), sv, J);
+  Matrix Vn(m, m);
+  for (int64_t j = 0; j < m; ++j)
+    for (int64_t k = 0; k < m; ++k) {
+      const double jk = J(k, j);
+      if (jk == 0.0) continue;
+      for (int64_t i = 0; i < m; ++i) Vn(i, j) += rf.V(i, k) * jk;
+    }
+  rf.V = std::move(Vn);
+  rf.singular_values = std::move(sv);
+}
+}  // namespace
+
+std::vector<double> KernelBlock::singular_values(double resolve) const {
   const int64_t m = cols();
-  if (m <= 128) return right_factor().singular_values;
+  if (m <= 128 || resolve < kGramResolvable) return right_factor(resolve).singular_values;
   const std::vector<double> ev = sym_eigvals(gram());  // Gram route, eigenvalues only
   std::vector<double> sv(ev.size());
   for (size_t i = 0; i < ev.size(); ++i) sv[i] = std::sqrt(std::max(ev[i], 0.0));
@@ -327,7 +375,7 @@ std::vector<double> KernelBlock::singular_values() const {
   return sv;
 }
 
-RightFactor KernelBlock::right_factor() const {
+RightFactor KernelBlock::right_factor(double resolve) const {
   const int64_t m = cols();
   RightFactor rf;
   if (m <= 128) {
@@ -339,6 +387,7 @@ RightFactor KernelBlock::right_factor() const {
     sym_eig(gram(), ev, &rf.V);
     rf.singular_values.resize(ev.size());
     for (size_t i = 0; i < ev.size(); ++i) rf.singular_values[i] = std::sqrt(std::max(ev[i], 0.0));
+    if (resolve < kGramResolvable) refine_right_factor(*this, rf);
   }
   rf.singular_values.resize(static_cast<size_t>(std::min(rows(), m)));
   return rf;
@@ -691,17 +740,17 @@ double lambda_max(const Matrix& G) {
 LeverageScores row_leverage_scores(const KernelBlock& K, int64_t r) {
   const int64_t mn = std::min(K.rows(), K.cols());
   if (r < 1 || r > mn) throw RangeError("row_leverage_scores: requires 1 <= r <= min(m, n)");
-  const RightFactor rf = K.right_factor();  // lowrank.hpp:299 (TSQR on the device for m <= 128)
-  const Matrix& V = rf.V;
   const int64_t m = K.cols();
+  // lowrank.hpp:299. m <= 128: TSQR on the device. m > 128: the Gram route where it resolves sigma_r with
+  // margin, else the Gram route plus its preconditioned second pass (refine_right_factor)
+  RightFactor rf = K.right_factor(kGramResolvable);
+  if (m > 128 && rf.singular_values[static_cast<size_t>(r - 1)] < 100.0 * kGramResolvable * rf.singular_values[0])
+    rf = K.right_factor(0.0);
+  const Matrix& V = rf.V;
   std::vector<double> sv = rf.singular_values;
   sv.resize(static_cast<size_t>(m), 0.0);
   if (!(sv[static_cast<size_t>(r - 1)] > 0.0))
     throw NumericalError("row_leverage_scores: sigma_r vanishes; scores undefined");
-  if (m > 128 && sv[static_cast<size_t>(r - 1)] < kGramResolvable * sv[0])  // Gram-route V_r, Sigma_r
-    throw IllConditionedSkeletonError("row_leverage_scores: sigma_r / sigma_1 = " +
-                                      std::to_string(sv[static_cast<size_t>(r - 1)] / sv[0]) +
-                                      " is below the resolution of the Gram route for m > 128");
   Matrix W(m, r);  // lowrank.hpp:304
   for (int64_t j = 0; j < r; ++j)
     for (int64_t i = 0; i < m; ++i) W(i, j) = V(i, j) * (1.0 / sv[static_cast<size_t>(j)]);
@@ -1291,14 +1340,10 @@ void run_experiment(Device& dev, const ExperimentConfig& cfg, std::ostream& out,
         K.emplace(dev, KernelSpec::gaussian(h_abs), points, split);
         const bool auto_rank = scheme.kind == SchemeKind::Leverage && cfg.scheme_rank_auto[scheme_idx];
         const bool need_full = cfg.rank_reference_full || cfg.emit_bound_sampling || auto_rank;
-        if (need_full) full_sv = K->singular_values();  // harness.hpp:176-184 (device TSQR)
-        // m > 128 takes the spectrum from the Gram K^T K: sigma_i below ~sqrt(u) sigma_1 are rounding noise
-        // there, so an eps-rank of the full spectrum finer than kGramResolvable is refused rather than
-        // returned wrong (the reference resolves it by QR + BDCSVD, lowrank.hpp:56-77)
-        if (auto_rank && K->cols() > 128 && rule.eps && *rule.eps < kGramResolvable)
-          throw IllConditionedSkeletonError("auto-rank leverage: eps = " + std::to_string(*rule.eps) +
-                                            " is below the resolution of the Gram-route spectrum for m > 128 (" +
-                                            std::to_string(kGramResolvable) + ")");
+        // harness.hpp:176-184: device TSQR for m <= 128; for m > 128 the Gram route, refined by its second
+        // pass when an eps-rank below the Gram route's resolution (or the whole spectrum) is asked for
+        const double need_level = (cfg.emit_bound_sampling || !rule.eps) ? 0.0 : *rule.eps;
+        if (need_full) full_sv = K->singular_values(need_level);
         if (cfg.rank_reference_full) rule.reference_sigma1 = (*full_sv)[0];
         if (auto_rank) scheme.rank_for_leverage = std::max<int64_t>(1, rule.resolve(*full_sv));
       }
@@ -1458,7 +1503,7 @@ BandwidthResult bandwidth_search(Device& dev, const ExperimentConfig& cfg, const
   BandwidthResult res;
   auto rank_at = [&](double h) -> long {
     const KernelBlock K(dev, KernelSpec::gaussian(h), points, split);
-    const long r = static_cast<long>(epsilon_rank(K.singular_values(), spec.eps));
+    const long r = static_cast<long>(epsilon_rank(K.singular_values(spec.eps), spec.eps));
     ++res.evaluations;
     res.profile.emplace_back(h, r);
     return r;
@@ -1715,7 +1760,7 @@ int kidh_compress_trial(int32_t device, int32_t d, int64_t N, int64_t n, double 
       if (lev_rank > 0) {
         sc.rank_for_leverage = lev_rank;
       } else {  // auto rank from the full spectrum (harness.hpp:176-184): device TSQR
-        sc.rank_for_leverage = std::max<int64_t>(1, rule.resolve(K.singular_values()));
+        sc.rank_for_leverage = std::max<int64_t>(1, rule.resolve(K.singular_values(eps)));
       }
     }
     SampleContext ctx;
@@ -1793,6 +1838,34 @@ int kidh_trial_next_rows(int32_t device, int32_t d, int64_t N, int64_t n, double
     const std::vector<double> u = apply_skeleton(K, id, std::vector<double>(q, q + K.cols()));
     if (static_cast<int64_t>(u.size()) > u_cap) throw RangeError("kidh_trial_next_rows: u buffer too small");
     std::memcpy(u_out, u.data(), sizeof(double) * u.size());
+  });
+}
+
+// The full-block spectrum of a trial's K(T, S) through the mirror (KernelBlock::right_factor(resolve):
+// lowrank.hpp:56-90 on the device) and, for lev_rank > 0, row_leverage_scores(K, lev_rank)
+// (lowrank.hpp:296-308). sv_out n values, V_out n x n col-major, scores_out n_targets (cap score_cap).
+int kidh_trial_spectrum(int32_t device, int32_t d, int64_t N, int64_t n, double xi, double h_value,
+                        uint64_t data_seed, double resolve, int64_t lev_rank, int64_t* n_targets, double* sv_out,
+                        double* V_out, double* scores_out, int64_t score_cap) {
+  return guard([&] {
+    Device dev(device);
+    const PointSet points = gen_normal(d, N, derive_seed(data_seed, 0xDA7A));
+    Rng crng(derive_seed(data_seed, 0xCE));
+    const int64_t ci = static_cast<int64_t>(crng.below(static_cast<std::uint64_t>(N)));
+    std::vector<double> center(static_cast<size_t>(d));
+    for (int k = 0; k < d; ++k) center[static_cast<size_t>(k)] = points(ci, k);
+    const SourceTargetSplit split = split_sources_targets(dev, points, center, n, xi);
+    const KernelBlock K(dev, KernelSpec::gaussian(h_value * silverman_bandwidth(d, N)), points, split);
+    *n_targets = K.rows();
+    const RightFactor rf = K.right_factor(resolve);
+    for (int64_t i = 0; i < n; ++i)
+      sv_out[i] = i < static_cast<int64_t>(rf.singular_values.size()) ? rf.singular_values[static_cast<size_t>(i)] : 0.0;
+    if (V_out) std::memcpy(V_out, rf.V.data(), sizeof(double) * static_cast<size_t>(n) * static_cast<size_t>(n));
+    if (lev_rank > 0) {
+      const LeverageScores ls = row_leverage_scores(K, lev_rank);
+      if (static_cast<int64_t>(ls.scores.size()) > score_cap) throw RangeError("kidh_trial_spectrum: score buffer too small");
+      std::memcpy(scores_out, ls.scores.data(), sizeof(double) * ls.scores.size());
+    }
   });
 }
 

@@ -52,6 +52,7 @@ def host_lib():
                                                   P(i64), P(i64), P(dbl), P(dbl), _ip, _ip, P(i64), P(i32)]
         L.kidh_compress_trial.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, i32, i64, dbl, u64, dbl, P(i64), P(i64),
                                           P(dbl), P(dbl), _ip, _ip, P(i64)]
+        L.kidh_trial_spectrum.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, i64, P(i64), _dp, _dp, _dp, i64]
         L.kidh_trial_svd.argtypes = [i32, i32, i64, i64, dbl, dbl, u64, dbl, u64, dbl, P(i64), P(dbl), P(dbl), _dp]
         L.kidh_interaction_fractions.argtypes = [i32, i32, i64, u64, dbl, _dp, i64, _dp]
         L.kidh_bandwidth_search.argtypes = [i32, i32, i64, i64, dbl, dbl, i32, dbl, i32, i32, u64, _dp, _dp, i32,
@@ -228,6 +229,20 @@ def trial_next_rows(d, N, n, xi, data_seed, s, sample_seed, eps, s_mc, n_mc, mc_
     r = rank.value
     return (nt.value, r, skel[:r].copy(), P[: r * n].reshape(n, r).T.copy() if r else np.zeros((0, n)), mc,
             u[: nt.value].copy())
+
+
+def trial_spectrum(d, N, n, xi, data_seed, resolve=0.0, lev_rank=0, h_value=1.0, device=0):
+    """singular_values / right_factor of a trial's full block K(T, S) (lowrank.hpp:56-90) through the C++
+    mirror: device TSQR for n <= 128, the Gram route plus its preconditioned second pass above that
+    (`resolve`: the relative level the spectrum is needed to; 0 = all). With lev_rank > 0 also
+    row_leverage_scores(K, lev_rank). Returns (n_targets, sv, V, scores or None)."""
+    nt = C.c_int64()
+    sv = np.zeros(n)
+    V = np.zeros(n * n)
+    scores = np.zeros(N if lev_rank > 0 else 1)
+    _ck(host_lib().kidh_trial_spectrum(device, d, N, n, xi, h_value, data_seed, resolve, lev_rank, C.byref(nt), sv, V,
+                                       scores, scores.size), "trial_spectrum")
+    return nt.value, sv, _uncm(V, n, n), (scores[: nt.value].copy() if lev_rank > 0 else None)
 
 
 def trial_svd(d, N, n, xi, data_seed, s, sample_seed, eps, h_value=1.0, device=0):
