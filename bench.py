@@ -60,6 +60,9 @@ WORKLOADS = {
     "c3-d5": dict(cfg="configs[2]", d=5, N=1_000_000, m=100, xi=3.0, h_value=1.0, s=0.02, eps=1e-8),
     "c4-d16": dict(cfg="configs[3]", d=16, N=12_000_000, m=256, xi=2.0, h_value=1.0, s=4e-4, eps=1e-2),
     "c4-d16-e8": dict(cfg="configs[3]", d=16, N=12_000_000, m=256, xi=2.0, h_value=1.0, s=4e-4, eps=1e-8),
+    # configs[3] at d=64: D_WS=2 leaves ~no N(0,I_64) targets, so throughput is measured on the
+    # UNFILTERED points (D_WS=0: every non-source point is a target) against the 256 nearest sources
+    "c4-d64-unfiltered": dict(cfg="configs[3]", d=64, N=10_000_000, m=256, xi=0.0, h_value=1.0, s=4e-4, eps=1e-2),
     # configs[4] at N=1 GPU: the largest single-GPU configuration (1.0012e8 points, 6.4 GB); sharded
     # over the ranks of a torchrun job for the scaling runs
     "c5": dict(cfg="configs[4]", d=8, N=100_120_000, m=512, xi=2.0, h_value=1.0, s=4e-5, eps=1e-2),

@@ -41,7 +41,7 @@ constexpr int kFNB = 32;                               // max D column blocks pe
 constexpr int kFEI = 40;                               // shorts per eval-warp list
 constexpr int kFMI = 4 + kFCB + 2 * kFTPW + 2;         // shorts per MMA-warp list
 constexpr int kFMeta = 16;                             // ints per (part, cta)
-constexpr int kFRing = 4;
+constexpr int kFRing = 4;                             // target-coordinate ring slots (2 when d > 32: shared memory)
 constexpr int kFRep = 16;                              // exp-table replicas (a 64-bit load is served per half-warp)
 constexpr int kFTab = kExpTab * kFRep;
 // named barriers: 0 = __syncthreads, K_A chunk ring full / empty (3 slots), K_B of stage s ready (2),
@@ -78,6 +78,7 @@ struct FxArgs {
   const short* elist;  // [part][cta][kFW][kFEI]: K_A group mask (2 shorts), nKN, K_B groups
   const short* mlist;  // [part][cta][kFW][kFMI]
   int CW;              // K_A chunk width (columns): 32, 48, 64 or 96
+  int ring;            // target-coordinate ring slots: copies run ring - 1 tiles ahead
   int ksplit;          // GEMM1 k-split over the 4 MMA warps (NE = 12)
   const int* gblk;     // [part][kFNB] global D block of each local block
   double* partial;     // [chunk][LG][LG]
@@ -234,8 +235,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
   const int DbS = ceil_to(A.nbs_max, 2) * 8 * kST;
   double* Xb = Db + (A.lev ? 0 : (size_t)S * DbS);                   // S x own_max x kST: peer partials
   double* Rk = Xb + (A.has_A ? (size_t)S * A.own_max * kST : 0);     // k-split partials [4][4 rb][kFCB][32][2]
-  double* ring = Rk + (A.ksplit ? 4 * 4 * kFCB * 64 : 0);             // kFRing x d x 32
-  uint64_t* bars = (uint64_t*)(ring + (size_t)kFRing * d * kTM);     // xfull[S], dfull[S], free[S]
+  double* ring = Rk + (A.ksplit ? 4 * 4 * kFCB * 64 : 0);             // A.ring x d x 32
+  uint64_t* bars = (uint64_t*)(ring + (size_t)A.ring * d * kTM);     // xfull[S], dfull[S], free[S]
   short* s_el = (short*)(bars + 3 * S);
   short* s_ml = s_el + kFW * kFEI;
   __shared__ double red_sk[kFW], red_tr[kFW];
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
     for (int e = tid; e < S * DbS; e += kFT) Db[e] = 0.0;
   if (A.has_A)
     for (int e = tid; e < S * A.own_max * kST; e += kFT) Xb[e] = 0.0;
-  for (int e = tid; e < kFRing * d * kTM; e += kFT) ring[e] = 0.0;
+  for (int e = tid; e < A.ring * d * kTM; e += kFT) ring[e] = 0.0;
   {
     const short* el = A.elist + ((size_t)part * 2 + cta) * kFW * kFEI;
     for (int e = tid; e < kFW * kFEI; e += kFT) s_el[e] = el[e];
@@ -306,18 +307,19 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
     };
     auto issue_copy = [&](int tl, int64_t prow) {
       if (prow >= 0) {
-        double* slot = ring + (size_t)(tl % kFRing) * d * kTM;
+        double* slot = ring + (size_t)(tl % A.ring) * d * kTM;
         for (int k = ew; k < d; k += NE) fx_cp8(slot + k * kTM + lane, A.tv.base + prow + (int64_t)k * A.tv.ld);
       }
       fx_commit();
     };
     int64_t next_row = -1;
+    const int PD = A.ring - 1;  // prefetch distance in tiles (3, or 1 with a 2-slot ring)
     if (copier) {
       issue_copy(0, row_of(0));
-      issue_copy(1, row_of(1));
+      if (PD > 1) issue_copy(1, row_of(1));
       fx_wait<0>();
-      issue_copy(2, row_of(2));
-      next_row = row_of(3);
+      if (PD > 2) issue_copy(2, row_of(2));
+      next_row = row_of(PD);
     }
     nbar_sync(kBEval, NE * 32);
     constexpr int DR = (D > 0 && D <= 8) ? D : 1;
@@ -326,10 +328,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
     int kq = 0;  // global K_A chunk counter (ring position)
     for (int it = 0; it < ntile; ++it) {
       if (copier) {
-        issue_copy(it + 3, next_row);
-        next_row = row_of(it + 4);
+        issue_copy(it + PD, next_row);
+        next_row = row_of(it + PD + 1);
       }
-      const double* slot = ring + (size_t)(it % kFRing) * d * kTM;
+      const double* slot = ring + (size_t)(it % A.ring) * d * kTM;
       // rows past the end of the target list sit at -far (padding sources at +far): every K entry of
       // such a row is exactly 0, the padding source columns included ((2 far)^2 d stays finite)
       const bool valid = trow(it) >= 0;
@@ -388,7 +390,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
         }
         nbar_arrive(kBKNF + s, kFT);
       }
-      if (copier) fx_wait<1>();
+      if (copier) {  // the next tile's coordinates have landed
+        if (PD > 1) fx_wait<1>();
+        else fx_wait<0>();
+      }
       nbar_sync(kBEval, NE * 32);
     }
     if (copier) fx_wait<0>();
@@ -1256,100 +1261,112 @@ int fused_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, dou
       for (int y = x; y < cnt; y += 2) t.push_back({lo + x, lo + y});
   };
   const int cap_tiles = 2 * NM * kFTPW;  // 2x2 tiles per part (two CTAs)
-  if (lev) {
-    for (int b0 = 0; b0 < NB; b0 += kFNB) {
-      FxPart p;
-      for (int b = b0; b < std::min(NB, b0 + kFNB); ++b) p.blocks.push_back(b);
-      parts.push_back(p);
+  // gs: blocks per group when the Gram is split -- one part per off-diagonal group pair (a gs x gs block
+  // square) and one per diagonal group (a triangle); each part evaluates only its groups' columns
+  auto build_parts = [&](int gs) {
+    parts.clear();
+    if (lev) {
+      for (int b0 = 0; b0 < NB; b0 += kFNB) {
+        FxPart p;
+        for (int b = b0; b < std::min(NB, b0 + kFNB); ++b) p.blocks.push_back(b);
+        parts.push_back(p);
+      }
+      return;
     }
-  } else {
     const int nt2 = (NB + 1) / 2;
-    if (NB <= kFNB && nt2 * (nt2 + 1) / 2 <= cap_tiles) {
+    if (gs >= 16 && NB <= kFNB && nt2 * (nt2 + 1) / 2 <= cap_tiles) {
       FxPart p;
       for (int b = 0; b < NB; ++b) p.blocks.push_back(b);
       tri_tiles(0, NB, p.tiles);
       parts.push_back(p);
-    } else {
-      // groups of 16 blocks: one part per off-diagonal group pair (a 16 x 16 block square) and one per
-      // diagonal group (a triangle); each part evaluates only its groups' columns
-      const int gs = 16, ng = (NB + gs - 1) / gs;
-      auto grp = [&](int gi) {
-        std::vector<int> v;
-        for (int b = gi * gs; b < std::min(NB, (gi + 1) * gs); ++b) v.push_back(b);
-        return v;
-      };
-      for (int i = 0; i < ng; ++i)
-        for (int j = i + 1; j < ng; ++j) {
-          FxPart p;
-          std::vector<int> gi = grp(i), gj = grp(j);
-          p.blocks = gi;
-          p.blocks.insert(p.blocks.end(), gj.begin(), gj.end());
-          for (int x = 0; x < (int)gi.size(); x += 2)
-            for (int y = 0; y < (int)gj.size(); y += 2) p.tiles.push_back({x, (int)gi.size() + y});
-          parts.push_back(p);
-        }
-      for (int i = 0; i < ng; ++i) {
+      return;
+    }
+    const int ng = (NB + gs - 1) / gs;
+    auto grp = [&](int gi) {
+      std::vector<int> v;
+      for (int b = gi * gs; b < std::min(NB, (gi + 1) * gs); ++b) v.push_back(b);
+      return v;
+    };
+    for (int i = 0; i < ng; ++i)
+      for (int j = i + 1; j < ng; ++j) {
         FxPart p;
-        p.blocks = grp(i);
-        tri_tiles(0, (int)p.blocks.size(), p.tiles);
+        std::vector<int> gi = grp(i), gj = grp(j);
+        p.blocks = gi;
+        p.blocks.insert(p.blocks.end(), gj.begin(), gj.end());
+        for (int x = 0; x < (int)gi.size(); x += 2)
+          for (int y = 0; y < (int)gj.size(); y += 2) p.tiles.push_back({x, (int)gi.size() + y});
         parts.push_back(p);
       }
+    for (int i = 0; i < ng; ++i) {
+      FxPart p;
+      p.blocks = grp(i);
+      tri_tiles(0, (int)p.blocks.size(), p.tiles);
+      parts.push_back(p);
     }
-  }
-  const int nparts = (int)parts.size();
-  int TPW = 1;
-  for (auto& p : parts) TPW = std::max(TPW, (int)((p.tiles.size() + 2 * NM - 1) / (2 * NM)));
-  if (TPW > kFTPW) return fail(c, KID_E_DIM, "fused pass: Gram part exceeds the register budget");
-  const int CBM = TPW >= 5 ? 3 : kFCB;
+  };
   // ---- k-split of the A columns over the two CTAs (chunks of CW columns, chosen with the smem below)
   const int a0 = has_A ? std::min(a, ceil_to((a + 1) / 2, 4)) : 0;
   const int a_lo[2] = {0, a0}, a_cnt[2] = {a0, a - a0};
   int acp_max = 0, CW = 32;
-  // ---- per (part, cta) geometry
   int nbs_max = 0, own_max = 0, spn_max = 0, srcw_max = 0;
-  for (auto& p : parts) {
-    const int nbS = (int)p.blocks.size(), h0 = (nbS + 1) / 2;
-    nbs_max = std::max(nbs_max, nbS);
-    own_max = std::max(own_max, std::max(h0, nbS - h0) * 8);
-    spn_max = std::max(spn_max, frag_stride(nbS * 8));
-  }
-  // k-split GEMM1: 4 MMA warps, every column block in one warp's accumulators
-  const int ksplit = (NM == 4 && has_A && nbs_max <= CBM) ? 1 : 0;
+  int nparts = 0, TPW = 1, CBM = kFCB, ksplit = 0;
   int S = 0, KSS = 0;
   bool m_smem = has_A;
   size_t smem = 0;
-  auto smem_of = [&](int cw, int st, int kss, bool msm) {
-    int acpm = 0;
-    for (int x = 0; x < 2; ++x) acpm = std::max(acpm, ceil_to(a_cnt[x], 4));
-    size_t w = kFTab + (size_t)d * (acpm + own_max);
-    if (has_A && msm) w += (size_t)acpm * spn_max;
-    if (has_A) w += (size_t)kss * cw * kST;
-    if (!lev) w += (size_t)st * ceil_to(nbs_max, 2) * 8 * kST;
-    if (has_A) w += (size_t)st * own_max * kST;
-    w += (size_t)kFRing * d * kTM;
-    if (ksplit) w += 4 * 4 * kFCB * 64;
-    return w * 8 + 3 * st * 8 + 2 * (kFW * kFEI + kFW * kFMI) + 64;
-  };
+  const int ring_slots = d > 32 ? 2 : kFRing;
   const size_t kMaxSmem = 227 * 1024 - 6144;  // minus the static arrays
   // chunk width: CW / 4 four-column groups per chunk spread over the NE eval warps (two each when it fits)
   int cw_try[2] = {NE == 12 ? 64 : 48, 32};  // measured best: c5 (12 eval warps) 64, c4-d16 (8) 48
   if (c->chunk_cols) cw_try[0] = c->chunk_cols;
-  for (int msm = (has_A ? 1 : 0); msm >= 0 && !S; --msm)
-    for (int cw : cw_try) {
-      for (int st : {2, 1}) {
-        for (int kss : {3, 2})
-          if (smem_of(cw, st, kss, msm) <= kMaxSmem) {
-            S = st;
-            KSS = kss;
-            CW = has_A ? cw : 32;
-            m_smem = msm;
-            smem = smem_of(cw, st, kss, msm);
-            break;
-          }
+  // smaller Gram groups (more parts, more exp recompute) only where the D tile of a 32-block part does not
+  // fit beside the sources (d = 64: 64 KB of source coordinates, 32 KB of target coordinates)
+  for (int gs : {16, 12, 8}) {
+    build_parts(gs);
+    nparts = (int)parts.size();
+    TPW = 1;
+    for (auto& p : parts) TPW = std::max(TPW, (int)((p.tiles.size() + 2 * NM - 1) / (2 * NM)));
+    if (TPW > kFTPW) return fail(c, KID_E_DIM, "fused pass: Gram part exceeds the register budget");
+    CBM = TPW >= 5 ? 3 : kFCB;
+    // ---- per (part, cta) geometry
+    nbs_max = own_max = spn_max = 0;
+    for (auto& p : parts) {
+      const int nbS = (int)p.blocks.size(), h0 = (nbS + 1) / 2;
+      nbs_max = std::max(nbs_max, nbS);
+      own_max = std::max(own_max, std::max(h0, nbS - h0) * 8);
+      spn_max = std::max(spn_max, frag_stride(nbS * 8));
+    }
+    // k-split GEMM1: 4 MMA warps, every column block in one warp's accumulators
+    ksplit = (NM == 4 && has_A && nbs_max <= CBM) ? 1 : 0;
+    auto smem_of = [&](int cw, int st, int kss, bool msm) {
+      int acpm = 0;
+      for (int x = 0; x < 2; ++x) acpm = std::max(acpm, ceil_to(a_cnt[x], 4));
+      size_t w = kFTab + (size_t)d * (acpm + own_max);
+      if (has_A && msm) w += (size_t)acpm * spn_max;
+      if (has_A) w += (size_t)kss * cw * kST;
+      if (!lev) w += (size_t)st * ceil_to(nbs_max, 2) * 8 * kST;
+      if (has_A) w += (size_t)st * own_max * kST;
+      w += (size_t)ring_slots * d * kTM;
+      if (ksplit) w += 4 * 4 * kFCB * 64;
+      return w * 8 + 3 * st * 8 + 2 * (kFW * kFEI + kFW * kFMI) + 64;
+    };
+    for (int msm = (has_A ? 1 : 0); msm >= 0 && !S; --msm)
+      for (int cw : cw_try) {
+        for (int st : {2, 1}) {
+          for (int kss : {3, 2})
+            if (smem_of(cw, st, kss, msm) <= kMaxSmem) {
+              S = st;
+              KSS = kss;
+              CW = has_A ? cw : 32;
+              m_smem = msm;
+              smem = smem_of(cw, st, kss, msm);
+              break;
+            }
+          if (S) break;
+        }
         if (S) break;
       }
-      if (S) break;
-    }
+    if (S || lev) break;
+  }
   if (!S) return fail(c, KID_E_DIM, "fused pass: tile buffers exceed shared memory");
   for (int x = 0; x < 2; ++x) acp_max = std::max(acp_max, ceil_to(a_cnt[x], 4));
   srcw_max = acp_max + own_max;
@@ -1524,6 +1541,7 @@ int fused_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, dou
   A.S = S;
   A.KSS = KSS;
   A.CW = CW;
+  A.ring = ring_slots;
   A.ksplit = ksplit;
   A.has_A = has_A;
   A.has_B = has_B;
