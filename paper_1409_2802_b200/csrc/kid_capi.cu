@@ -200,6 +200,11 @@ int kid_set_option(kid_ctx* c, int32_t key, int64_t value) {
     c->kernel_choice = (int)value;
     return KID_OK;
   }
+  if (key == KID_OPT_TILE_WARPS) {
+    if (value != 0 && value != 8 && value != 12) return fail(c, KID_E_RANGE, "kid_set_option: tile warps must be 0, 8 or 12");
+    c->tile_warps = (int)value;
+    return KID_OK;
+  }
   return fail(c, KID_E_RANGE, "kid_set_option: unknown option");
 }
 
