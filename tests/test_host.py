@@ -181,3 +181,52 @@ def test_host_lambda_max(n, kind):
     ref = np.linalg.eigvalsh(A)[-1]
     got = H.lambda_max(A)
     assert abs(got - ref) <= 1e-12 * ref, (got, ref)
+
+
+def test_host_id_vs_lapack_cpqr(H):
+    """An independent pin of the ID restatement (lowrank.hpp:135-262: column-pivoted Householder QR,
+    P = R11^-1 [R11 R12] Pi^T): LAPACK's dgeqp3 (scipy) on sampled Gaussian-kernel rows. Both pick the
+    largest remaining column norm at every step, so wherever that choice is not a near-tie the pivot
+    sequences -- hence the skeletons -- must coincide, and the projections agree to the conditioning of R11."""
+    import scipy.linalg as sla
+    from oracle import oracle as O
+    checked = 0
+    for d, N, n, s, eps in [(2, 20_000, 100, 0.02, 1e-6), (3, 20_000, 100, 0.02, 1e-4), (5, 20_000, 64, 0.03, 1e-8),
+                            (8, 30_000, 200, 0.02, 1e-2), (1, 10_000, 100, 0.05, 1e-10)]:
+        t = O.prepare_trial(d, N, n, 2.0, O.derive_seed(1, 0, 0))
+        K = O.kernel_matrix(t.targets, t.sources, t.h)
+        rows = O.sample_rows(O.SCHEME_UNIFORM, K.shape[0], s, O.derive_seed(3, 0, 1))
+        A = K[rows]
+        r = int(H.epsilon_rank(H.singular_values(A), eps))
+        if r < 1 or r >= n:
+            continue
+        skel, P = H.interpolative_decomposition(A, r)
+        Q, R, piv = sla.qr(A, mode="economic", pivoting=True)
+        # pivot steps with a clear winner: replay LAPACK's sequence and measure the margin of each choice
+        W = A.copy()
+        clear = True
+        for k in range(r):
+            nr = np.sqrt((W ** 2).sum(0))
+            nr[piv[:k]] = -1.0
+            order = np.argsort(nr)[::-1]
+            if nr[order[1]] > (1.0 - 1e-6) * nr[order[0]]:
+                clear = False
+                break
+            assert order[0] == piv[k]
+            q = Q[:, k]
+            W = W - np.outer(q, q @ W)
+        if not clear:
+            continue
+        checked += 1
+        assert np.array_equal(np.sort(skel), np.sort(piv[:r]))
+        # P against LAPACK's: columns piv[:r] carry the identity, the rest R11^-1 R12
+        T = sla.solve_triangular(R[:r, :r], R[:r, r:])
+        P_ref = np.zeros((r, n))
+        P_ref[np.arange(r), piv[:r]] = 1.0
+        P_ref[:, piv[r:]] = T
+        # rows of P follow the skeleton order of the ID; map both to ascending column index
+        o1, o2 = np.argsort(skel), np.argsort(piv[:r])
+        cond = np.linalg.cond(R[:r, :r])
+        assert np.max(np.abs(P[o1] - P_ref[o2])) <= 1e-13 * cond * max(1.0, np.abs(P_ref).max())
+        assert np.linalg.norm(A[:, skel] @ P - A, 2) <= 10 * np.linalg.norm(A[:, piv[:r]] @ P_ref - A, 2) + 1e-14
+    assert checked >= 3
