@@ -177,6 +177,10 @@ int kid_select_rows(kid_ctx* ctx, const int64_t* rows, int64_t n);
 /* ---- diagnostics: the FP64 passes' exp(x), x <= 0 (for accuracy checks against libm) ---- */
 int kid_exp_check(kid_ctx* ctx, const double* x, int64_t n, double* y);
 
+/* ---- diagnostics: canary check of a -DKID_GUARD build (64 KB guard zones around every device buffer of the
+ * library): corrupted guard bytes, 0 = clean; -1 when the library was built without the guards ---- */
+int64_t kid_guard_check(kid_ctx* ctx);
+
 /* ---- instrumentation: number of kernels this context has launched ---- */
 int64_t kid_launch_count(const kid_ctx* ctx);
 /* Kernel timing: when enabled, each pass records a CUDA event pair on its stream around its

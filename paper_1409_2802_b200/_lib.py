@@ -39,7 +39,7 @@ SYMBOLS = ["kid_abi_version", "kid_host_alloc", "kid_host_free", "kid_create", "
            "kid_gram_dev", "kid_leverage", "kid_leverage_dev", "kid_recon_error", "kid_recon_prepare",
            "kid_recon_error_dev", "kid_eval_rows", "kid_apply_skeleton", "kid_apply_skeleton_dev", "kid_select_rows",
            "kid_launch_count", "kid_profile", "kid_profile_read", "kid_exp_check", "kid_set_path", "kid_last_kernel", "kid_set_option",
-           "kid_device_id", "kid_stream", "kid_device_alloc", "kid_device_free", "kid_memcpy_dtoh"]
+           "kid_device_id", "kid_stream", "kid_device_alloc", "kid_device_free", "kid_memcpy_dtoh", "kid_guard_check"]
 
 
 def cuda_lib():
@@ -97,6 +97,12 @@ def cuda_lib():
         L.kid_launch_count.restype = i64
         L.kid_profile.argtypes = [vp, i32]
         L.kid_exp_check.argtypes = [vp, _dp, i64, _dp]
+        L.kid_guard_check.argtypes = [vp]
+        L.kid_device_alloc.argtypes = [vp, C.c_size_t]
+        L.kid_device_alloc.restype = vp
+        L.kid_device_free.argtypes = [vp, vp]
+        L.kid_device_free.restype = None
+        L.kid_guard_check.restype = i64
         L.kid_profile_read.argtypes = [vp, vp, i64, P(i64)]
         _cuda = L
     return _cuda
@@ -167,6 +173,19 @@ class Device:
         n = C.c_int64()
         self._ck(self.L.kid_profile_read(self.h, buf.ctypes.data, cap, C.byref(n)), "kid_profile_read")
         return buf[: min(n.value, cap)].copy()
+
+    def device_alloc(self, nbytes: int) -> int:
+        p = self.L.kid_device_alloc(self.h, nbytes)
+        if not p:
+            raise KidError(KID_E_OOM, "kid_device_alloc failed")
+        return int(p)
+
+    def device_free(self, p: int):
+        self.L.kid_device_free(self.h, p)
+
+    def guard_check(self) -> int:
+        """Corrupted canary bytes around the library's device buffers (-DKID_GUARD build); -1 without guards."""
+        return int(self.L.kid_guard_check(self.h))
 
     def exp_check(self, x) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)

@@ -53,6 +53,24 @@ def build_cuda(force=False, verbose=False):
     return CUDA_SO
 
 
+def build_guard(verbose=False):
+    """libkernid_cuda_guard.so: the same objects with kid_capi.cu compiled -DKID_GUARD (64 KB canary zones
+    around every device buffer, kid_guard_check) -- the out-of-bounds check of tools/guard_cases.py, built on
+    demand (compute-sanitizer is closed on this GPU pool). Not part of build_all."""
+    build_cuda(False, verbose)
+    objdir = os.path.join(PKG, "build")
+    gobj = os.path.join(objdir, "kid_capi_guard.o")
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-DKID_GUARD", "-c", "-o", gobj,
+           os.path.join(CSRC, "kid_capi.cu")]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    out = os.path.join(PKG, "libkernid_cuda_guard.so")
+    objs = [gobj] + [os.path.join(objdir, f[:-3] + ".o") for f in CU_SRCS if f != "kid_capi.cu"]
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", out] + objs, check=True)
+    return out
+
+
 def build_host(force=False, verbose=False):
     if not os.path.isdir(HOST):
         return None
@@ -77,4 +95,7 @@ def build_all(force=False, verbose=False):
 
 
 if __name__ == "__main__":
-    build_all(force="--force" in sys.argv, verbose=True)
+    if "--guard" in sys.argv:
+        print(build_guard(verbose=True))
+    else:
+        build_all(force="--force" in sys.argv, verbose=True)

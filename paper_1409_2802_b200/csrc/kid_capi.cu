@@ -2,6 +2,8 @@
 // Host buffers in, host buffers out; no exceptions cross the boundary; status codes map
 // onto the reference exception taxonomy (proj/include/kernid/errors.hpp:11-77).
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <cstring>
 #include <new>
 #include <numeric>
@@ -23,13 +25,55 @@ int cuda_fail(kid_ctx* c, cudaError_t e, const char* where) {
   return fail(c, e == cudaErrorMemoryAllocation ? KID_E_OOM : KID_E_CUDA, msg);
 }
 
+// Device allocations of the library. A -DKID_GUARD build (tools/gpu/r02_guard.sh; compute-sanitizer is closed
+// on this GPU pool) brackets every allocation with 64 KB canary zones that kid_guard_check() verifies: an
+// out-of-bounds global store of any kernel within 64 KB of a library buffer shows up as a corrupted canary.
+#ifdef KID_GUARD
+namespace {
+constexpr size_t kGuardBytes = 64 * 1024;
+constexpr int kGuardByte = 0xA5;
+struct GuardRec { char* base; size_t bytes; };
+std::mutex g_guard_mu;
+std::unordered_map<void*, GuardRec> g_guard;
+}  // namespace
+#endif
+cudaError_t dev_malloc(void** p, size_t bytes) {
+#ifdef KID_GUARD
+  const size_t padded = (bytes + 255) / 256 * 256;
+  char* base = nullptr;
+  cudaError_t e = cudaMalloc((void**)&base, padded + 2 * kGuardBytes);
+  if (e != cudaSuccess) return e;
+  cudaMemset(base, kGuardByte, kGuardBytes);
+  cudaMemset(base + kGuardBytes + bytes, kGuardByte, padded - bytes + kGuardBytes);
+  *p = base + kGuardBytes;
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  g_guard[*p] = GuardRec{base, bytes};
+  return cudaSuccess;
+#else
+  return cudaMalloc(p, bytes);
+#endif
+}
+void dev_free(void* p) {
+  if (!p) return;
+#ifdef KID_GUARD
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  auto it = g_guard.find(p);
+  if (it != g_guard.end()) {
+    cudaFree(it->second.base);
+    g_guard.erase(it);
+    return;
+  }
+#endif
+  cudaFree(p);
+}
+
 int ensure(kid_ctx* c, void** p, size_t* cap, size_t bytes) {
   if (*p && *cap >= bytes) return KID_OK;
-  if (*p) cudaFree(*p);
+  if (*p) dev_free(*p);
   *p = nullptr;
   *cap = 0;
   const size_t want = std::max<size_t>(bytes, 256);
-  cudaError_t e = cudaMalloc(p, want);
+  cudaError_t e = dev_malloc(p, want);
   if (e != cudaSuccess) {
     *p = nullptr;
     cuda_fail(c, e, "cudaMalloc");
@@ -119,7 +163,7 @@ int kid_create(kid_ctx** out, int32_t device) {
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&c->counter, sizeof(int64_t) * 8);
+  if (e == cudaSuccess) e = dev_malloc((void**)&c->counter, sizeof(int64_t) * 8);
   if (e != cudaSuccess) {
     delete c;
     (void)cudaGetLastError();
@@ -136,8 +180,7 @@ void kid_destroy(kid_ctx* c) {
   cudaStreamSynchronize(c->stream);
   void* bufs[] = {c->pts_own, c->dist, c->flag, c->tgt_idx, c->blk_tgt, c->src, c->src_perm, c->P2,
                   c->scratch, c->partial, c->counter, c->sort_tmp, c->sub_idx};
-  for (void* p : bufs)
-    if (p) cudaFree(p);
+  for (void* p : bufs) dev_free(p);
   if (c->hbuf) cudaFreeHost(c->hbuf);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -161,7 +204,7 @@ void* kid_stream(kid_ctx* c) { return c ? (void*)c->stream : nullptr; }
 void* kid_device_alloc(kid_ctx* c, size_t bytes) {
   if (!c || set_device(c)) return nullptr;
   void* p = nullptr;
-  if (cudaMalloc(&p, bytes ? bytes : 8) != cudaSuccess) {
+  if (dev_malloc(&p, bytes ? bytes : 8) != cudaSuccess) {
     cuda_fail(c, cudaGetLastError(), "kid_device_alloc");
     return nullptr;
   }
@@ -171,7 +214,32 @@ void* kid_device_alloc(kid_ctx* c, size_t bytes) {
 void kid_device_free(kid_ctx* c, void* p) {
   if (!c || !p) return;
   set_device(c);
-  cudaFree(p);
+  dev_free(p);
+}
+
+// Corrupted canary bytes around the library's live device allocations (0 = clean); -1 when the library was
+// not built with -DKID_GUARD.
+int64_t kid_guard_check(kid_ctx* c) {
+#ifdef KID_GUARD
+  if (!c || set_device(c)) return -2;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  int64_t bad = 0;
+  std::vector<unsigned char> h;
+  for (auto& kv : g_guard) {
+    const GuardRec& g = kv.second;
+    const size_t padded = (g.bytes + 255) / 256 * 256;
+    const size_t tail = padded - g.bytes + kGuardBytes;
+    h.resize(kGuardBytes + tail);
+    cudaMemcpy(h.data(), g.base, kGuardBytes, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h.data() + kGuardBytes, g.base + kGuardBytes + g.bytes, tail, cudaMemcpyDeviceToHost);
+    for (unsigned char b : h) bad += b != (unsigned char)kGuardByte;
+  }
+  return bad;
+#else
+  (void)c;
+  return -1;
+#endif
 }
 
 int kid_memcpy_dtoh(kid_ctx* c, void* dst, const void* src, size_t bytes) {
