@@ -261,6 +261,10 @@ def measure_pass(wl_name, args, torch, ws, rank, local, steps, warmup, e2e_steps
         dev.set_option(2, args.chunk_cols)
     if getattr(args, "kernel", 0):
         dev.set_option(3, args.kernel)
+    if getattr(args, "tile_form", 0):
+        dev.set_option(5, args.tile_form)
+    if getattr(args, "path", 0):
+        dev.set_path(args.path)
     if getattr(args, "tile_warps", 0):
         dev.set_option(4, args.tile_warps)
     stream = torch.cuda.current_stream()
@@ -760,6 +764,8 @@ def main():
     ap.add_argument("--eval-warps", type=int, default=0, help="cluster kernel eval warps (0 auto, 8, 12)")
     ap.add_argument("--chunk-cols", type=int, default=0, help="cluster kernel K_A chunk width (0 auto, 32-96)")
     ap.add_argument("--tile-warps", type=int, default=0, help="warp-tile kernel warps per CTA (0 auto, 8, 12)")
+    ap.add_argument("--tile-form", type=int, default=0, help="warp-tile kernel form: 0 auto, 1 one CTA per SM, 2 CTA pair")
+    ap.add_argument("--path", type=int, default=0, help="kernel family: 0 auto, 1 always the cluster kernels")
     ap.add_argument("--kernel", type=int, default=0, help="large-m kernel: 0 auto, 1 k_fused, 2 k_fused_w")
     ap.add_argument("--svd-proj", action="store_true", help="--pass svd through kid_proj_gram (C = V_perp) instead of the ID route")
     ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms", "gram", "leverage"])

@@ -273,6 +273,11 @@ int kid_set_option(kid_ctx* c, int32_t key, int64_t value) {
     c->tile_warps = (int)value;
     return KID_OK;
   }
+  if (key == KID_OPT_TILE_FORM) {
+    if (value < 0 || value > 2) return fail(c, KID_E_RANGE, "kid_set_option: tile form must be 0, 1 or 2");
+    c->tile_form = (int)value;
+    return KID_OK;
+  }
   return fail(c, KID_E_RANGE, "kid_set_option: unknown option");
 }
 

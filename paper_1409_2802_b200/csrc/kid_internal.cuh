@@ -208,6 +208,7 @@ struct kid_ctx {
   int eval_warps = 0;
   int chunk_cols = 0;
   int tile_warps = 0;     // kid_set_option(KID_OPT_TILE_WARPS): warps per CTA of the warp-tile kernel (0 auto, 8, 12)
+  int tile_form = 0;      // kid_set_option(KID_OPT_TILE_FORM): warp-tile kernel form (0 auto, 1 solo, 2 cluster)
   int kernel_choice = 0;  // kid_set_option(KID_OPT_KERNEL): 0 auto, 1 k_fused, 2 k_fused_w where it applies  // kid_set_option(KID_OPT_CHUNK_COLS): K_A chunk width of the cluster kernel (0 auto)  // kid_set_option(KID_OPT_EVAL_WARPS): eval warps of the cluster kernel (0 auto, 8, 12)
   const char* last_kernel = "";  // dominant kernel of the last pass (kid_last_kernel)  // kid_set_path: which kernel family serves the Gram / leverage passes
   void* sort_tmp = nullptr;       // CUB radix-sort temporary storage (pass 1)

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "kid_device.cuh"
+#include "kid_fused.cuh"
 
 namespace kid {
 
@@ -701,6 +702,12 @@ int gram_dev(kid_ctx* c, double h, int64_t r, double* d_out) {
   if (meff < 1) return sumsq_dev(c, h, d_out);  // full-rank skeleton: D == 0 exactly, only ||K||_F^2
   const int NBN = ceil_to(meff, 8) / 8;
   const int LG = NBN * 8;
+  // few D columns (n <= 32: the high-rank end of the eps sweeps): the warp-tile kernel, one CTA per SM --
+  // every warp runs its own 32-row tile end to end, no producer / consumer hand-off (kid_fused_w.cu)
+  if (r > 0 && NBN <= 4 && c->kernel_choice != 1 && c->path != KID_PATH_CLUSTER) {
+    const int rc = fused_w_dev(c, h, FX_RESID, nullptr, 0, d_out);
+    if (rc != 1) return rc;
+  }
   // upper-triangular warp tiles of WA x 2 blocks (8x16 when NBN <= 12, else 16x16), row-major,
   // as (a0, b0) block coordinates; fewer padded slots than 16x16 tiles for the small-m configs
   const int WA = NBN <= 12 ? 1 : 2;

@@ -89,10 +89,13 @@ def test_cluster_residual(oracle, cluster, d, n, eps, kern):
         cluster.set_option(3, 0)
 
 
-@pytest.mark.parametrize("d,n,r", [(8, 100, 80), (3, 64, 60), (16, 48, 17), (5, 40, 39), (8, 200, 175)])
+@pytest.mark.parametrize("d,n,r", [(8, 100, 80), (3, 64, 60), (16, 48, 17), (5, 40, 39), (8, 200, 175), (2, 100, 90),
+                                   (4, 37, 30), (1, 16, 5), (7, 100, 70), (12, 40, 33)])
 def test_warp_tile_kernel(oracle, dev, d, n, r):
-    """k_fused_w (n - r <= 32 D columns: 1 to 4 column blocks, ragged tiles) against the oracle, and the same
-    Grams from k_fused within the rounding ladder; bitwise reproducible run to run."""
+    """k_fused_w (n - r <= 32 D columns: 1 to 4 column blocks, ragged tiles) in both forms -- one CTA per SM
+    (the automatic choice here: M and the sources fit one SM) and the CTA pair with its DSMEM exchange --
+    against the oracle, the same Grams from k_fused within the rounding ladder, bitwise reproducible run to
+    run; the automatic path of kid_recon_error takes it for n <= 32."""
     t, K = _block(oracle, d, 15_000, n)
     dev.set_points(t.points)
     dev.split(t.center, n, 2.0)
@@ -101,20 +104,32 @@ def test_warp_tile_kernel(oracle, dev, d, n, r):
     bound, _, _ = _resid_bound(K, res, r_DtD)
     out = {}
     try:
-        for kern in (2, 1):
-            dev.set_path(1)
-            dev.set_option(3, kern)
-            out[kern] = dev.recon_error(t.h, res.skeleton, res.P)
-            if kern == 2:
-                assert dev.last_kernel() == "k_fused_w"
-                again = dev.recon_error(t.h, res.skeleton, res.P)
-                assert np.array_equal(again[2], out[2][2]) and again[0] == out[2][0]
+        auto = dev.recon_error(t.h, res.skeleton, res.P)
+        assert dev.last_kernel() == "k_fused_w (solo)"
+        out["auto"] = auto
+        for form, warps in ((1, 0), (1, 8), (2, 0)):
+            dev.set_option(5, form)
+            dev.set_option(4, warps)
+            got = dev.recon_error(t.h, res.skeleton, res.P)
+            assert dev.last_kernel() == ("k_fused_w (solo)" if form == 1 else "k_fused_w")
+            again = dev.recon_error(t.h, res.skeleton, res.P)
+            assert np.array_equal(again[2], got[2]) and again[0] == got[0]
+            out[(form, warps)] = got
+        dev.set_option(5, 0)
+        dev.set_option(4, 0)
+        dev.set_path(1)
+        dev.set_option(3, 1)
+        out["k_fused"] = dev.recon_error(t.h, res.skeleton, res.P)
+        assert dev.last_kernel() == "k_fused"
     finally:
         dev.set_option(3, 0)
+        dev.set_option(4, 0)
+        dev.set_option(5, 0)
         dev.set_path(0)
-    for kern in (1, 2):
-        assert np.all(np.abs(out[kern][2] - r_DtD) <= bound + 1e-300)
-        assert out[kern][1] == pytest.approx(float(np.sum(K * K)), rel=1e-12)
+    assert np.array_equal(out["auto"][2], out[(1, 0)][2])
+    for key, got in out.items():
+        assert np.all(np.abs(got[2] - r_DtD) <= bound + 1e-300), key
+        assert got[1] == pytest.approx(float(np.sum(K * K)), rel=1e-12), key
 
 
 def test_cluster_residual_rank_one_and_full(oracle, cluster):
