@@ -87,6 +87,19 @@ def flops_per_entry_strict(d: int, m: int, r: int) -> float:
     return 3 * d + 1 + F_EXP + 2 + 2.0 * r * me / m + me * (me + 1) / m
 
 
+def hbm_peak():
+    """HBM roofline denominator (GB/s): the driver-measured copy bandwidth in MEASURED_PEAKS.json, else the
+    profiling recipe's fallback (6650 GB/s, "of fallback")."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            with open(p) as f:
+                return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
+        except (KeyError, ValueError, OSError):
+            pass
+    return 6650.0, "fallback of /opt/skills/guides/B200_PROFILING.md (MEASURED_PEAKS.json absent)"
+
+
 def load_peaks():
     """FP64 roofline denominator: the SUSTAINED DMMA rate of tools/fp64_peaks.cu (seconds-long
     back-to-back launches, the regime of a 0.1-1 s pass); the burst figure is kept beside it."""
@@ -250,11 +263,8 @@ def setup(wl, ws, rank, local, torch):
     return dev, prob
 
 
-# ----------------------------------------------------------------- our arm
-def measure_pass(wl_name, args, torch, ws, rank, local, steps, warmup, e2e_steps):
-    """Set up one workload, time the device-resident fused pass, optionally the e2e path."""
-    wl = WORKLOADS[wl_name]
-    dev, prob = setup(wl, ws, rank, local, torch)
+def apply_options(dev, args):
+    """Tuning / A-B switches of the library (results agree to the rounding ladder either way)."""
     if getattr(args, "eval_warps", 0):
         dev.set_option(1, args.eval_warps)
     if getattr(args, "chunk_cols", 0):
@@ -267,6 +277,14 @@ def measure_pass(wl_name, args, torch, ws, rank, local, steps, warmup, e2e_steps
         dev.set_path(args.path)
     if getattr(args, "tile_warps", 0):
         dev.set_option(4, args.tile_warps)
+
+
+# ----------------------------------------------------------------- our arm
+def measure_pass(wl_name, args, torch, ws, rank, local, steps, warmup, e2e_steps):
+    """Set up one workload, time the device-resident fused pass, optionally the e2e path."""
+    wl = WORKLOADS[wl_name]
+    dev, prob = setup(wl, ws, rank, local, torch)
+    apply_options(dev, args)
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
     m, r = wl["m"], prob.r
@@ -418,14 +436,14 @@ def run_split(args):
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     kd = float(np.mean(kms[0::2])) if len(kms) >= 2 else float("nan")
     kc = float(np.mean(kms[1::2])) if len(kms) >= 2 else float("nan")
-    peak = 6552.6
+    peak, peak_src = hbm_peak()
     b_alg = 8.0 * d * N + 8.0 * prob.nt
-    b_dist = 8.0 * d * N + 8.0 * N  # read points, write dist
-    b_comp = 8.0 * N + 8.0 * prob.nt  # read dist, write indices
+    b_dist = 8.0 * d * N + 1.0 * N  # k_dist_flag: read the points, write one flag byte per point
+    b_comp = 1.0 * N + 8.0 * prob.nt  # k_compact_flag: read the flags, write the target indices
     line = {"metric": "split_sources_targets points/s (pass 1)", "value": N / (ms / 1e3), "unit": "points/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "dtype": "f64", "config": {"workload": f"{args.config}: N={N}, d={d}, m={m}, N_T={prob.nt}"},
-            "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak,
+            "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
                          "achieved": b_alg / (ms / 1e3) / 1e9, "frac": b_alg / (ms / 1e3) / 1e9 / peak,
                          "algorithmic_bytes": b_alg,
                          "k_dist_cand": {"ms": kd, "gbs": b_dist / (kd / 1e3) / 1e9},
@@ -498,6 +516,7 @@ def run_next_pass(args):
     torch.cuda.set_stream(torch.cuda.Stream())
     wl = WORKLOADS[args.config]
     dev, prob = setup(wl, 1, 0, local, torch)
+    apply_options(dev, args)
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
     d, m = wl["d"], wl["m"]
@@ -568,6 +587,8 @@ def run_next_pass(args):
     launches = dev.launches - l0
     kms = dev.profile_read()
     dev.profile(False)
+    if args.pass_ in ("gram", "leverage"):
+        kern = dev.last_kernel()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     kavg = float(np.mean(kms)) if len(kms) else float("nan")
     entries = float(prob.nt) * m
@@ -766,7 +787,7 @@ def main():
     ap.add_argument("--tile-warps", type=int, default=0, help="warp-tile kernel warps per CTA (0 auto, 8, 12)")
     ap.add_argument("--tile-form", type=int, default=0, help="warp-tile kernel form: 0 auto, 1 one CTA per SM, 2 CTA pair")
     ap.add_argument("--path", type=int, default=0, help="kernel family: 0 auto, 1 always the cluster kernels")
-    ap.add_argument("--kernel", type=int, default=0, help="large-m kernel: 0 auto, 1 k_fused, 2 k_fused_w")
+    ap.add_argument("--kernel", type=int, default=0, help="kernel: 0 auto, 1 k_fused, 2 k_fused_w, 3 k_gram2 (K^T K at any m)")
     ap.add_argument("--svd-proj", action="store_true", help="--pass svd through kid_proj_gram (C = V_perp) instead of the ID route")
     ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms", "gram", "leverage"])
     args = ap.parse_args()

@@ -787,6 +787,12 @@ int fused_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, dou
   if (mode == FX_RESID && c->P2_host.size() < (size_t)std::max(r, 1) * frag_stride(n))
     return fail(c, KID_E_ERROR, "fused pass: host copy of P2 is stale");
   const int NB = (n + 7) / 8;
+  // K^T K beyond one SM's registers (m > 128): the two-phase kernel k_gram2, one CTA per SM (kid_gram2.cu);
+  // KID_OPT_KERNEL = 1 keeps the cluster kernel, 3 takes k_gram2 at any m (tests)
+  if (mode == FX_GRAM && c->kernel_choice != 1 && (m > 128 || c->kernel_choice == 3)) {
+    const int rc = gram2_dev(c, h, d_out);
+    if (rc != 1) return rc;
+  }
   // few D columns and an A part: the warp-tile kernel (kid_set_option KID_OPT_KERNEL selects explicitly)
   if (c->kernel_choice != 1 && !lev && has_A && NB <= 4) {
     const int rc = fused_w_dev(c, h, mode, Mh, n64, d_out);

@@ -60,4 +60,7 @@ int launch_fx_reduce(kid_ctx* c, const double* partial, int nchunks, int LG, int
 // the shape does not qualify
 int fused_w_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, double* d_out);
 
+// K^T K by the two-phase kernel k_gram2 (kid_gram2.cu); returns 1 when its tile buffers do not fit shared memory
+int gram2_dev(kid_ctx* c, double h, double* d_out);
+
 }  // namespace kid

@@ -115,6 +115,6 @@ def test_large_config_slice(oracle, dev, cfg, d, N, m, rows, eps):
     dev.select_rows(np.arange(rows, dtype=np.int64))
     try:
         _device_vs(O, dev, K, skel, P, t.h, r_sd, r_sk, r_DtD, r_KtK)
-        assert dev.last_kernel() == "k_fused"
+        assert dev.last_kernel() in ("k_fused", "k_gram2")  # the last pass of _device_vs: K^T K (m > 128)
     finally:
         dev.select_rows(None)

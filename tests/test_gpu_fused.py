@@ -205,16 +205,47 @@ def test_large_m_residual(oracle, dev, d, n, eps):
     assert _gram_ok(G, r_KtK)
 
 
-@pytest.mark.parametrize("d,n", [(16, 256), (8, 512)])
+@pytest.mark.parametrize("d,n", [(16, 256), (8, 512), (5, 300), (3, 129), (64, 256)])
 def test_large_m_gram_parts(oracle, dev, d, n):
-    """The m x m Gram at m = 256 / 512 does not fit one cluster's registers: several parts
-    (grid.y), each evaluating only the D columns of its blocks; every block written once."""
-    t, K = _block(oracle, d, 9_000, n, xi=1.0)
+    """The m x m Gram for m > 128 does not fit one SM's registers: parts (grid.y), each evaluating only the
+    columns of its blocks, every block written once. Both kernels -- the two-phase k_gram2 (the automatic
+    choice; d = 64 falls back to the cluster kernel: shared memory) and the warp-specialised cluster kernel
+    k_fused -- against the oracle; ragged column groups (m = 300, 129), run-to-run bitwise equality."""
+    xi = 1.0 if d < 64 else 0.0
+    t, K = _block(oracle, d, 9_000, n, xi=xi)
+    dev.set_points(t.points)
+    dev.split(t.center, n, xi)
+    ref = K.T @ K
+    try:
+        for kern in (0, 1):
+            dev.set_option(3, kern)
+            G, sk = dev.gram(t.h)
+            assert dev.last_kernel() == ("k_gram2" if kern == 0 and d < 64 else "k_fused")
+            assert _gram_ok(G, ref), kern
+            assert np.array_equal(G, G.T)
+            assert sk == pytest.approx(np.sum(K * K), rel=1e-12)
+            G2, sk2 = dev.gram(t.h)
+            assert np.array_equal(G, G2) and sk == sk2
+    finally:
+        dev.set_option(3, 0)
+
+
+@pytest.mark.parametrize("d,n,N", [(2, 100, 20_000), (3, 37, 5_000), (8, 16, 40), (16, 130, 4_000), (7, 8, 1_000), (1, 20, 3_000)])
+def test_gram2_small_and_ragged(oracle, dev, d, n, N):
+    """k_gram2 forced (KID_OPT_KERNEL = 3) on small / ragged blocks: one diagonal part with padded warp tiles,
+    fewer targets than one tile, m not a multiple of 8, generic d."""
+    t, K = _block(oracle, d, N, n, xi=1.0)
     dev.set_points(t.points)
     dev.split(t.center, n, 1.0)
-    G, sk = dev.gram(t.h)
-    ref = K.T @ K
-    assert _gram_ok(G, ref)
+    try:
+        dev.set_path(1)
+        dev.set_option(3, 3)
+        G, sk = dev.gram(t.h)
+        assert dev.last_kernel() == "k_gram2"
+    finally:
+        dev.set_option(3, 0)
+        dev.set_path(0)
+    assert _gram_ok(G, K.T @ K)
     assert np.array_equal(G, G.T)
     assert sk == pytest.approx(np.sum(K * K), rel=1e-12)
 
