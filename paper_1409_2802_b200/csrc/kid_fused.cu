@@ -794,7 +794,7 @@ int fused_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, dou
     if (rc != 1) return rc;
   }
   // few D columns and an A part: the warp-tile kernel (kid_set_option KID_OPT_KERNEL selects explicitly)
-  if (c->kernel_choice != 1 && !lev && has_A && NB <= 4) {
+  if (c->kernel_choice != 1 && !lev && has_A && NB <= 6) {
     const int rc = fused_w_dev(c, h, mode, Mh, n64, d_out);
     if (rc != 1) return rc;
   }

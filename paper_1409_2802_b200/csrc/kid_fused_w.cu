@@ -22,9 +22,11 @@ namespace {
 //   cluster the CTA pair splits the k range (M and the A sources do not fit one SM); warp w of each CTA works
 //           on the same tile and exchanges partials / final halves with its twin through per-warp mbarriers.
 constexpr int kWW = 12;  // max warps per CTA (runtime: blockDim.x / 32)
-template <bool SOLO>
-__host__ __device__ constexpr int fw_wg() { return SOLO ? 10 : 6; }  // max Gram blocks per CTA (NB <= 4: 10 upper blocks)
-constexpr int kWG = fw_wg<true>();  // glist stride
+// Gram blocks a warp accumulates: all NB (NB + 1) / 2 upper blocks (one CTA), or its CTA's half of them
+template <int NB, bool SOLO>
+__host__ __device__ constexpr int fw_wg() { return SOLO ? NB * (NB + 1) / 2 : (NB * (NB + 1) / 2 + 1) / 2; }
+constexpr int kWNB = 6;                        // D column blocks: up to 6 for the pair (n <= 48), 5 for one CTA
+constexpr int kWG = kWNB * (kWNB + 1) / 2;     // glist stride
 
 struct FwArgs {
   TargetView tv;
@@ -50,7 +52,7 @@ struct FwArgs {
 template <int D, int NB, bool SOLO, int MAXW>
 __global__ void __launch_bounds__(MAXW * 32, 1) k_fused_w(const __grid_constant__ FwArgs A) {
   constexpr int WST = 8 * kST;  // stage: 8 columns x 32 rows
-  constexpr int WG = fw_wg<SOLO>();
+  constexpr int WG = fw_wg<NB, SOLO>();
   const int d = D ? D : A.d;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int NW = (int)(blockDim.x >> 5), NT = (int)blockDim.x;
@@ -318,7 +320,8 @@ __global__ void __launch_bounds__(MAXW * 32, 1) k_fused_w(const __grid_constant_
 
 }  // namespace
 
-// The warp-tile kernel (k_fused_w) for residual / projected Grams with n <= 32 D columns and an A part.
+// The warp-tile kernel (k_fused_w) for residual / projected Grams with few D columns (n <= 40 in one CTA, n <= 48
+// for the CTA pair; at m <= 128 the caller sends n <= 32) and an A part.
 // SOLO (one CTA per SM, no exchange) where the whole coefficient matrix and all sources fit one SM's shared
 // memory; the 2-CTA cluster form (k range split over the pair) otherwise. KID_OPT_TILE_FORM forces one.
 // Returns 1 when the shape does not qualify (the caller takes k_gram / k_fused).
@@ -329,7 +332,7 @@ int fused_w_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, d
   const int a = mode == FX_RESID ? r : m;
   const bool has_B = mode == FX_RESID;
   const int NB = (n + 7) / 8;
-  if (a < 1 || NB < 1 || NB > 4 || (mode != FX_RESID && mode != FX_PROJ)) return 1;
+  if (a < 1 || NB < 1 || NB > kWNB || (mode != FX_RESID && mode != FX_PROJ)) return 1;
   const std::vector<double>& sh = mode == FX_RESID ? c->src_perm_host : c->src_host;
   if (sh.size() != (size_t)m * d) return fail(c, KID_E_ERROR, "fused pass: host copy of the sources is stale");
   if (mode == FX_RESID && c->P2_host.size() < (size_t)std::max(r, 1) * frag_stride(n))
@@ -363,11 +366,11 @@ int fused_w_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, d
   // warps per CTA: solo 12 (3 per SM sub-partition; c2-d3 r = 88: 0.274 ms against 0.298 at 8) where their tile
   // areas fit, else 8 at up to 255 registers (c5: the 168-register build of 12 warps costs 5 %); the pair 8
   auto warps_of = [&](const Geo& g) {
-    if (c->tile_warps == 8 || g.ncta == 2) return 8;
+    if (c->tile_warps == 8 || g.ncta == 2 || NB > 4) return 8;  // 5 / 6 column blocks need the 255-register build
     return smem_of(g, 12) <= kSmemMax ? 12 : 8;
   };
   Geo G = geo_of(true);
-  bool solo = c->tile_form != 2 && smem_of(G, 8) <= kSmemMax;
+  bool solo = c->tile_form != 2 && NB < kWNB && smem_of(G, 8) <= kSmemMax;  // one warp holds <= 15 Gram blocks
   if (!solo) {
     if (c->tile_form == 1) return 1;
     G = geo_of(false);
@@ -487,7 +490,9 @@ int fused_w_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, d
     case 1: FW_LAUNCH_S(DD, 1, SS, WW) break;  \
     case 2: FW_LAUNCH_S(DD, 2, SS, WW) break;  \
     case 3: FW_LAUNCH_S(DD, 3, SS, WW) break;  \
-    default: FW_LAUNCH_S(DD, 4, SS, WW) break; \
+    case 4: FW_LAUNCH_S(DD, 4, SS, WW) break;  \
+    case 5: FW_LAUNCH_S(DD, 5, SS, WW) break;  \
+    default: FW_LAUNCH_S(DD, 6, SS, WW) break; \
   }
   c->last_kernel = solo ? "k_fused_w (solo)" : "k_fused_w";
   prof_begin(c);

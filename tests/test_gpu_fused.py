@@ -132,6 +132,30 @@ def test_warp_tile_kernel(oracle, dev, d, n, r):
         assert got[1] == pytest.approx(float(np.sum(K * K)), rel=1e-12), key
 
 
+@pytest.mark.parametrize("d,n,r,form", [(16, 200, 160, "k_fused_w (solo)"), (8, 256, 210, "k_fused_w"),
+                                        (5, 150, 108, "k_fused_w"), (8, 512, 478, "k_fused_w")])
+def test_warp_tile_kernel_wide(oracle, dev, d, n, r, form):
+    """5 / 6 column blocks (33 <= n - r <= 48) at m > 128: one CTA per SM up to 40 D columns, the CTA pair up
+    to 48; against the oracle and against k_fused."""
+    t, K = _block(oracle, d, 12_000, n, xi=1.0)
+    dev.set_points(t.points)
+    dev.split(t.center, n, 1.0)
+    res = oracle.compress_id(K, np.arange(0, K.shape[0], 5), fixed_r=r)
+    _, _, r_DtD, _ = oracle.residual_stats(K, res.skeleton, res.P)
+    bound, _, _ = _resid_bound(K, res, r_DtD)
+    try:
+        got = dev.recon_error(t.h, res.skeleton, res.P)
+        assert dev.last_kernel() == form
+        dev.set_option(3, 1)
+        ref = dev.recon_error(t.h, res.skeleton, res.P)
+        assert dev.last_kernel() == "k_fused"
+    finally:
+        dev.set_option(3, 0)
+    for g in (got, ref):
+        assert np.all(np.abs(g[2] - r_DtD) <= bound + 1e-300)
+        assert g[1] == pytest.approx(float(np.sum(K * K)), rel=1e-12)
+
+
 def test_cluster_residual_rank_one_and_full(oracle, cluster):
     """rank 1 (one skeleton column: the A k-slice of CTA 1 is empty) and r = m - 1 (one D column)."""
     t, K = _block(oracle, 3, 10_000, 40)
