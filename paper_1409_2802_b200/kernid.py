@@ -23,12 +23,29 @@ _ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
 UNIFORM, BERNOULLI, EUCLIDEAN_NORM, LEVERAGE = 0, 1, 2, 4
 
 
+def _preload_nccl():
+    """libkernid_host.so needs libnccl.so.2 (kernid_multi.cpp). When PyTorch is installed, load the NCCL it
+    bundles first: the loader then binds the host library to that copy (same soname), and a later
+    `import torch` in the same process finds the symbols of its own NCCL instead of an older system one."""
+    try:
+        import glob
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for loc in (spec.submodule_search_locations if spec else []) or []:
+            for so in sorted(glob.glob(os.path.join(loc, "lib", "libnccl.so.*"))):
+                C.CDLL(so, mode=C.RTLD_GLOBAL)
+                return
+    except (ImportError, OSError, ValueError):
+        pass
+
+
 def host_lib():
     global _host
     if _host is None:
         cuda_lib()
         if not os.path.exists(HOST_SO):
             raise OSError(f"{HOST_SO} missing: run __graft_entry__.build()")
+        _preload_nccl()
         L = C.CDLL(HOST_SO)
         i64, i32, u64, dbl, P = C.c_int64, C.c_int32, C.c_uint64, C.c_double, C.POINTER
         L.kidh_last_error.restype = C.c_char_p

@@ -144,6 +144,7 @@ def test_warp_tile_kernel_wide(oracle, dev, d, n, r, form):
     _, _, r_DtD, _ = oracle.residual_stats(K, res.skeleton, res.P)
     bound, _, _ = _resid_bound(K, res, r_DtD)
     try:
+        dev.set_path(1)  # (m = 150 would otherwise fit k_gram)
         got = dev.recon_error(t.h, res.skeleton, res.P)
         assert dev.last_kernel() == form
         dev.set_option(3, 1)
@@ -151,6 +152,7 @@ def test_warp_tile_kernel_wide(oracle, dev, d, n, r, form):
         assert dev.last_kernel() == "k_fused"
     finally:
         dev.set_option(3, 0)
+        dev.set_path(0)
     for g in (got, ref):
         assert np.all(np.abs(g[2] - r_DtD) <= bound + 1e-300)
         assert g[1] == pytest.approx(float(np.sum(K * K)), rel=1e-12)

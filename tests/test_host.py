@@ -230,3 +230,12 @@ def test_host_id_vs_lapack_cpqr(H):
         assert np.max(np.abs(P[o1] - P_ref[o2])) <= 1e-13 * cond * max(1.0, np.abs(P_ref).max())
         assert np.linalg.norm(A[:, skel] @ P - A, 2) <= 10 * np.linalg.norm(A[:, piv[:r]] @ P_ref - A, 2) + 1e-14
     assert checked >= 3
+
+
+def test_host_library_then_torch_in_one_process():
+    """libkernid_host.so links NCCL (kernid_multi.cpp); loading it before PyTorch must not pin an older system
+    libnccl.so.2 under torch's feet (kernid._preload_nccl loads the copy torch bundles first)."""
+    code = ("import sys; sys.path.insert(0, %r); from paper_1409_2802_b200 import kernid as H; H.host_lib(); "
+            "import torch; import torch.distributed; print('ok', torch.distributed.is_nccl_available())" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.startswith("ok"), out.stderr[-2000:]
