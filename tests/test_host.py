@@ -8,6 +8,7 @@ No GPU is needed here.
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
