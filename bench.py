@@ -787,7 +787,7 @@ def main():
     ap.add_argument("--tile-warps", type=int, default=0, help="warp-tile kernel warps per CTA (0 auto, 8, 12)")
     ap.add_argument("--tile-form", type=int, default=0, help="warp-tile kernel form: 0 auto, 1 one CTA per SM, 2 CTA pair")
     ap.add_argument("--path", type=int, default=0, help="kernel family: 0 auto, 1 always the cluster kernels")
-    ap.add_argument("--kernel", type=int, default=0, help="kernel: 0 auto, 1 k_fused, 2 k_fused_w, 3 k_gram2 (K^T K at any m), 4 k_gram instead of k_resid3")
+    ap.add_argument("--kernel", type=int, default=0, help="kernel: 0 auto, 1 k_fused, 2 k_fused_w, 3 k_gram2 (K^T K at any m)")
     ap.add_argument("--svd-proj", action="store_true", help="--pass svd through kid_proj_gram (C = V_perp) instead of the ID route")
     ap.add_argument("--pass", dest="pass_", default="recon", choices=["recon", "split", "apply", "svd", "tsqr", "rownorms", "gram", "leverage"])
     args = ap.parse_args()

@@ -73,7 +73,7 @@ const char* kid_last_kernel(const kid_ctx* ctx);
    eval warps of 16 per CTA (the rest run the DMMA contractions). */
 #define KID_OPT_EVAL_WARPS 1
 #define KID_OPT_CHUNK_COLS 2 /* K_A chunk width: 0 (auto), 32, 48, 64, 96 */
-#define KID_OPT_KERNEL 3     /* 0 auto, 1 the warp-specialised k_fused, 2 the warp-tile k_fused_w (n <= 32), 3 k_gram2 for K^T K at any m, 4 the warp-specialised k_gram instead of k_resid3 */
+#define KID_OPT_KERNEL 3     /* 0 auto, 1 the warp-specialised k_fused, 2 the warp-tile k_fused_w (n <= 32), 3 k_gram2 for K^T K at any m */
 #define KID_OPT_TILE_WARPS 4 /* warps per CTA of k_fused_w: 0 auto (12 where shared memory allows), 8 */
 #define KID_OPT_TILE_FORM 5  /* k_fused_w form: 0 auto (one CTA per SM where M and the sources fit it), 1 solo, 2 the CTA pair */
 int kid_set_option(kid_ctx* ctx, int32_t key, int64_t value);

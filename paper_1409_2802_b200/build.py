@@ -16,7 +16,7 @@ CUDA_SO = os.path.join(PKG, "libkernid_cuda.so")
 HOST_SO = os.path.join(PKG, "libkernid_host.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SRCS = ["kid_capi.cu", "kid_split.cu", "kid_passes.cu", "kid_next.cu", "kid_fused.cu", "kid_fused_w.cu", "kid_gram2.cu", "kid_resid3.cu"]
+CU_SRCS = ["kid_capi.cu", "kid_split.cu", "kid_passes.cu", "kid_next.cu", "kid_fused.cu", "kid_fused_w.cu", "kid_gram2.cu"]
 HOST_SRCS = ["kernid_host.cpp", "kernid_multi.cpp"]
 
 

@@ -264,7 +264,7 @@ int kid_set_option(kid_ctx* c, int32_t key, int64_t value) {
     return KID_OK;
   }
   if (key == KID_OPT_KERNEL) {
-    if (value < 0 || value > 4) return fail(c, KID_E_RANGE, "kid_set_option: kernel must be 0 .. 4");
+    if (value < 0 || value > 3) return fail(c, KID_E_RANGE, "kid_set_option: kernel must be 0, 1, 2 or 3");
     c->kernel_choice = (int)value;
     return KID_OK;
   }

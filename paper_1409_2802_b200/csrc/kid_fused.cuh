@@ -63,8 +63,4 @@ int fused_w_dev(kid_ctx* c, double h, int mode, const double* Mh, int64_t n64, d
 // K^T K by the two-phase kernel k_gram2 (kid_gram2.cu); returns 1 when its tile buffers do not fit shared memory
 int gram2_dev(kid_ctx* c, double h, double* d_out);
 
-// the residual pass for 33 .. 128 D columns on one SM by the three-phase kernel k_resid3 (kid_resid3.cu); returns 1
-// when the shape does not qualify
-int resid3_dev(kid_ctx* c, double h, double* d_out);
-
 }  // namespace kid

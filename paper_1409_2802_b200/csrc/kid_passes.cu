@@ -708,11 +708,6 @@ int gram_dev(kid_ctx* c, double h, int64_t r, double* d_out) {
     const int rc = fused_w_dev(c, h, FX_RESID, nullptr, 0, d_out);
     if (rc != 1) return rc;
   }
-  // 33 .. 128 D columns on one SM: the three-phase kernel (kid_resid3.cu); KID_OPT_KERNEL = 4 keeps k_gram
-  if (r > 0 && c->kernel_choice != 1 && c->kernel_choice != 4 && c->path != KID_PATH_CLUSTER) {
-    const int rc = resid3_dev(c, h, d_out);
-    if (rc != 1) return rc;
-  }
   // upper-triangular warp tiles of WA x 2 blocks (8x16 when NBN <= 12, else 16x16), row-major,
   // as (a0, b0) block coordinates; fewer padded slots than 16x16 tiles for the small-m configs
   const int WA = NBN <= 12 ? 1 : 2;
