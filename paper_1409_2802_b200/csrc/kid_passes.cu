@@ -30,38 +30,44 @@ namespace {
 
 
 // ------------------------------------------------------------------ row norms
+// w_i = ||K_i||_2 (sampling.hpp:189-196): one thread per target, four sources at a time (four independent
+// exp chains, pre-scaled coordinates, the structure of k_sumsq), the squares summed over j in source order.
 template <int D>
 __global__ void __launch_bounds__(256) k_row_norms(TargetView tv, int d_rt, const double* __restrict__ src,
-                                                   int64_t m, double negc, double* __restrict__ w) {
+                                                   int m, double cscale, double* __restrict__ w) {
   const int d = D ? D : d_rt;
-  extern __shared__ double s_src[];  // d x m, s_src[j + k*m]
+  const int m4 = ceil_to(m, 4);
+  extern __shared__ __align__(16) double s_src[];  // d x m4 scaled sources (padding far away: K == 0)
   __shared__ double s_tab[kExpTabWords];
   stage_exp_table(s_tab, threadIdx.x, blockDim.x);
-  for (int64_t e = threadIdx.x; e < m * d; e += blockDim.x) s_src[e] = src[e];
+  for (int e = threadIdx.x; e < d * m4; e += blockDim.x) {
+    const int k = e / m4, j = e - k * m4;
+    s_src[e] = j < m ? src[j + (int64_t)k * m] * cscale : 1.0e150;
+  }
   __syncthreads();
+  const double* tabl = s_tab + (threadIdx.x & 31);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tv.nt; i += (int64_t)gridDim.x * blockDim.x) {
-    double t[D ? D : 1];
-    if (D) {
+    constexpr int DR = D ? D : 1;
+    double t[DR];
+    if constexpr (D > 0) {
 #pragma unroll
-      for (int k = 0; k < (D ? D : 1); ++k) t[k] = tcoord(tv, i, k);
+      for (int k = 0; k < D; ++k) t[k] = tcoord(tv, i, k) * cscale;
     }
     double acc = 0.0;
-    for (int64_t j = 0; j < m; ++j) {
-      double sq = 0.0;
-      if (D) {
-#pragma unroll
-        for (int k = 0; k < (D ? D : 1); ++k) {
-          const double diff = __dsub_rn(t[k], s_src[j + k * m]);
-          sq = __dadd_rn(sq, __dmul_rn(diff, diff));
-        }
-      } else {
-        for (int k = 0; k < d; ++k) {
-          const double diff = __dsub_rn(tcoord(tv, i, k), s_src[j + k * m]);
-          sq = __dadd_rn(sq, __dmul_rn(diff, diff));
-        }
+    for (int j = 0; j < m4; j += 4) {
+      double kv[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < d; ++k) {
+        const double tk = D ? t[D ? k : 0] : tcoord(tv, i, k) * cscale;
+        const double* xk = s_src + k * m4 + j;
+        const double a0 = tk - xk[0], a1 = tk - xk[1], a2 = tk - xk[2], a3 = tk - xk[3];
+        kv[0] = fma(a0, a0, kv[0]);
+        kv[1] = fma(a1, a1, kv[1]);
+        kv[2] = fma(a2, a2, kv[2]);
+        kv[3] = fma(a3, a3, kv[3]);
       }
-      const double kv = exp_fast(sq * negc, s_tab + (threadIdx.x & 31));
-      acc = __dadd_rn(acc, __dmul_rn(kv, kv));  // sequential over j (sampling.hpp:193)
+      exp_neg_fast_n<4>(kv, tabl);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = fma(kv[u], kv[u], acc);  // in source order (sampling.hpp:193)
     }
     w[i] = __dsqrt_rn(acc);
   }
@@ -592,14 +598,14 @@ int row_norms_dev(kid_ctx* c, double h, double* d_w) {
   if (int rc = check_block(c, h)) return rc;
   if (c->nt == 0) return KID_OK;
   if (int rc = init_device_tables()) return fail(c, rc, "exp table upload failed");
-  const double denom = -1.0 / (2.0 * h * h);
-  const size_t sm = sizeof(double) * c->m * c->d;
+  const double cscale = std::sqrt(1.0 / (2.0 * h * h));
+  const size_t sm = sizeof(double) * (size_t)ceil_to((int)c->m, 4) * c->d;
   if (sm > 200 * 1024) return fail(c, KID_E_DIM, "row_norms: m*d too large for shared memory");
   const int blocks = (int)std::min<int64_t>((c->nt + 255) / 256, (int64_t)c->sms * 8);
-#define LAUNCH(DD)                                                                              \
-  {                                                                                             \
-    cudaFuncSetAttribute(k_row_norms<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    k_row_norms<DD><<<blocks, 256, sm, c->stream>>>(view(c), c->d, c->src, c->m, denom, d_w);   \
+#define LAUNCH(DD)                                                                                   \
+  {                                                                                                  \
+    cudaFuncSetAttribute(k_row_norms<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
+    k_row_norms<DD><<<blocks, 256, sm, c->stream>>>(view(c), c->d, c->src, (int)c->m, cscale, d_w);  \
   }
   prof_begin(c);
   KID_DISPATCH_D(c->d, LAUNCH)
