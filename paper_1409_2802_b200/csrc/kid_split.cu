@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kCT) k_compact_flag(const unsigned char* __res
 // Device-side selection of the n sources, in two launches (the candidate count is read on the
 // device): k_split_rank -- kSelCtas CTAs each stage all <= kSelMax candidates in shared memory and
 // rank their share under (dist, idx), nth_element's comparator (geometry.hpp:40-47), by counting
-// (warp-uniform broadcast reads, no sorting network); the n of rank < n land at sel[rank]. Then
+// (one warp per candidate, no sorting network); the n of rank < n land at sel[rank]. Then
 // k_split_place (one CTA): rho = the largest of the n (geometry.hpp:52-53), the n re-ranked by index
 // (geometry.hpp:50-51), the source coordinates gathered. ctrl = [rho, fallback flag (overflow or
 // fewer than n candidates)].
@@ -464,11 +464,16 @@ __global__ void __launch_bounds__(kRankT) k_split_rank(const unsigned long long*
     idx[i] = ci[i];
   }
   __syncthreads();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+  // one warp per candidate: the lanes stride over the others (consecutive shared-memory words), the counts are
+  // summed over the warp -- cnt / 32 dependent steps per candidate instead of cnt
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nwarps = (int)(gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < cnt; i += nwarps) {
     const unsigned long long ki = key[i], ii = idx[i];
     int rank = 0;
-    for (int j = 0; j < cnt; ++j) rank += (key[j] < ki) || (key[j] == ki && idx[j] < ii);
-    if (rank < nl) {
+    for (int j = lane; j < cnt; j += 32) rank += (key[j] < ki) || (key[j] == ki && idx[j] < ii);
+    rank = __reduce_add_sync(0xffffffffu, rank);
+    if (lane == 0 && rank < nl) {
       sel[rank] = ki;
       sel[kSelT + rank] = ii;
     }
