@@ -424,13 +424,17 @@ __global__ void __launch_bounds__(kCT) k_compact_flag(const unsigned char* __res
       if (tile == ntiles - 1) *total_out = excl + total;
     }
   }
-  // stage this tile's targets in index order, then one coalesced store
-  int k = my_off;
-  unsigned bb = bits;
-  while (bb) {
-    const int j = __ffs(bb) - 1;
-    bb &= bb - 1;
-    stage[k++] = first + j;
+  // stage this tile's targets in index order, then one coalesced store. Warp-transposed: in step s the 32
+  // lanes place the 32 points of thread s (lane = bit), so a dense run lands on 32 consecutive words -- a thread
+  // writing its own 32 points put every lane on one bank (offsets 32 doubles apart: a 32-way conflict per store)
+  {
+    const int64_t wfirst = tile * kFTile + (int64_t)warp * 32 * kFIPT;
+#pragma unroll 4
+    for (int sidx = 0; sidx < 32; ++sidx) {
+      const unsigned bs = __shfl_sync(0xffffffffu, bits, sidx);
+      const int os = __shfl_sync(0xffffffffu, my_off, sidx);
+      if ((bs >> lane) & 1u) stage[os + __popc(bs & ((1u << lane) - 1u))] = wfirst + (int64_t)sidx * kFIPT + lane;
+    }
   }
   __syncthreads();
   const long long excl = excl_s;
