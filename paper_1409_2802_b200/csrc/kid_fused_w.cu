@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) k_fused_w(const __grid_constant_
   double g[WG][2];
 #pragma unroll
   for (int q = 0; q < WG; ++q) g[q][0] = g[q][1] = 0.0;
-  double sk = 0.0;
+  double skv[4] = {0.0, 0.0, 0.0, 0.0};  // ||K||^2 in four independent chains (one per column of a group)
   const int64_t tile_lo = A.ntiles * chunk / A.ncl, tile_hi = A.ntiles * (chunk + 1) / A.ncl;
   const int ngroups = acp / 4;
   int u = 0;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) k_fused_w(const __grid_constant_
       eval4(4 * gq, kv);
       if (ska) {
 #pragma unroll
-        for (int v = 0; v < 4; ++v) sk = fma(kv[v], kv[v], sk);
+        for (int v = 0; v < 4; ++v) skv[v] = fma(kv[v], kv[v], skv[v]);
       }
       double* st = stage + (gq & 1) * 4 * kST;  // two halves of the stage alternate between groups
 #pragma unroll
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) k_fused_w(const __grid_constant_
         eval4(acp + ob * 8 + 4, k1);
         if (ska) {
 #pragma unroll
-          for (int v = 0; v < 4; ++v) sk = fma(k0[v], k0[v], fma(k1[v], k1[v], sk));
+          for (int v = 0; v < 4; ++v) skv[v] = fma(k0[v], k0[v], fma(k1[v], k1[v], skv[v]));
         }
         __syncwarp();
 #pragma unroll
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) k_fused_w(const __grid_constant_
       red_g[q * 64 + 2 * lane + 1] = g[q][1];
     }
   }
-  sk = warp_sum(sk);
+  const double sk = warp_sum((skv[0] + skv[1]) + (skv[2] + skv[3]));
   if (lane == 0) red_sk[w] = sk;
   __syncthreads();
   double trw = 0.0;

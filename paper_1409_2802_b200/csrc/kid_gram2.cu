@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kG2T, 1) k_gram2(const __grid_constant__ G2Arg
     for (int i = 0; i < kG2H; ++i)
 #pragma unroll
       for (int j = 0; j < kG2H; ++j) acc[hh][i][j][0] = acc[hh][i][j][1] = 0.0;
-  double sk = 0.0;
+  double skv[4] = {0.0, 0.0, 0.0, 0.0};  // ||K||^2 in four independent chains
   const double* tabl = s_tab + (lane & (kFRep - 1));
   const int ngroups = ncolp / 4;
   const int64_t tile_lo = A.ntiles * chunk / A.nchunks, tile_hi = A.ntiles * (chunk + 1) / A.nchunks;
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kG2T, 1) k_gram2(const __grid_constant__ G2Arg
       for (int v = 0; v < 4; ++v) kt[(4 * g + v) * kST + lane] = kv[v];
       if (count) {
 #pragma unroll
-        for (int v = 0; v < 4; ++v) sk = fma(kv[v], kv[v], sk);
+        for (int v = 0; v < 4; ++v) skv[v] = fma(kv[v], kv[v], skv[v]);
       }
     }
     g2_wait_all();    // the next tile's coordinates have landed (this thread's copies; the barrier publishes them)
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kG2T, 1) k_gram2(const __grid_constant__ G2Arg
         }
   }
   trd = warp_sum(trd);
-  sk = warp_sum(sk);
+  const double sk = warp_sum((skv[0] + skv[1]) + (skv[2] + skv[3]));
   if (lane == 0) {
     red_tr[w] = trd;
     red_sk[w] = sk;

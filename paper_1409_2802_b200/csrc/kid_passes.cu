@@ -31,7 +31,7 @@ namespace {
 
 // ------------------------------------------------------------------ row norms
 // w_i = ||K_i||_2 (sampling.hpp:189-196): one thread per target, four sources at a time (four independent
-// exp chains, pre-scaled coordinates, the structure of k_sumsq), the squares summed over j in source order.
+// exp chains, pre-scaled coordinates, the structure of k_sumsq), the squares summed in four interleaved chains.
 template <int D>
 __global__ void __launch_bounds__(256) k_row_norms(TargetView tv, int d_rt, const double* __restrict__ src,
                                                    int m, double cscale, double* __restrict__ w) {
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) k_row_norms(TargetView tv, int d_rt, cons
 #pragma unroll
       for (int k = 0; k < D; ++k) t[k] = tcoord(tv, i, k) * cscale;
     }
-    double acc = 0.0;
+    double av[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains (sources j, j + 4, ... each)
     for (int j = 0; j < m4; j += 4) {
       double kv[4] = {0.0, 0.0, 0.0, 0.0};
       for (int k = 0; k < d; ++k) {
@@ -67,9 +67,9 @@ __global__ void __launch_bounds__(256) k_row_norms(TargetView tv, int d_rt, cons
       }
       exp_neg_fast_n<4>(kv, tabl);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc = fma(kv[u], kv[u], acc);  // in source order (sampling.hpp:193)
+      for (int u = 0; u < 4; ++u) av[u] = fma(kv[u], kv[u], av[u]);
     }
-    w[i] = __dsqrt_rn(acc);
+    w[i] = __dsqrt_rn((av[0] + av[1]) + (av[2] + av[3]));
   }
 }
 
