@@ -7,13 +7,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --
 mkdir -p gpurun_out/table
 python -c "
 import json; d=json.load(open('gpurun_out/r02_bench_default.json')); print(d['ms_per_step'], d['roofline']['frac'], d['e2e']['ms_per_step'], d['also']['c2-d3']['e2e'], d['also']['c2-d3']['ms_per_step'])"
-timeout 900 ncu --set full --clock-control none -k regex:"k_dist_flag|k_compact_flag|k_split_rank" -c 3 -f -o gpurun_out/r02_split_c5_final python bench.py --pass split --steps 1 --warmup 3 > gpurun_out/r02_ncu_split.log 2>&1; echo "ncu split rc=$?"
-ncu -i gpurun_out/r02_split_c5_final.ncu-rep --page raw --csv 2>/dev/null | python -c "
-import csv, sys
-rows = list(csv.reader(sys.stdin))
-h = rows[0]
-keys = ['Kernel Name', 'gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'dram__throughput.avg.pct_of_peak_sustained_elapsed', 'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum']
-idx = [h.index(k) for k in keys if k in h]
-print(', '.join(h[i] for i in idx)); print(', '.join(rows[1][i] for i in idx))
-for r in rows[2:]: print(', '.join(r[i] for i in idx))
-" > gpurun_out/r02_split_c5_final.txt 2>&1
+for p in gram rownorms; do timeout 600 python bench.py --pass $p --config c5 --steps 3 --warmup 2 > gpurun_out/table/${p}_c5.json 2>/dev/null; done
+python -c "
+import json
+for p in ('gram','rownorms'):
+    d=json.load(open('gpurun_out/table/%s_c5.json'%p)); print(p, d['ms_per_step'], d['roofline']['frac'])"
