@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
     const unsigned gmask = (unsigned)(unsigned short)el[0] | ((unsigned)(unsigned short)el[1] << 16);
     const int nKN = el[2];
     const short* itKN = el + 3;
-    double sk = 0.0;
+    double skv[4] = {0.0, 0.0, 0.0, 0.0};  // ||K||^2 in four independent chains
     const bool copier = ew < d;
     const int64_t nt = A.tv.nt;
     auto trow = [&](int tl) -> int64_t {
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
         for (int u = 0; u < 4; ++u) out[u * kST + lane] = kv[u];
         if (count) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sk = fma(kv[u], kv[u], sk);
+          for (int u = 0; u < 4; ++u) skv[u] = fma(kv[u], kv[u], skv[u]);
         }
       };
       // K_A chunks of this CTA's k-slice: this warp's 4-column groups of every 32-column chunk
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ FxArgs
       nbar_sync(kBEval, NE * 32);
     }
     if (copier) fx_wait<0>();
-    sk = warp_sum(sk);
+    const double sk = warp_sum((skv[0] + skv[1]) + (skv[2] + skv[3]));
     if (lane == 0) red_sk[ew] = sk;
   } else {
     // ================================================================ MMA warps
